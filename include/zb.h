@@ -1,0 +1,262 @@
+/*
+ * zb.h — C ABI of the B200-native Zero Bubble Pipeline Parallelism hot path
+ * (arXiv 2401.10241; PAPER.md = /root/reference/PAPER.md, cited P:<line>).
+ *
+ * The hot path (BASELINE.json north_star) is one pipeline
+ * stage of a GPT-style transformer whose backward is split into
+ *   B: input gradient   dX  = dY W        ("B")
+ *   W: weight gradient  dW += dY^T X      ("W")
+ * with F/B/W passes ordered by 1F1B / ZB-H1 / ZB-H2 or the automatic
+ * scheduler and an optimizer step with post-validation instead of
+ * a synchronous grad-norm / NaN all-reduce (App. C).
+ *
+ * Conventions (all entry points):
+ *  - Every call returns zb_status_t; 0 = ZB_OK, < 0 = error.  The message of
+ *    the last error on the calling thread is returned by zb_last_error().
+ *    No C++ exception crosses the ABI.
+ *  - The caller owns every buffer it passes; the library never frees caller
+ *    memory.  Device pointers ("dev") are CUDA device addresses on the
+ *    context's device; host pointers ("host") are ordinary CPU memory.
+ *  - Times are int64 nanoseconds (or any consistent integer unit), memory
+ *    int64 bytes, so that schedules compare exactly.
+ *  - Device work is asynchronous on the context's stream; launch errors are
+ *    returned immediately, device faults surface at zb_ctx_sync().
+ *  - Row-major layouts throughout; T = b*s tokens of one microbatch.
+ */
+#ifndef ZB_H
+#define ZB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t zb_status_t;
+enum {
+  ZB_OK = 0,
+  ZB_EINVAL = -1,  /* bad argument (sizes, pointers, family, call order)            */
+  ZB_ELIMIT = -2,  /* M_limit < M_B, or a handcrafted family's peak exceeds M_limit  */
+  ZB_ECAP = -3,    /* output capacity too small (out_cap < 3*p*m, arena too small)   */
+  ZB_ECUDA = -4,   /* CUDA runtime / launch error                                    */
+  ZB_ENCCL = -5,   /* NCCL error or libnccl unavailable                              */
+  ZB_ESTATE = -6   /* invalid state: rollback at t = 0, lr*wd == 1, missing passes   */
+};
+
+/* ------------------------------------------------------------------------ */
+/* Schedules (§2, §3.1, App. F)         */
+/* ------------------------------------------------------------------------ */
+
+enum { ZB_F = 0, ZB_B = 1, ZB_W = 2 };                         /* pass kinds */
+enum { ZB_1F1B = 0, ZB_H1 = 1, ZB_H2 = 2, ZB_AUTO = 3 };       /* families        */
+#define ZB_MAX_STAGES 64
+
+/* One pass (i, j, c) of App. F plus its stash slot and the
+ * simulator's predicted start / end (same unit as the T_* inputs). */
+typedef struct {
+  int32_t stage, microbatch, kind, slot;
+  int64_t start, end;
+} zb_pass_t;
+
+typedef struct {
+  int64_t cost;                    /* max over stages of last end - first start */
+  int64_t work;                    /* m (T_F + T_B + T_W)                               */
+  double bubble_rate;              /* (cost - work) / cost                      */
+  int64_t peak_bytes[ZB_MAX_STAGES];  /* order-based Delta-M prefix peak ((7))   */
+  int32_t n_slots[ZB_MAX_STAGES];     /* stash slots per stage (lowest free at F, freed at W) */
+  int32_t chosen;   /* AUTO: 2*fill_warmup + skip_lead (0..3), 4 = ZB-H1, 5 = ZB-H2; else -1/4/5 */
+  int32_t n_passes; /* 3 p m                                                             */
+} zb_sim_t;
+
+/* zb_schedule: build the pass lists of `family` for p stages and m
+ * microbatches.  T_F/T_B/T_W/T_comm: per-pass times (uniform across
+ * stages); M_B / M_W: activation bytes one F / one B retains (Table 1,
+ * P:95-107 as Delta-M); M_limit: per-stage activation budget
+ * (AUTO: required, >= M_B; handcrafted families: <= 0 means unchecked).
+ * out[0 .. 3pm) receives stage 0's list, then stage 1's, ... each in
+ * execution order.  1F1B is simulated with its fused backward (upstream B
+ * waits for the downstream W).  `sim` may be NULL.
+ * Errors: ZB_EINVAL (p < 1, p > 64, m < 1, negative times, bad family),
+ * ZB_ECAP (out_cap < 3pm), ZB_ELIMIT (see enum). */
+zb_status_t zb_schedule(int32_t p, int32_t m, int64_t T_F, int64_t T_B, int64_t T_W, int64_t T_comm,
+                        int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family, zb_pass_t* out,
+                        int32_t out_cap, zb_sim_t* sim);
+
+/* zb_simulate: ASAP timing (App. F constraints (4)-(6) as execution
+ * semantics) of arbitrary per-stage lists in `passes` (grouped by stage, each
+ * stage in execution order), with per-stage times T_F[p], T_B[p], T_W[p]
+ * (host arrays) — used to predict bubbles from measured pass times (§5.3).
+ * Writes start / end into passes[] and fills sim (peak_bytes from M_B/M_W).
+ * fused != 0 models 1F1B's fused backward.  ZB_ESTATE if the lists deadlock. */
+zb_status_t zb_simulate(int32_t p, int32_t m, zb_pass_t* passes, int32_t n, const int64_t* T_F,
+                        const int64_t* T_B, const int64_t* T_W, int64_t T_comm, int64_t M_B, int64_t M_W,
+                        int32_t fused, zb_sim_t* sim);
+
+/* ------------------------------------------------------------------------ */
+/* Stage context: one pipeline stage on one GPU                              */
+/* ------------------------------------------------------------------------ */
+
+enum { ZB_DTYPE_BF16 = 0, ZB_DTYPE_F32 = 1 };
+
+typedef struct {
+  int32_t h, a, L, s, b, V; /* hidden, heads, total layers, seq, microbatch, vocab */
+  int32_t p, stage;         /* this context is stage `stage` of p                               */
+  int32_t layer_first, layer_last; /* global layer range [first, last) held by the stage        */
+  int32_t m;                /* microbatches per iteration (loss = (1/m) sum of token means)     */
+  int32_t n_slots;          /* activation-stash slots (zb_sim_t.n_slots[stage])                 */
+  int32_t dtype;            /* ZB_DTYPE_BF16: tcgen05 bf16 GEMMs, f32 accumulation;             */
+                            /* ZB_DTYPE_F32: f32 everywhere (1e-5 parity mode)                   */
+  int32_t reserved;
+} zb_model_cfg_t;
+
+typedef struct zb_ctx zb_ctx_t;
+
+/* Bytes of device memory the context carves out of the caller's arena:
+ * parameters (f32 master + bf16 copy), gradients (f32), AdamW moments,
+ * n_slots stash slots (M_B per slot, §8(a) a6) and per-stage scratch. */
+zb_status_t zb_ctx_arena_bytes(const zb_model_cfg_t* cfg, size_t* bytes);
+
+/* Activation bytes one F retains until its W (= M_B = M_W of this build). */
+zb_status_t zb_ctx_slot_bytes(const zb_model_cfg_t* cfg, size_t* bytes);
+
+/* Create a context.  arena: dev buffer of >= zb_ctx_arena_bytes (256-byte
+ * aligned, owned by the caller, e.g. a torch uint8 tensor); stream: the
+ * cudaStream_t all work is enqueued on (NULL = legacy default stream). */
+zb_status_t zb_ctx_create(const zb_model_cfg_t* cfg, void* arena, size_t arena_bytes, void* stream,
+                          zb_ctx_t** out);
+zb_status_t zb_ctx_destroy(zb_ctx_t* ctx);
+/* Wait for all device work of the context; returns ZB_ECUDA on a device fault. */
+zb_status_t zb_ctx_sync(zb_ctx_t* ctx);
+
+/* Number of parameter tensors of the stage and their element counts, in the
+ * canonical order (zb_synth.param_specs: stage 0 wte, wpe; per layer ln1_g,
+ * ln1_b, qkv_w [3h,h], qkv_b, proj_w [h,h], proj_b, ln2_g, ln2_b, fc1_w
+ * [4h,h], fc1_b, fc2_w [h,4h], fc2_b; last stage lnf_g, lnf_b, head_w [V,h]). */
+zb_status_t zb_ctx_param_count(zb_ctx_t* ctx, int32_t* n);
+zb_status_t zb_ctx_param_numel(zb_ctx_t* ctx, int64_t* numel /* [n] */);
+/* Upload host f32 parameters (canonical order); resets AdamW state and t. */
+zb_status_t zb_ctx_set_params(zb_ctx_t* ctx, const float* const* host_params, int32_t n);
+/* Download f32 master parameters / accumulated f32 gradients / AdamW moments (syncs). */
+zb_status_t zb_ctx_get_params(zb_ctx_t* ctx, float* const* host_out, int32_t n);
+zb_status_t zb_ctx_get_grads(zb_ctx_t* ctx, float* const* host_out, int32_t n);
+zb_status_t zb_ctx_get_moments(zb_ctx_t* ctx, float* const* host_m, float* const* host_v, int32_t n);
+/* Start a new iteration: the first W (and first B for LayerNorm grads) of the
+ * iteration overwrites instead of accumulating; the loss accumulator resets. */
+zb_status_t zb_ctx_begin_iteration(zb_ctx_t* ctx);
+/* Sum over microbatches of the stage's loss contributions (last stage), syncs. */
+zb_status_t zb_ctx_read_loss(zb_ctx_t* ctx, double* loss);
+/* Device pointer of a slot's [T,h] input buffer (stage > 0) or its [T,h]
+ * received-gradient buffer (stage < p-1): which = 0 input, 1 gradient. */
+zb_status_t zb_ctx_slot_ptr(zb_ctx_t* ctx, int32_t slot, int32_t which, void** dev_ptr);
+
+/* F of microbatch mb into stash `slot`.  in: stage 0: dev int32
+ * tokens [T]; else dev activations [T,h] in the context dtype (copied into
+ * the slot unless it is the slot's own input buffer).  out: dev [T,h] output
+ * activations (stages < p-1; may be another context's slot input), ignored
+ * on the last stage.  labels: dev int32 [T] on the last stage (else NULL).
+ * Last stage: F ends at LN_f; the head and the loss run in its B. */
+zb_status_t zb_stage_forward(zb_ctx_t* ctx, int32_t mb, int32_t slot, const void* in, void* out,
+                             const int32_t* labels);
+/* B of microbatch mb: all input gradients, attention backward,
+ * LayerNorm parameter grads; keeps (X, dY) of the four linears in the slot
+ * for W.  dy: dev [T,h] gradient of the stage output (stages < p-1; copied
+ * into the slot unless it is the slot's own gradient buffer; NULL on the last
+ * stage).  dx: dev [T,h] gradient of the stage input (stages > 0; else NULL).
+ * Last stage: LM head + cross-entropy + head weight gradient (eager, C8). */
+zb_status_t zb_stage_backward_input(zb_ctx_t* ctx, int32_t mb, int32_t slot, const void* dy, void* dx);
+/* W of microbatch mb: dW += dY^T X for the four linears of every
+ * layer (f32 accumulation into persistent f32 grads), bias grads, and on
+ * stage 0 the embedding grads.  Frees nothing; the slot may be reused by
+ * the next F after this call. */
+zb_status_t zb_stage_backward_weight(zb_ctx_t* ctx, int32_t mb, int32_t slot);
+
+/* ------------------------------------------------------------------------ */
+/* Iterations                                                                 */
+/* ------------------------------------------------------------------------ */
+
+enum { ZB_RUN_HOST_INPUTS = 1, /* tokens / labels are host pointers: H2D inside the call */
+       ZB_RUN_TIMING = 2       /* record CUDA events at every pass boundary               */ };
+
+typedef struct {
+  int32_t n_passes;
+  float pass_start_ms[3 * 1024]; /* relative to the first pass start (ZB_RUN_TIMING)   */
+  float pass_end_ms[3 * 1024];
+  double loss;                   /* filled by zb_ctx_read_loss, not by the run calls    */
+} zb_iter_stats_t;
+
+/* Run this stage's passes (one iteration) in list order on one context.
+ * Single-GPU, single-stage (p = 1) or with an attached NCCL communicator
+ * (zb_ctx_attach_nccl) for p > 1.  tokens: int32 [m, b, s] (stage 0),
+ * labels: int32 [m, b, s] (last stage); device unless ZB_RUN_HOST_INPUTS.
+ * stats may be NULL; with ZB_RUN_TIMING it is filled at the next zb_ctx_sync
+ * / zb_ctx_read_stats. */
+zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, int32_t n, const int32_t* tokens,
+                             const int32_t* labels, int32_t flags);
+
+/* Run all p stages of one iteration in one process on one GPU ("virtual
+ * stages": SURVEY §4): ctxs[p] share the device; passes[] holds every
+ * stage's list (zb_schedule output); execution follows the simulator's
+ * predicted order, P2P replaced by device copies into the receiver's slot. */
+zb_status_t zb_run_iteration_local(zb_ctx_t* const* ctxs, int32_t p, const zb_pass_t* passes, int32_t n,
+                                   const int32_t* tokens, const int32_t* labels, int32_t flags);
+
+/* Per-pass event times of the last ZB_RUN_TIMING run (syncs). */
+zb_status_t zb_ctx_read_stats(zb_ctx_t* ctx, zb_iter_stats_t* stats);
+
+/* ------------------------------------------------------------------------ */
+/* Optimizer with post-validation (§4, App. C)   */
+/* ------------------------------------------------------------------------ */
+
+enum { ZB_OPT_SYNC = 0, ZB_OPT_PV = 1 };
+enum { ZB_ACT_NONE = 0, ZB_ACT_STEP = 1, ZB_ACT_SKIP = 2, ZB_ACT_DEFER = 3, ZB_ACT_ROLLBACK = 4,
+       ZB_ACT_ROLLBACK_REDO = 5, ZB_ACT_DEFERRED_STEP = 6, ZB_ACT_CLIPPED_STEP = 7 };
+
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay, clip;
+  int32_t mode; /* ZB_OPT_SYNC or ZB_OPT_PV */
+} zb_optim_cfg_t;
+
+typedef struct {
+  double local_sumsq, partial_sumsq, full_sumsq;
+  int32_t local_nonfinite, partial_nonfinite, full_nonfinite;
+  int32_t first_action, final_action; /* ZB_ACT_*                         */
+  int32_t t;                          /* AdamW time stamp after the call  */
+} zb_pv_report_t;
+
+/* One optimizer step of the stage(s).  Single context (p = 1): local state
+ * = partial = full; in ZB_OPT_PV mode the step is taken optimistically and
+ * validated by zb_post_validate_finish.  With an attached NCCL communicator
+ * the partial state (sum of squares, non-finite flag) is received from
+ * stage-1, combined and sent to stage+1 before the predicated step (no host
+ * synchronisation; the decision is made on the device).  All device side. */
+zb_status_t zb_post_validate_step(zb_ctx_t* ctx, const zb_optim_cfg_t* cfg);
+/* Validation with the fully reduced state (received from stage+1, forwarded
+ * to stage-1): nothing, rollback (Algorithm 1), rollback + clipped redo, or
+ * the deferred clipped step, predicated on the device. */
+zb_status_t zb_post_validate_finish(zb_ctx_t* ctx, const zb_optim_cfg_t* cfg);
+/* p contexts of one process (virtual stages): the partial chain 1 -> p, the
+ * per-stage predicated steps, then the full state p -> 1 and validation. */
+zb_status_t zb_post_validate_local(zb_ctx_t* const* ctxs, int32_t p, const zb_optim_cfg_t* cfg);
+/* Report of the last step / validation (syncs). */
+zb_status_t zb_ctx_read_pv_report(zb_ctx_t* ctx, zb_pv_report_t* rep);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU: one process per GPU, NCCL P2P over NVLink       */
+/* ------------------------------------------------------------------------ */
+
+/* 128-byte ncclUniqueId, created on rank 0 and broadcast by the caller
+ * (torch.distributed).  ZB_ENCCL if libnccl.so.2 cannot be loaded. */
+zb_status_t zb_nccl_unique_id(void* id128);
+/* Attach a communicator (rank = stage, world = p) used by zb_run_iteration
+ * for activation / gradient send-recv on two side streams and by the
+ * post-validation chain. */
+zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* id128, int32_t rank, int32_t world);
+
+const char* zb_last_error(void);
+const char* zb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZB_H */

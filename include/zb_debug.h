@@ -1,0 +1,42 @@
+/*
+ * zb_debug.h — kernel-level entry points of libzb used by the parity tests
+ * (tests/test_gpu_kernels.py).  Same conventions as zb.h: device pointers,
+ * the caller owns every buffer, work is enqueued on `stream` (cudaStream_t,
+ * NULL = default), errors are returned as zb_status_t with zb_last_error().
+ * They expose the exact kernels the stage passes launch, so each can be
+ * checked against the oracle in isolation.
+ */
+#ifndef ZB_DEBUG_H
+#define ZB_DEBUG_H
+#include "zb.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* GEMM of the F / B / W contractions:
+ *   C[m,n] (op)= sum_k A(m,k) B(n,k),
+ *   A(m,k) = a_mn ? A[k*lda + m] : A[m*lda + k]   (a_mn: A stored [K, M])
+ *   B(n,k) = b_mn ? B[k*ldb + n] : B[n*ldb + k]   (b_mn: B stored [K, N])
+ * dtype ZB_DTYPE_BF16: A, B bf16 (tcgen05 kernel), activation outputs bf16;
+ * ZB_DTYPE_F32: everything f32 (SIMT kernel).
+ * epi: 0 C = acc (+bias); 1 C = acc + bias, aux = GeLU(C); 2 C = aux + acc (+bias);
+ *      3 C = acc * GeLU'(aux); 4 C(f32) = acc + (beta ? C : 0); 5 C(f32) = acc.
+ * N and ldc must be multiples of 8; operands 16-byte aligned. */
+zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn,
+                        const void* B, int64_t ldb, int32_t b_mn, int32_t epi, void* C, int64_t ldc,
+                        const float* bias, void* aux, int64_t ldaux, int32_t beta, void* stream);
+
+/* Causal multi-head attention forward on a packed qkv [b*s, 3h] (Q, K, V
+ * column blocks, head k at columns k*d of each): o [b*s, h], lse [b, a, s] f32. */
+zb_status_t zb_dbg_attention_fwd(int32_t dtype, int32_t b, int32_t s, int32_t a, int32_t d, const void* qkv,
+                                 void* o, float* lse, void* stream);
+/* Attention backward: dqkv [b*s, 3h] from qkv, o, do, lse; delta: f32 scratch [b, a, s]. */
+zb_status_t zb_dbg_attention_bwd(int32_t dtype, int32_t b, int32_t s, int32_t a, int32_t d, const void* qkv,
+                                 const void* o, const void* dout, const float* lse, void* dqkv, float* delta,
+                                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,139 @@
+// extern "C" entry points: errors, version, zb_schedule, zb_simulate.
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "abi_util.h"
+#include "zb_sched.h"
+#include "zb.h"
+
+namespace zb {
+thread_local std::string g_last_error;
+}
+
+extern "C" const char* zb_last_error(void) { return zb::g_last_error.c_str(); }
+extern "C" const char* zb_version(void) { return "zb-b200 0.1 (sm_100a)"; }
+
+using namespace zb;
+
+static zb_status_t fill(const sched::Lists& lists, const std::vector<int64_t>& tf, const std::vector<int64_t>& tb,
+                        const std::vector<int64_t>& tw, int64_t Tcomm, bool fused, int64_t MB, int64_t MW, int chosen,
+                        zb_pass_t* out, int32_t out_cap, zb_sim_t* sim) {
+  const int p = static_cast<int>(lists.size());
+  size_t n = 0;
+  for (auto& o : lists) n += o.size();
+  if (out != nullptr && static_cast<size_t>(out_cap) < n) return set_error(ZB_ECAP, "out_cap < 3*p*m");
+  sched::SimResult r = sched::simulate(lists, tf, tb, tw, Tcomm, fused);
+  std::vector<int> counts;
+  auto slots = sched::assign_slots(lists, &counts);
+  auto peaks = sched::memory_peaks(lists, MB, MW);
+  if (out != nullptr) {
+    size_t k = 0;
+    for (int s = 0; s < p; ++s)
+      for (size_t i = 0; i < lists[s].size(); ++i) {
+        zb_pass_t& q = out[k++];
+        q.stage = s;
+        q.microbatch = lists[s][i].j;
+        q.kind = lists[s][i].kind;
+        q.slot = slots[s][i];
+        q.start = r.start[s][i];
+        q.end = r.end[s][i];
+      }
+  }
+  if (sim != nullptr) {
+    std::memset(sim, 0, sizeof(*sim));
+    sim->cost = r.cost;
+    sim->work = r.work;
+    sim->bubble_rate = r.bubble_rate;
+    for (int s = 0; s < p; ++s) {
+      sim->peak_bytes[s] = peaks[s];
+      sim->n_slots[s] = counts[s];
+    }
+    sim->chosen = chosen;
+    sim->n_passes = static_cast<int32_t>(n);
+  }
+  return ZB_OK;
+}
+
+extern "C" zb_status_t zb_schedule(int32_t p, int32_t m, int64_t T_F, int64_t T_B, int64_t T_W, int64_t T_comm,
+                                   int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family, zb_pass_t* out,
+                                   int32_t out_cap, zb_sim_t* sim) {
+  ZB_TRY {
+    if (p < 1 || p > ZB_MAX_STAGES || m < 1) return set_error(ZB_EINVAL, "need 1 <= p <= 64 and m >= 1");
+    if (T_F < 0 || T_B < 0 || T_W < 0 || T_comm < 0 || M_B < 0 || M_W < 0)
+      return set_error(ZB_EINVAL, "times and memory must be >= 0");
+    if (out != nullptr && static_cast<int64_t>(out_cap) < 3LL * p * m) return set_error(ZB_ECAP, "out_cap < 3*p*m");
+    sched::Lists lists;
+    int chosen = -1;
+    bool fused = false;
+    switch (family) {
+      case ZB_1F1B: lists = sched::build_1f1b(p, m); fused = true; break;
+      case ZB_H1: lists = sched::build_zbh1(p, m); chosen = 4; break;
+      case ZB_H2: lists = sched::build_zbh2(p, m); chosen = 5; break;
+      case ZB_AUTO:
+        if (M_limit < M_B) return set_error(ZB_ELIMIT, "AUTO needs M_limit >= M_B");
+        lists = sched::auto_schedule(p, m, T_F, T_B, T_W, T_comm, M_B, M_W, M_limit, &chosen);
+        break;
+      default: return set_error(ZB_EINVAL, "unknown family");
+    }
+    if (family != ZB_AUTO && M_limit > 0) {
+      auto pk = sched::memory_peaks(lists, M_B, M_W);
+      if (*std::max_element(pk.begin(), pk.end()) > M_limit)
+        return set_error(ZB_ELIMIT, "family peak memory exceeds M_limit");
+    }
+    std::vector<int64_t> tf(p, T_F), tb(p, T_B), tw(p, T_W);
+    return fill(lists, tf, tb, tw, T_comm, fused, M_B, M_W, chosen, out, out_cap, sim);
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_simulate(int32_t p, int32_t m, zb_pass_t* passes, int32_t n, const int64_t* T_F,
+                                   const int64_t* T_B, const int64_t* T_W, int64_t T_comm, int64_t M_B, int64_t M_W,
+                                   int32_t fused, zb_sim_t* sim) {
+  ZB_TRY {
+    if (p < 1 || p > ZB_MAX_STAGES || m < 1 || passes == nullptr || n != 3 * p * m || !T_F || !T_B || !T_W)
+      return set_error(ZB_EINVAL, "zb_simulate: bad arguments");
+    sched::Lists lists(p);
+    for (int i = 0; i < n; ++i) {
+      const zb_pass_t& q = passes[i];
+      if (q.stage < 0 || q.stage >= p || q.microbatch < 0 || q.microbatch >= m || q.kind < 0 || q.kind > 2)
+        return set_error(ZB_EINVAL, "zb_simulate: pass out of range");
+      lists[q.stage].push_back({q.kind, q.microbatch});
+    }
+    for (auto& o : lists)
+      if (static_cast<int>(o.size()) != 3 * m) return set_error(ZB_EINVAL, "zb_simulate: each stage needs 3m passes");
+    std::vector<int64_t> tf(T_F, T_F + p), tb(T_B, T_B + p), tw(T_W, T_W + p);
+    sched::SimResult r;
+    try {
+      r = sched::simulate(lists, tf, tb, tw, T_comm, fused != 0);
+    } catch (const std::runtime_error& e) {
+      return set_error(ZB_ESTATE, e.what());
+    }
+    // write times back in the caller's order
+    std::vector<size_t> pos(p, 0);
+    for (int i = 0; i < n; ++i) {
+      int s = passes[i].stage;
+      passes[i].start = r.start[s][pos[s]];
+      passes[i].end = r.end[s][pos[s]];
+      ++pos[s];
+    }
+    std::vector<int> counts;
+    sched::assign_slots(lists, &counts);
+    auto peaks = sched::memory_peaks(lists, M_B, M_W);
+    if (sim) {
+      std::memset(sim, 0, sizeof(*sim));
+      sim->cost = r.cost;
+      sim->work = r.work;
+      sim->bubble_rate = r.bubble_rate;
+      for (int s = 0; s < p; ++s) {
+        sim->peak_bytes[s] = peaks[s];
+        sim->n_slots[s] = counts[s];
+      }
+      sim->chosen = -1;
+      sim->n_passes = n;
+    }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}

@@ -1,0 +1,405 @@
+// tcgen05 / TMEM / TMA bf16 GEMM for the F, B and W contractions, plus the
+// SIMT f32 GEMM of the parity mode.  See gemm.h for the operand conventions.
+//
+// bf16 kernel (one CTA per SM, persistent, warp-specialised):
+//   warp 0     TMA producer: 128x64 A tile + BNx64 B tile per stage, 128B swizzle,
+//              K-major boxes {64, rows} or MN-major boxes {64, 64}
+//   warp 1     MMA issuer: tcgen05.mma.cta_group::1.kind::f16 128xBNx16, f32
+//              accumulator in TMEM, double-buffered (2 x BN columns)
+//   warp 2     TMEM allocator
+//   warps 4-7  epilogue: tcgen05.ld 32x32b.x32 -> fused epilogue -> global
+// The smem ring (full/empty mbarriers) overlaps TMA with MMA; the TMEM ring
+// (tfull/tempty) overlaps a tile's epilogue with the next tile's MMAs.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm.h"
+#include "sm100.cuh"
+
+namespace zb {
+
+// ------------------------------------------------------------------ epilogue
+template <int EPI, typename TO>
+__device__ __forceinline__ void epi8(const EpiArgs& e, int64_t row, int col, float* v) {
+  if (EPI == EPI_F32_STORE || EPI == EPI_F32_ACC) {
+    float* c = reinterpret_cast<float*>(e.C) + row * e.ldc + col;
+    if (EPI == EPI_F32_ACC && e.beta) {
+      float o[8];
+      Vec8<float>::load(c, o);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] += o[i];
+    }
+    Vec8<float>::store(c, v);
+    return;
+  }
+  if (EPI != EPI_GELU_BWD && e.bias != nullptr) {
+    float b[8];
+    Vec8<float>::load(e.bias + col, b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += b[i];
+  }
+  TO* c = reinterpret_cast<TO*>(e.C) + row * e.ldc + col;
+  if (EPI == EPI_STORE) {
+    Vec8<TO>::store(c, v);
+  } else if (EPI == EPI_BIAS_GELU) {
+    Vec8<TO>::store(c, v);
+    float g[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] = gelu_f(v[i]);
+    Vec8<TO>::store(reinterpret_cast<TO*>(e.aux) + row * e.ldaux + col, g);
+  } else if (EPI == EPI_RESID) {
+    float r[8];
+    Vec8<TO>::load(reinterpret_cast<const TO*>(e.aux) + row * e.ldaux + col, r);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] += r[i];
+    Vec8<TO>::store(c, v);
+  } else if (EPI == EPI_GELU_BWD) {
+    float u[8];
+    Vec8<TO>::load(reinterpret_cast<const TO*>(e.aux) + row * e.ldaux + col, u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f(u[i]);
+    Vec8<TO>::store(c, v);
+  }
+}
+
+// ------------------------------------------------------------------ tcgen05 kernel
+namespace tc {
+constexpr int BM = 128, BK = 64;
+constexpr int A_BYTES = BM * BK * 2;
+template <int BN> struct Cfg {
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN >= 256) ? 4 : 6;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mt, int& nt) {
+  constexpr int G = 8;  // group of 8 M-tiles swept across N for L2 reuse
+  int per_group = G * num_n;
+  int group = t / per_group;
+  int first_m = group * G;
+  int gm = min(num_m - first_m, G);
+  int r = t % per_group;
+  mt = first_m + r % gm;
+  nt = r / gm;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI, typename TO>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const EpiArgs ep,
+              int M, int N, int K) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&tfull[i], 1);
+      sm100::mbar_init(&tempty[i], 128);
+    }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+  }
+  if (warp == 2) sm100::tmem_alloc<C::TMEM_COLS>(tslot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n, nk = (K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int mt, nt;
+        tile_coords(t, num_m, num_n, mt, nt);
+        const int m0 = mt * BM, n0 = nt * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          sm100::mbar_wait(&empty[stage], ph ^ 1);
+          sm100::mbar_arrive_expect_tx(&full[stage], C::STAGE);
+          uint8_t* sa = smem + stage * C::STAGE;
+          uint8_t* sb = sa + A_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            sm100::tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+          } else {
+            sm100::tma_load_2d(sa, &tmA, &full[stage], m0, k0);
+            sm100::tma_load_2d(sa + 8192, &tmA, &full[stage], m0 + 64, k0);
+          }
+          if (!B_MN) {
+            sm100::tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i) sm100::tma_load_2d(sb + i * 8192, &tmB, &full[stage], n0 + 64 * i, k0);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = sm100::idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        sm100::mbar_wait(&tempty[acc], aph ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d = tbase + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          sm100::mbar_wait(&full[stage], ph);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_addr(smem + stage * C::STAGE);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? sm100::smem_desc(sa + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
+                                     : sm100::smem_desc(sa + kk * 32, 16, 1024, sm100::kSwizzle128B);
+            const uint64_t bd = B_MN ? sm100::smem_desc(sb + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
+                                     : sm100::smem_desc(sb + kk * 32, 16, 1024, sm100::kSwizzle128B);
+            sm100::mma_bf16_ss(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          sm100::mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+        sm100::mma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      int mt, nt;
+      tile_coords(t, num_m, num_n, mt, nt);
+      const int64_t row = static_cast<int64_t>(mt) * BM + ew * 32 + lane;
+      sm100::mbar_wait(&tfull[acc], aph);
+      sm100::tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        sm100::tmem_ld32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        sm100::tmem_ld_wait();
+        const int col0 = nt * BN + c * 32;
+        if (row < M) {
+          float* v = reinterpret_cast<float*>(r);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (col0 + g * 8 < N) epi8<EPI, TO>(ep, row, col0 + g * 8, v + g * 8);
+        }
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 2) sm100::tmem_dealloc<C::TMEM_COLS>(tbase);
+}
+}  // namespace tc
+
+// ------------------------------------------------------------------ SIMT f32 kernel
+namespace simt {
+constexpr int BT = 64, BKK = 16;
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(64) k_gemm_f32(const float* __restrict__ A, int64_t lda, const float* __restrict__ B,
+                                                 int64_t ldb, const EpiArgs ep, int M, int N, int K) {
+  __shared__ float As[BKK][BT + 4];
+  __shared__ float Bs[BKK][BT + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * BT, n0 = blockIdx.x * BT;
+  const int tr = tid / 8, tcol = tid % 8;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += BKK) {
+    for (int e = tid; e < BT * BKK; e += 64) {
+      int mm, kk;
+      if (A_MN) { mm = e % BT; kk = e / BT; } else { kk = e % BKK; mm = e / BKK; }
+      int gm = m0 + mm, gk = k0 + kk;
+      float a = 0.f;
+      if (gm < M && gk < K) a = A_MN ? A[static_cast<int64_t>(gk) * lda + gm] : A[static_cast<int64_t>(gm) * lda + gk];
+      As[kk][mm] = a;
+      int nn;
+      if (B_MN) { nn = e % BT; kk = e / BT; } else { kk = e % BKK; nn = e / BKK; }
+      int gn = n0 + nn;
+      gk = k0 + kk;
+      float b = 0.f;
+      if (gn < N && gk < K) b = B_MN ? B[static_cast<int64_t>(gk) * ldb + gn] : B[static_cast<int64_t>(gn) * ldb + gk];
+      Bs[kk][nn] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BKK; ++kk) {
+      float a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = As[kk][tr * 8 + i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = Bs[kk][tcol * 8 + j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const int col = n0 + tcol * 8;
+  if (col >= N) return;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int64_t row = m0 + tr * 8 + i;
+    if (row < M) epi8<EPI, float>(ep, row, col, acc[i]);
+  }
+}
+}  // namespace simt
+
+// ------------------------------------------------------------------ host side
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    ZB_CUDA(cudaGetDevice(&dev));
+    ZB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [outer, inner] view with leading dim ld.
+static CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                             uint32_t box_outer) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15))
+    throw CudaError("gemm: operand must be 16-byte aligned with a 16-byte multiple row pitch");
+  CUtensorMap tm;
+  cuuint64_t gdim[2] = {inner, outer};
+  cuuint64_t gstride[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return tm;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static void launch_tc(const GemmArgs& g, cudaStream_t st) {
+  using C = tc::Cfg<BN>;
+  auto kern = tc::k_gemm_tc<BN, A_MN, B_MN, EPI, bf16>;
+  static bool attr = false;
+  if (!attr) {
+    ZB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CUtensorMap ta = A_MN ? make_tmap(g.A, g.M, g.K, g.lda, 64, 64) : make_tmap(g.A, g.K, g.M, g.lda, 64, tc::BM);
+  CUtensorMap tb = B_MN ? make_tmap(g.B, g.N, g.K, g.ldb, 64, 64) : make_tmap(g.B, g.K, g.N, g.ldb, 64, BN);
+  const int tiles = static_cast<int>(ceil_div(g.M, tc::BM) * ceil_div(g.N, BN));
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, 256, C::SMEM, st>>>(ta, tb, g.ep, g.M, g.N, g.K);
+  ZB_LAUNCH_CHECK();
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static void dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
+  switch (g.epi) {
+    case EPI_STORE: return launch_tc<BN, A_MN, B_MN, EPI_STORE>(g, st);
+    case EPI_BIAS_GELU: return launch_tc<BN, A_MN, B_MN, EPI_BIAS_GELU>(g, st);
+    case EPI_RESID: return launch_tc<BN, A_MN, B_MN, EPI_RESID>(g, st);
+    case EPI_GELU_BWD: return launch_tc<BN, A_MN, B_MN, EPI_GELU_BWD>(g, st);
+    case EPI_F32_ACC: return launch_tc<BN, A_MN, B_MN, EPI_F32_ACC>(g, st);
+    case EPI_F32_STORE: return launch_tc<BN, A_MN, B_MN, EPI_F32_STORE>(g, st);
+  }
+  throw CudaError("gemm: bad epilogue");
+}
+
+template <int BN>
+static void dispatch_major_tc(const GemmArgs& g, cudaStream_t st) {
+  if (!g.a_mn && !g.b_mn) return dispatch_epi_tc<BN, false, false>(g, st);
+  if (!g.a_mn && g.b_mn) return dispatch_epi_tc<BN, false, true>(g, st);
+  if (g.a_mn && g.b_mn) return dispatch_epi_tc<BN, true, true>(g, st);
+  return dispatch_epi_tc<BN, true, false>(g, st);
+}
+
+template <bool A_MN, bool B_MN>
+static void dispatch_epi_f32(const GemmArgs& g, cudaStream_t st) {
+  dim3 grid(static_cast<unsigned>(ceil_div(g.N, simt::BT)), static_cast<unsigned>(ceil_div(g.M, simt::BT)));
+  const float* A = static_cast<const float*>(g.A);
+  const float* B = static_cast<const float*>(g.B);
+  switch (g.epi) {
+#define ZB_F32_CASE(E) \
+  case E: simt::k_gemm_f32<A_MN, B_MN, E><<<grid, 64, 0, st>>>(A, g.lda, B, g.ldb, g.ep, g.M, g.N, g.K); break;
+    ZB_F32_CASE(EPI_STORE)
+    ZB_F32_CASE(EPI_BIAS_GELU)
+    ZB_F32_CASE(EPI_RESID)
+    ZB_F32_CASE(EPI_GELU_BWD)
+    ZB_F32_CASE(EPI_F32_ACC)
+    ZB_F32_CASE(EPI_F32_STORE)
+#undef ZB_F32_CASE
+    default: throw CudaError("gemm: bad epilogue");
+  }
+  ZB_LAUNCH_CHECK();
+}
+
+void gemm(const GemmArgs& g, DType dt, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
+  if (g.N % 8 != 0 || g.ep.ldc % 8 != 0) throw CudaError("gemm: N and ldc must be multiples of 8");
+  if (dt == DT_F32) {
+    if (!g.a_mn && !g.b_mn) return dispatch_epi_f32<false, false>(g, st);
+    if (!g.a_mn && g.b_mn) return dispatch_epi_f32<false, true>(g, st);
+    if (g.a_mn && g.b_mn) return dispatch_epi_f32<true, true>(g, st);
+    return dispatch_epi_f32<true, false>(g, st);
+  }
+  if (g.N <= 128)
+    dispatch_major_tc<128>(g, st);
+  else
+    dispatch_major_tc<256>(g, st);
+}
+
+}  // namespace zb

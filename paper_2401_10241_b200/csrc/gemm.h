@@ -1,0 +1,57 @@
+// GEMM entry used by the stage passes (F, B and W contractions).
+//
+//   C[m, n] (op)= sum_k A(m, k) * B(n, k)
+//   A(m, k) = a_mn ? A[k * lda + m] : A[m * lda + k]
+//   B(n, k) = b_mn ? B[k * ldb + n] : B[n * ldb + k]
+//
+// F:  Y  = X  W^T   A = X  [T, n_in]  K-major,  B = W [n_out, n_in] K-major
+// B:  dX = dY W     A = dY [T, n_out] K-major,  B = W [n_out, n_in] MN-major
+// W:  dW += dY^T X  A = dY [T, n_out] MN-major, B = X [T, n_in]     MN-major
+//
+// bf16 mode runs the tcgen05 / TMEM / TMA kernel (gemm.cu); f32 mode (the
+// 1e-5 parity mode of BASELINE.json) runs a SIMT FFMA kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace zb {
+
+enum Epi : int32_t {
+  EPI_STORE = 0,      // C = acc (+ bias)                       (activation dtype)
+  EPI_BIAS_GELU = 1,  // C = acc + bias; aux = GeLU(acc + bias) (activation dtype)
+  EPI_RESID = 2,      // C = aux + acc (+ bias)                 (activation dtype)
+  EPI_GELU_BWD = 3,   // C = acc * GeLU'(aux)                   (activation dtype; C may alias aux)
+  EPI_F32_ACC = 4,    // C(f32) = acc + (beta ? C : 0)
+  EPI_F32_STORE = 5,  // C(f32) = acc
+};
+
+struct EpiArgs {
+  void* C;
+  int64_t ldc;
+  const float* bias;
+  void* aux;
+  int64_t ldaux;
+  int32_t beta;
+};
+
+struct GemmArgs {
+  int32_t M, N, K;
+  const void* A;
+  int64_t lda;
+  bool a_mn;
+  const void* B;
+  int64_t ldb;
+  bool b_mn;
+  int32_t epi;
+  EpiArgs ep;
+};
+
+// Throws zb::CudaError on launch failure / unsupported shapes.
+void gemm(const GemmArgs& g, DType dt, cudaStream_t stream);
+
+// number of SMs of the current device (cached)
+int num_sms();
+
+}  // namespace zb
