@@ -36,6 +36,14 @@ zb_status_t zb_dbg_attention_bwd(int32_t dtype, int32_t b, int32_t s, int32_t a,
                                  const void* o, const void* dout, const float* lse, void* dqkv, float* delta,
                                  void* stream);
 
+/* Kernel-class timing used by bench.py for the live roofline numbers: when
+ * enabled, every GEMM / attention launch is bracketed by CUDA events on its
+ * stream and its algorithmic FLOPs are recorded.  Classes: 0 all GEMMs,
+ * 1 attention forward, 2 attention backward, 3 F GEMMs (X W^T), 4 B GEMMs
+ * (dY W), 5 W GEMMs (dY^T X).  read() synchronises the pending events. */
+zb_status_t zb_dbg_kernel_timing(int32_t enable, int32_t reset);
+zb_status_t zb_dbg_kernel_timing_read(int32_t cls, double* total_ms, double* total_flops, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

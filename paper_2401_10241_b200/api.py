@@ -1,11 +1,18 @@
-"""Thin Python wrappers over include/zb.h (marshalling only; no compute here)."""
+"""Thin Python wrappers over include/zb.h (marshalling only; no compute here).
+
+torch provides device memory (the context arena) and streams; every step of
+the hot path runs in libzb.so's kernels.
+"""
 from __future__ import annotations
 
 import ctypes as C
 from typing import Dict, List, Optional, Sequence, Tuple
 
-from ._lib import (FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, check, lib, zb_model_cfg_t, zb_optim_cfg_t, zb_pass_t,
-                   zb_pv_report_t, zb_sim_t, zb_iter_stats_t)
+import numpy as np
+
+from ._lib import (FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING,
+                   ACTIONS, check, lib, zb_iter_stats_t, zb_model_cfg_t, zb_optim_cfg_t, zb_pass_t, zb_pv_report_t,
+                   zb_sim_t)
 
 KIND_NAME = {0: "F", 1: "B", 2: "W"}
 
@@ -30,6 +37,14 @@ def stage_lists(passes, p: int) -> List[List[Tuple[str, int]]]:
     return lists
 
 
+def stage_passes(passes, stage: int):
+    sel = [q for q in passes if q.stage == stage]
+    arr = (zb_pass_t * len(sel))()
+    for i, q in enumerate(sel):
+        arr[i] = q
+    return arr
+
+
 def simulate(p: int, m: int, lists: Sequence[Sequence[Tuple[str, int]]], T_F, T_B, T_W, T_comm: int = 0,
              M_B: int = 1, M_W: int = 1, fused: bool = False):
     kinds = {"F": 0, "B": 1, "W": 2}
@@ -47,7 +62,7 @@ def simulate(p: int, m: int, lists: Sequence[Sequence[Tuple[str, int]]], T_F, T_
     return arr, sim
 
 
-# ------------------------------------------------------------------ kernels (debug entry points)
+# ------------------------------------------------------------------ helpers
 
 def _ptr(t) -> Optional[int]:
     return None if t is None else t.data_ptr()
@@ -60,9 +75,164 @@ def _stream(stream) -> Optional[int]:
     return stream
 
 
+# ------------------------------------------------------------------ stage context
+
+def model_cfg(cfg, p: int, stage: int, m: int, n_slots: int, dtype: str = "bf16") -> zb_model_cfg_t:
+    from zb_synth import stage_layers
+    first, last = stage_layers(cfg.L, p, stage)
+    return zb_model_cfg_t(cfg.h, cfg.a, cfg.L, cfg.s, cfg.b, cfg.V, p, stage, first, last, m, n_slots,
+                          ZB_DTYPE_BF16 if dtype == "bf16" else ZB_DTYPE_F32, 0)
+
+
+def arena_bytes(mc: zb_model_cfg_t) -> int:
+    n = C.c_size_t()
+    check(lib.zb_ctx_arena_bytes(C.byref(mc), C.byref(n)))
+    return n.value
+
+
+def slot_bytes(mc: zb_model_cfg_t) -> int:
+    n = C.c_size_t()
+    check(lib.zb_ctx_slot_bytes(C.byref(mc), C.byref(n)))
+    return n.value
+
+
+class Context:
+    """One pipeline stage (zb_ctx_t) with a torch-allocated device arena."""
+
+    def __init__(self, cfg, p: int, stage: int, m: int, n_slots: int, dtype: str = "bf16", stream=None):
+        import torch
+        self.cfg, self.p, self.stage, self.m, self.dtype = cfg, p, stage, m, dtype
+        self.mc = model_cfg(cfg, p, stage, m, n_slots, dtype)
+        self.nbytes = arena_bytes(self.mc)
+        self.arena = torch.empty(self.nbytes, dtype=torch.uint8, device="cuda")
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        h = C.c_void_p()
+        check(lib.zb_ctx_create(C.byref(self.mc), self.arena.data_ptr(), self.nbytes, self.stream.cuda_stream,
+                                C.byref(h)))
+        self.h = h
+        n = C.c_int32()
+        check(lib.zb_ctx_param_count(self.h, C.byref(n)))
+        self.n_params = n.value
+        numel = (C.c_int64 * self.n_params)()
+        check(lib.zb_ctx_param_numel(self.h, numel))
+        self.numel = list(numel)
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib.zb_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # parameters -------------------------------------------------------------
+    def set_params(self, arrays: Sequence[np.ndarray]):
+        arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in arrays]
+        assert len(arrs) == self.n_params, (len(arrs), self.n_params)
+        for a, n in zip(arrs, self.numel):
+            assert a.size == n, (a.shape, n)
+        ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        check(lib.zb_ctx_set_params(self.h, ptrs, len(arrs)))
+
+    def _get(self, fn) -> List[np.ndarray]:
+        outs = [np.empty(n, dtype=np.float32) for n in self.numel]
+        ptrs = (C.c_void_p * len(outs))(*[a.ctypes.data for a in outs])
+        check(fn(self.h, ptrs, len(outs)))
+        return outs
+
+    def get_params(self):
+        return self._get(lib.zb_ctx_get_params)
+
+    def get_grads(self):
+        return self._get(lib.zb_ctx_get_grads)
+
+    def get_moments(self):
+        ms = [np.empty(n, dtype=np.float32) for n in self.numel]
+        vs = [np.empty(n, dtype=np.float32) for n in self.numel]
+        pm = (C.c_void_p * len(ms))(*[a.ctypes.data for a in ms])
+        pv = (C.c_void_p * len(vs))(*[a.ctypes.data for a in vs])
+        check(lib.zb_ctx_get_moments(self.h, pm, pv, len(ms)))
+        return ms, vs
+
+    # passes -----------------------------------------------------------------
+    def begin_iteration(self):
+        check(lib.zb_ctx_begin_iteration(self.h))
+
+    def slot_ptr(self, slot: int, which: int) -> int:
+        p = C.c_void_p()
+        check(lib.zb_ctx_slot_ptr(self.h, slot, which, C.byref(p)))
+        return p.value
+
+    def forward(self, mb, slot, inp: int, out: Optional[int] = None, labels: Optional[int] = None):
+        check(lib.zb_stage_forward(self.h, mb, slot, inp, out, labels))
+
+    def backward_input(self, mb, slot, dy: Optional[int] = None, dx: Optional[int] = None):
+        check(lib.zb_stage_backward_input(self.h, mb, slot, dy, dx))
+
+    def backward_weight(self, mb, slot):
+        check(lib.zb_stage_backward_weight(self.h, mb, slot))
+
+    def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False):
+        flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0)
+        tp = tokens.ctypes.data if host_inputs and tokens is not None else _ptr(tokens)
+        lp = labels.ctypes.data if host_inputs and labels is not None else _ptr(labels)
+        check(lib.zb_run_iteration(self.h, passes, len(passes), tp, lp, flags))
+
+    def sync(self):
+        check(lib.zb_ctx_sync(self.h))
+
+    def loss(self) -> float:
+        v = C.c_double()
+        check(lib.zb_ctx_read_loss(self.h, C.byref(v)))
+        return v.value
+
+    def stats(self):
+        st = zb_iter_stats_t()
+        check(lib.zb_ctx_read_stats(self.h, C.byref(st)))
+        n = st.n_passes
+        return list(st.pass_start_ms[:n]), list(st.pass_end_ms[:n])
+
+    # optimizer --------------------------------------------------------------
+    def post_validate_step(self, opt: zb_optim_cfg_t):
+        check(lib.zb_post_validate_step(self.h, C.byref(opt)))
+
+    def post_validate_finish(self, opt: zb_optim_cfg_t):
+        check(lib.zb_post_validate_finish(self.h, C.byref(opt)))
+
+    def pv_report(self) -> Dict:
+        r = zb_pv_report_t()
+        check(lib.zb_ctx_read_pv_report(self.h, C.byref(r)))
+        return dict(local_sumsq=r.local_sumsq, partial_sumsq=r.partial_sumsq, full_sumsq=r.full_sumsq,
+                    local_nonfinite=r.local_nonfinite, partial_nonfinite=r.partial_nonfinite,
+                    full_nonfinite=r.full_nonfinite, first=ACTIONS[r.first_action], final=ACTIONS[r.final_action],
+                    t=r.t)
+
+
+def optim_cfg(lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, clip=1.0, mode="pv") -> zb_optim_cfg_t:
+    return zb_optim_cfg_t(lr, beta1, beta2, eps, weight_decay, clip, ZB_OPT_PV if mode == "pv" else ZB_OPT_SYNC)
+
+
+def run_local(ctxs: Sequence[Context], passes, tokens, labels, host_inputs=False, timing=False):
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0)
+    tp = tokens.ctypes.data if host_inputs else _ptr(tokens)
+    lp = labels.ctypes.data if host_inputs else _ptr(labels)
+    check(lib.zb_run_iteration_local(arr, len(ctxs), passes, len(passes), tp, lp, flags))
+
+
+def post_validate_local(ctxs: Sequence[Context], opt: zb_optim_cfg_t):
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    check(lib.zb_post_validate_local(arr, len(ctxs), C.byref(opt)))
+
+
+# ------------------------------------------------------------------ kernels (debug entry points)
+
 def dbg_gemm(A, B, C_out, *, M, N, K, a_mn=False, b_mn=False, epi=0, bias=None, aux=None, beta=0,
              lda=None, ldb=None, ldc=None, ldaux=None, stream=None):
-    dtype = ZB_DTYPE_F32 if A.dtype.is_floating_point and A.element_size() == 4 else ZB_DTYPE_BF16
+    dtype = ZB_DTYPE_F32 if A.element_size() == 4 else ZB_DTYPE_BF16
     lda = lda if lda is not None else A.shape[-1]
     ldb = ldb if ldb is not None else B.shape[-1]
     ldc = ldc if ldc is not None else C_out.shape[-1]

@@ -1,6 +1,8 @@
 // Kernel-level extern "C" entry points (include/zb_debug.h) for the parity tests.
 #include "abi_util.h"
+#include "attention.h"
 #include "gemm.h"
+#include "ktimer.h"
 #include "zb_debug.h"
 
 using namespace zb;
@@ -25,3 +27,58 @@ extern "C" zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t 
   ZB_CATCH
 }
 
+
+extern "C" zb_status_t zb_dbg_attention_fwd(int32_t dtype, int32_t b, int32_t s, int32_t a, int32_t d,
+                                            const void* qkv, void* o, float* lse, void* stream) {
+  ZB_TRY {
+    if (dtype != ZB_DTYPE_BF16 && dtype != ZB_DTYPE_F32) return set_error(ZB_EINVAL, "bad dtype");
+    AttnShape sh{b, s, a, d};
+    attention_fwd(sh, static_cast<DType>(dtype), qkv, o, lse, static_cast<cudaStream_t>(stream));
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_dbg_attention_bwd(int32_t dtype, int32_t b, int32_t s, int32_t a, int32_t d,
+                                            const void* qkv, const void* o, const void* dout, const float* lse,
+                                            void* dqkv, float* delta, void* stream) {
+  ZB_TRY {
+    if (dtype != ZB_DTYPE_BF16 && dtype != ZB_DTYPE_F32) return set_error(ZB_EINVAL, "bad dtype");
+    AttnShape sh{b, s, a, d};
+    attention_bwd(sh, static_cast<DType>(dtype), qkv, o, dout, lse, dqkv, delta, static_cast<cudaStream_t>(stream));
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_dbg_kernel_timing(int32_t enable, int32_t reset) {
+  ZB_TRY {
+    if (reset) ktimer::reset();
+    ktimer::set_enabled(enable != 0);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_dbg_kernel_timing_read(int32_t cls, double* total_ms, double* total_flops,
+                                                 int64_t* launches) {
+  ZB_TRY {
+    if (cls < 0 || cls >= ktimer::N_CLASSES || !total_ms || !total_flops || !launches)
+      return set_error(ZB_EINVAL, "bad kernel timing query");
+    if (cls == 0) {  // all GEMMs = F + B + W classes
+      double ms = 0, fl = 0;
+      int64_t n = 0;
+      for (int c : {ktimer::GEMM_F, ktimer::GEMM_B, ktimer::GEMM_W}) {
+        double a, b;
+        int64_t k;
+        ktimer::read(c, &a, &b, &k);
+        ms += a; fl += b; n += k;
+      }
+      *total_ms = ms; *total_flops = fl; *launches = n;
+    } else {
+      ktimer::read(cls, total_ms, total_flops, launches);
+    }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}

@@ -13,8 +13,11 @@
 #include <math.h>
 
 #include "attention.h"
+#include "ktimer.h"
 
 namespace zb {
+void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const void* o, const void* dout,
+                        const float* lse, void* dqkv, float* delta, cudaStream_t st);
 namespace attn {
 
 constexpr int TILE = 64;
@@ -575,18 +578,30 @@ static void bwd_f32(const AttnShape& sh, const void* qkv, const void* dout, cons
 
 void attention_fwd(const AttnShape& sh, DType dt, const void* qkv, void* o, float* lse, cudaStream_t st) {
   if (sh.b <= 0 || sh.s <= 0 || sh.a <= 0) return;
+  // algorithmic causal FLOPs: Q K^T and P V over the lower triangle
+  const int tk = ktimer::start(ktimer::ATTN_FWD, 2.0 * sh.b * sh.a * static_cast<double>(sh.s) * sh.s * sh.d, st);
   switch (sh.d) {
-    case 64: return dt == DT_BF16 ? attn::fwd_bf16<64>(sh, qkv, o, lse, st) : attn::fwd_f32<64>(sh, qkv, o, lse, st);
-    case 96: return dt == DT_BF16 ? attn::fwd_bf16<96>(sh, qkv, o, lse, st) : attn::fwd_f32<96>(sh, qkv, o, lse, st);
+    case 64: dt == DT_BF16 ? attn::fwd_bf16<64>(sh, qkv, o, lse, st) : attn::fwd_f32<64>(sh, qkv, o, lse, st); break;
+    case 96: dt == DT_BF16 ? attn::fwd_bf16<96>(sh, qkv, o, lse, st) : attn::fwd_f32<96>(sh, qkv, o, lse, st); break;
     case 128:
-      return dt == DT_BF16 ? attn::fwd_bf16<128>(sh, qkv, o, lse, st) : attn::fwd_f32<128>(sh, qkv, o, lse, st);
+      dt == DT_BF16 ? attn::fwd_bf16<128>(sh, qkv, o, lse, st) : attn::fwd_f32<128>(sh, qkv, o, lse, st);
+      break;
+    default: throw CudaError("attention: head dim must be 64, 96 or 128");
   }
-  throw CudaError("attention: head dim must be 64, 96 or 128");
+  ktimer::stop(tk, st);
 }
 
 void attention_bwd(const AttnShape& sh, DType dt, const void* qkv, const void* o, const void* dout, const float* lse,
                    void* dqkv, float* delta, cudaStream_t st) {
   if (sh.b <= 0 || sh.s <= 0 || sh.a <= 0) return;
+  // algorithmic causal FLOPs of the five backward products (recomputation not counted)
+  const int tk = ktimer::start(ktimer::ATTN_BWD, 5.0 * sh.b * sh.a * static_cast<double>(sh.s) * sh.s * sh.d, st);
+  attention_bwd_impl(sh, dt, qkv, o, dout, lse, dqkv, delta, st);
+  ktimer::stop(tk, st);
+}
+
+void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const void* o, const void* dout,
+                        const float* lse, void* dqkv, float* delta, cudaStream_t st) {
   const int rows = sh.b * sh.s;
   const int warps = rows * sh.a;
   const int blocks = (warps * 32 + 255) / 256;

@@ -1,0 +1,56 @@
+// NCCL P2P transport between adjacent pipeline stages (one process per GPU).
+//
+// libnccl.so.2 is loaded lazily with dlopen (the single-GPU path never needs
+// it).  Every adjacent pair (s, s+1) gets two 2-rank communicators: one for
+// activations s -> s+1 and one for gradients s+1 -> s (separate
+// directions never head-of-line block each other); each communicator is
+// driven by its own stream on each side, and its message order is the
+// microbatch order of the passes that produce / consume it, which is the same
+// on both ends for every schedule (F and B lists are microbatch-monotone).
+// The post-validation partial state rides the activation channel (after the
+// iteration's last activation) and the full state rides the gradient channel
+// (before the next iteration's first gradient).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "zb.h"
+
+namespace zb {
+
+struct Ctx;
+
+struct Comm {
+  int rank = 0, world = 1;
+  // [0] activations to stage+1, [1] activations from stage-1,
+  // [2] gradients to stage-1,   [3] gradients from stage+1   (nullptr where absent)
+  void* comm[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t stream[4] = {nullptr, nullptr, nullptr, nullptr};
+  // send staging ring for activations (written by F, drained by the act-send stream)
+  std::vector<void*> act_buf;
+  std::vector<cudaEvent_t> act_buf_free;
+  int act_next = 0;
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_next = 0;
+  void* scalars = nullptr;  // 2 x 16 B device buffer for PV messages
+  ~Comm();
+  cudaEvent_t event();
+};
+
+// ncclGetUniqueId through dlopen'ed libnccl (128 bytes).
+void nccl_unique_id(void* id128);
+// ids: 2*(world-1) unique ids, [k] for the activation comm of pair (k, k+1),
+// [world-1+k] for the gradient comm of the same pair.
+void attach_nccl(Ctx& c, const void* ids, int rank, int world);
+// One iteration of this stage's passes with NCCL send / recv.
+void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* tokens, const int32_t* labels,
+                        int flags);
+// Post-validation chain messages over the attached communicators.
+void pv_recv_partial(Ctx& c);
+void pv_send_partial(Ctx& c);
+void pv_recv_full(Ctx& c);
+void pv_send_full(Ctx& c);
+
+}  // namespace zb

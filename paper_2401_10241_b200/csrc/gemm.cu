@@ -15,6 +15,7 @@
 #include <mutex>
 
 #include "gemm.h"
+#include "ktimer.h"
 #include "sm100.cuh"
 
 namespace zb {
@@ -390,16 +391,19 @@ static void dispatch_epi_f32(const GemmArgs& g, cudaStream_t st) {
 void gemm(const GemmArgs& g, DType dt, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
   if (g.N % 8 != 0 || g.ep.ldc % 8 != 0) throw CudaError("gemm: N and ldc must be multiples of 8");
+  const int cls = g.a_mn ? ktimer::GEMM_W : (g.b_mn ? ktimer::GEMM_B : ktimer::GEMM_F);
+  const int tk = ktimer::start(cls, 2.0 * g.M * g.N * static_cast<double>(g.K), st);
   if (dt == DT_F32) {
-    if (!g.a_mn && !g.b_mn) return dispatch_epi_f32<false, false>(g, st);
-    if (!g.a_mn && g.b_mn) return dispatch_epi_f32<false, true>(g, st);
-    if (g.a_mn && g.b_mn) return dispatch_epi_f32<true, true>(g, st);
-    return dispatch_epi_f32<true, false>(g, st);
-  }
-  if (g.N <= 128)
+    if (!g.a_mn && !g.b_mn) dispatch_epi_f32<false, false>(g, st);
+    else if (!g.a_mn && g.b_mn) dispatch_epi_f32<false, true>(g, st);
+    else if (g.a_mn && g.b_mn) dispatch_epi_f32<true, true>(g, st);
+    else dispatch_epi_f32<true, false>(g, st);
+  } else if (g.N <= 128) {
     dispatch_major_tc<128>(g, st);
-  else
+  } else {
     dispatch_major_tc<256>(g, st);
+  }
+  ktimer::stop(tk, st);
 }
 
 }  // namespace zb

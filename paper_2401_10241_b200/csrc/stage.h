@@ -1,0 +1,108 @@
+// Stage context: one pipeline stage on one GPU (include/zb.h zb_ctx_t).
+//
+// Arena layout (all carved from one caller-owned device buffer, 256-B aligned):
+//   params   f32 master theta, f32 grads, f32 AdamW m / v (flat; matrices and
+//            embeddings first = the weight-decay region; linear matrices first
+//            of all = the bf16 shadow region), bf16 shadow (bf16 mode)
+//   slots    n_slots x stash slot: per layer X, LN1, QKV, O,
+//            X1, LN2, U, G [T, *] + f32 stats; per slot DY [T,h], tokens,
+//            labels; last stage XL, LNF [T,h]
+//   scratch  spare QKV [T,3h] (pointer-swapped with a slot's QKV in B),
+//            dO / dLN [T,h], attention delta, column-sum partials, logits f32
+//            [T,V] + dlogits [T,V] (last stage), loss rows, sort keys,
+//            token / label staging [m,T], optimizer scratch.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "ops.h"
+#include "zb.h"
+
+namespace zb {
+
+struct Comm;  // NCCL transport (comm.cpp)
+
+struct LayerW {
+  float *ln1_g, *ln1_b, *qkv_b, *proj_b, *ln2_g, *ln2_b, *fc1_b, *fc2_b;  // f32 master
+  void *qkv_w, *proj_w, *fc1_w, *fc2_w;                                  // compute copies
+  float *g_ln1_g, *g_ln1_b, *g_qkv_b, *g_proj_b, *g_ln2_g, *g_ln2_b, *g_fc1_b, *g_fc2_b;
+  float *g_qkv_w, *g_proj_w, *g_fc1_w, *g_fc2_w;
+};
+
+struct LayerAct {
+  void *x, *ln1, *qkv, *o, *x1, *ln2, *u, *g;
+  float *mu1, *rs1, *mu2, *rs2, *lse;
+};
+
+struct Slot {
+  std::vector<LayerAct> L;
+  void* dy;
+  void* xl;
+  void* lnf;
+  float *muf, *rsf;
+  int32_t* tok;
+  int32_t* lab;
+};
+
+struct ParamRef {
+  int64_t off, numel;
+};
+
+struct Ctx {
+  zb_model_cfg_t cfg{};
+  DType dt = DT_BF16;
+  size_t esz = 2;
+  cudaStream_t stream = nullptr;
+  int T = 0, h = 0, a = 0, d = 0, Ls = 0, V = 0, s = 0, b = 0;
+  bool first = false, last = false;
+
+  // parameters (flat)
+  int64_t n_total = 0, n_wd = 0, n_shadow = 0;
+  float *theta = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
+  bf16* shadow = nullptr;
+  std::vector<ParamRef> params;  // canonical order
+  std::vector<LayerW> lw;
+  float *wte = nullptr, *wpe = nullptr, *lnf_g = nullptr, *lnf_b = nullptr;
+  void* head_w = nullptr;
+  float *g_wte = nullptr, *g_wpe = nullptr, *g_lnf_g = nullptr, *g_lnf_b = nullptr, *g_head_w = nullptr;
+
+  // stash and scratch
+  std::vector<Slot> slots;
+  void *spare_qkv = nullptr, *d_o = nullptr, *d_ln = nullptr, *dlogits = nullptr;
+  float *delta = nullptr, *part_a = nullptr, *part_b = nullptr, *logits = nullptr, *loss_rows = nullptr;
+  uint32_t* keys = nullptr;
+  int32_t *tok_stage = nullptr, *lab_stage = nullptr;
+  double* loss_acc = nullptr;
+  double* norm_part = nullptr;
+  int32_t* nf_part = nullptr;
+  PvState* pv = nullptr;
+
+  bool first_b_done = false, first_w_done = false;
+
+  // timing (ZB_RUN_TIMING)
+  std::vector<cudaEvent_t> ev_start, ev_end;
+  int n_timed = 0;
+
+  std::unique_ptr<Comm> comm;
+
+  ~Ctx();
+
+  // passes
+  void forward(int mb, int slot, const void* in, void* out, const int32_t* labels);
+  void backward_input(int mb, int slot, const void* dy, void* dx);
+  void backward_weight(int mb, int slot);
+
+  void timing_begin(int idx);
+  void timing_end(int idx);
+};
+
+// arena sizing / carving (base == nullptr: size only)
+size_t carve(Ctx& c, uint8_t* base);
+size_t slot_bytes(const zb_model_cfg_t& cfg);
+void validate_cfg(const zb_model_cfg_t& cfg);
+
+}  // namespace zb

@@ -1,0 +1,236 @@
+"""GPU parity of whole stage passes F / B / W and iterations through the C-ABI
+against the fp64 oracle (oracle/model.py) on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): f32 mode normwise relative
+error <= 1e-5 for the loss and every gradient; bf16 mode (bf16 operands,
+f32 accumulation) <= 2e-2 per tensor and <= 1e-2 mean over tensors.  Schedules
+must produce bitwise-identical gradients."""
+import numpy as np
+import pytest
+
+import zb_synth
+from zbtest_util import cuda_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA GPU")]
+
+SHAPES = {
+    "d64": zb_synth.ModelConfig("d64", h=64, a=1, L=4, s=256, b=2, V=512, p=4, m=3, family="zbh1"),
+    "d96": zb_synth.ModelConfig("d96", h=192, a=2, L=2, s=128, b=2, V=264, p=2, m=2, family="zbh1"),
+    "d128": zb_synth.ModelConfig("d128", h=256, a=2, L=2, s=192, b=1, V=512, p=2, m=2, family="zbh1"),
+}
+MATRICES = ("qkv_w", "proj_w", "fc1_w", "fc2_w", "head_w")
+
+
+def rel(x, ref):
+    return float(np.linalg.norm(np.ravel(x) - np.ravel(ref)) / max(np.linalg.norm(ref), 1e-30))
+
+
+def inputs(cfg, it=0):
+    tok = zb_synth.make_tokens(cfg, it)
+    return np.ascontiguousarray(tok[..., :cfg.s]), np.ascontiguousarray(tok[..., 1:])
+
+
+def make_ctxs(cfg, p, dtype, family="zbh1", n_slots=None):
+    from paper_2401_10241_b200 import api
+    passes, sim = api.schedule(family, p, cfg.m, 10, 11, 6, 0, M_limit=2 * p * 10 if family == "auto" else 0,
+                               M_B=10, M_W=10)
+    ctxs = []
+    for s in range(p):
+        c = api.Context(cfg, p, s, cfg.m, max(1, sim.n_slots[s]), dtype=dtype)
+        params = zb_synth.make_stage_params(cfg, p, s)
+        c.set_params([params[n] for n, _, _ in zb_synth.param_specs(cfg, p, s)])
+        ctxs.append(c)
+    return ctxs, passes
+
+
+def oracle_grads(cfg, dtype):
+    from oracle import model as om
+    params = zb_synth.make_model_params(cfg)
+    if dtype == "bf16":
+        params = {k: (zb_synth.round_to_bf16(v) if k.endswith(MATRICES) else v) for k, v in params.items()}
+    tok = zb_synth.make_tokens(cfg, 0)
+    return om.reference_iteration(cfg, params, tok)
+
+
+def gpu_run(cfg, p, dtype, family="zbh1"):
+    import torch
+    from paper_2401_10241_b200 import api
+    ctxs, passes = make_ctxs(cfg, p, dtype, family)
+    tok, lab = inputs(cfg)
+    tok_d = torch.from_numpy(tok).cuda()
+    lab_d = torch.from_numpy(lab).cuda()
+    if p == 1:
+        ctxs[0].run_iteration(passes, tok_d, lab_d)
+    else:
+        api.run_local(ctxs, passes, tok_d, lab_d)
+    loss = ctxs[-1].loss()
+    grads = {}
+    for s, c in enumerate(ctxs):
+        for (name, shape, _), g in zip(zb_synth.param_specs(cfg, p, s), c.get_grads()):
+            grads[name] = g.reshape(shape)
+    return loss, grads, ctxs
+
+
+def check_tolerance(loss, grads, ref_loss, ref_grads, dtype):
+    errs = {k: rel(grads[k], ref_grads[k]) for k in ref_grads}
+    if dtype == "f32":
+        assert abs(loss - ref_loss) <= 1e-5 * abs(ref_loss)
+        bad = {k: e for k, e in errs.items() if e > 1e-5}
+        assert not bad, bad
+    else:
+        assert abs(loss - ref_loss) <= 2e-2 * abs(ref_loss)
+        bad = {k: e for k, e in errs.items() if e > 2e-2}
+        assert not bad, bad
+        assert np.mean(list(errs.values())) <= 1e-2
+    return errs
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("shape", list(SHAPES))
+def test_single_stage_iteration_vs_oracle(shape, dtype):
+    cfg = SHAPES[shape]
+    ref_loss, ref = oracle_grads(cfg, dtype)
+    loss, grads, _ = gpu_run(cfg, 1, dtype)
+    check_tolerance(loss, grads, ref_loss, ref, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_virtual_stages_bitwise_across_schedules(dtype):
+    """identical results across 1F1B / ZB-H1 / ZB-H2 / AUTO (and p = 1)."""
+    cfg = SHAPES["d64"].with_(m=5)
+    base_loss, base, _ = gpu_run(cfg, 1, dtype)
+    for fam in ("1f1b", "zbh1", "zbh2", "auto"):
+        loss, grads, _ = gpu_run(cfg, 4, dtype, fam)
+        assert loss == base_loss, fam
+        for k in base:
+            assert np.array_equal(grads[k], base[k]), (fam, k)
+
+
+def test_tiny_config_c1_vs_oracle_f32():
+    """BASELINE.json configs[0]: tiny 8-layer stack, h 64, p 4, m 8, ZB-H1 vs 1F1B."""
+    cfg = zb_synth.CONFIGS["tiny"]
+    ref_loss, ref = oracle_grads(cfg, "f32")
+    for fam in ("zbh1", "1f1b"):
+        loss, grads, _ = gpu_run(cfg, 4, "f32", fam)
+        check_tolerance(loss, grads, ref_loss, ref, "f32")
+
+
+def test_tiny_config_c1_vs_oracle_bf16():
+    cfg = zb_synth.CONFIGS["tiny"]
+    ref_loss, ref = oracle_grads(cfg, "bf16")
+    loss, grads, _ = gpu_run(cfg, 4, "bf16", "zbh1")
+    check_tolerance(loss, grads, ref_loss, ref, "bf16")
+
+
+def test_pass_api_and_input_copies():
+    """zb_stage_forward / backward_input / backward_weight called directly with
+    caller buffers (copied into the slot) equal the runner (zb_run_iteration_local)."""
+    import torch
+    from paper_2401_10241_b200 import api
+    cfg = SHAPES["d64"].with_(m=2)
+    _, ref, _ = gpu_run(cfg, 2, "f32")
+    ctxs, passes = make_ctxs(cfg, 2, "f32")
+    tok, lab = inputs(cfg)
+    tok_d = torch.from_numpy(tok).cuda()
+    lab_d = torch.from_numpy(lab).cuda()
+    T, h = cfg.T, cfg.h
+    act = torch.empty(T, h, device="cuda")
+    grad = torch.empty(T, h, device="cuda")
+    for c in ctxs:
+        c.begin_iteration()
+    slot = [{q.microbatch: q.slot for q in passes if q.stage == s and q.kind == 0} for s in range(2)]
+    for j in range(cfg.m):
+        ctxs[0].forward(j, slot[0][j], tok_d[j].data_ptr(), act.data_ptr())
+        ctxs[1].forward(j, slot[1][j], act.data_ptr(), None, lab_d[j].data_ptr())
+        ctxs[1].backward_input(j, slot[1][j], None, grad.data_ptr())
+        ctxs[0].backward_input(j, slot[0][j], grad.data_ptr(), None)
+        ctxs[1].backward_weight(j, slot[1][j])
+        ctxs[0].backward_weight(j, slot[0][j])
+    for s, c in enumerate(ctxs):
+        for (name, shape, _), g in zip(zb_synth.param_specs(cfg, 2, s), c.get_grads()):
+            assert np.array_equal(g.reshape(shape), ref[name]), name
+
+
+def test_host_inputs_equal_device_inputs():
+    from paper_2401_10241_b200 import api
+    cfg = SHAPES["d64"].with_(m=2)
+    loss_d, ref, _ = gpu_run(cfg, 1, "bf16")
+    ctxs, passes = make_ctxs(cfg, 1, "bf16")
+    tok, lab = inputs(cfg)
+    ctxs[0].run_iteration(passes, tok, lab, host_inputs=True)
+    assert ctxs[0].loss() == loss_d
+    for (name, shape, _), g in zip(zb_synth.param_specs(cfg, 1, 0), ctxs[0].get_grads()):
+        assert np.array_equal(g.reshape(shape), ref[name])
+
+
+# ------------------------------------------------------------------ optimizer + post-validation
+
+def _params_of(ctxs, cfg, p):
+    out = {}
+    for s, c in enumerate(ctxs):
+        for (name, shape, _), v in zip(zb_synth.param_specs(cfg, p, s), c.get_params()):
+            out[name] = v.reshape(shape)
+    return out
+
+
+@pytest.mark.parametrize("clip_mode", ["none", "stage0-rollback", "all-defer"])
+def test_post_validation_vs_sync_and_oracle(clip_mode):
+    from oracle import optim as oo
+    from paper_2401_10241_b200 import api
+    cfg = SHAPES["d64"]
+    p = 4
+    _, g_all, ctx_sync = gpu_run(cfg, p, "f32")
+    _, _, ctx_pv = gpu_run(cfg, p, "f32")
+    # stage-local squared norms decide which path each stage takes
+    loc = [sum(float(np.sum(g.astype(np.float64) ** 2)) for g in c.get_grads()) for c in ctx_sync]
+    clip = {"none": 1e6, "stage0-rollback": float(np.sqrt(loc[0])) * 1.001,
+            "all-defer": float(np.sqrt(loc[0])) * 0.5}[clip_mode]
+    hyp = dict(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, clip=clip)
+    api.post_validate_local(ctx_sync, api.optim_cfg(mode="sync", **hyp))
+    api.post_validate_local(ctx_pv, api.optim_cfg(mode="pv", **hyp))
+    reps = [c.pv_report() for c in ctx_pv]
+    if clip_mode == "none":
+        assert [r["first"] for r in reps] == ["step"] * p and [r["final"] for r in reps] == ["none"] * p
+    elif clip_mode == "stage0-rollback":
+        assert reps[0]["first"] == "step" and reps[0]["final"] == "rollback+redo"
+        assert all(r["first"] == "defer" and r["final"] == "deferred-step" for r in reps[1:])
+    else:
+        assert all(r["first"] == "defer" and r["final"] == "deferred-step" for r in reps)
+    assert all(r["t"] == 1 for r in reps)
+    ps, pp = _params_of(ctx_sync, cfg, p), _params_of(ctx_pv, cfg, p)
+    for k in ps:
+        if clip_mode == "stage0-rollback" and k in {n for n, _, _ in zb_synth.param_specs(cfg, p, 0)}:
+            assert rel(pp[k], ps[k]) < 1e-6, k       # rounding of the f32 inverse step
+        else:
+            assert np.array_equal(pp[k], ps[k]), k   # clean / deferred paths: bitwise
+    # the synchronous GPU step against Algorithm 1 in fp64 on the same gradients
+    theta0 = zb_synth.make_model_params(cfg)
+    S = sum(loc)
+    coef = min(1.0, clip / (np.sqrt(S) + 1e-6))
+    for k, v in ps.items():
+        wd = 0.1 if theta0[k].ndim >= 2 else 0.0
+        want, _, _, _ = oo.adamw_step(theta0[k].astype(np.float64), 0.0, 0.0, 0, g_all[k].astype(np.float64) * coef,
+                                      1e-3, 0.9, 0.95, 1e-8, wd)
+        assert rel(v, want) < 1e-6, k
+
+
+def test_nan_skips_step_everywhere():
+    from paper_2401_10241_b200 import api
+    cfg = SHAPES["d64"]
+    p = 2
+    ctxs, passes = make_ctxs(cfg, p, "f32")
+    params = zb_synth.make_stage_params(cfg, p, 1)
+    lst = [params[n] for n, _, _ in zb_synth.param_specs(cfg, p, 1)]
+    lst[0] = lst[0].copy()
+    lst[0][0] = np.nan                      # stage 1's first LayerNorm gain
+    ctxs[1].set_params(lst)
+    import torch
+    tok, lab = inputs(cfg)
+    api.run_local(ctxs, passes, torch.from_numpy(tok).cuda(), torch.from_numpy(lab).cuda())
+    before = [c.get_params() for c in ctxs]
+    api.post_validate_local(ctxs, api.optim_cfg(mode="pv", lr=1e-3))
+    for c, b in zip(ctxs, before):
+        r = c.pv_report()
+        assert r["full_nonfinite"] == 1 and r["t"] == 0
+        for x, y in zip(c.get_params(), b):
+            assert np.array_equal(x, y, equal_nan=True)
