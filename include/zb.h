@@ -146,8 +146,9 @@ zb_status_t zb_ctx_get_moments(zb_ctx_t* ctx, float* const* host_m, float* const
 zb_status_t zb_ctx_begin_iteration(zb_ctx_t* ctx);
 /* Sum over microbatches of the stage's loss contributions (last stage), syncs. */
 zb_status_t zb_ctx_read_loss(zb_ctx_t* ctx, double* loss);
-/* Device pointer of a slot's [T,h] input buffer (stage > 0) or its [T,h]
- * received-gradient buffer (stage < p-1): which = 0 input, 1 gradient. */
+/* Device pointer of a slot's [T,h] input buffer (stage > 0, context dtype)
+ * or its [T,h] f32 received-gradient buffer (stage < p-1): which = 0 input,
+ * 1 gradient. */
 zb_status_t zb_ctx_slot_ptr(zb_ctx_t* ctx, int32_t slot, int32_t which, void** dev_ptr);
 
 /* F of microbatch mb into stash `slot`.  in: stage 0: dev int32
@@ -160,9 +161,11 @@ zb_status_t zb_stage_forward(zb_ctx_t* ctx, int32_t mb, int32_t slot, const void
                              const int32_t* labels);
 /* B of microbatch mb: all input gradients, attention backward,
  * LayerNorm parameter grads; keeps (X, dY) of the four linears in the slot
- * for W.  dy: dev [T,h] gradient of the stage output (stages < p-1; copied
- * into the slot unless it is the slot's own gradient buffer; NULL on the last
- * stage).  dx: dev [T,h] gradient of the stage input (stages > 0; else NULL).
+ * for W.  Gradients that cross stages are f32 in both modes (the residual-
+ * gradient stream is carried in f32, DESIGN.md R-grad32).  dy: dev f32
+ * [T,h] gradient of the stage output (stages < p-1; copied into the slot
+ * unless it is the slot's own gradient buffer; NULL on the last stage).
+ * dx: dev f32 [T,h] gradient of the stage input (stages > 0; else NULL).
  * Last stage: LM head + cross-entropy + head weight gradient (eager, C8). */
 zb_status_t zb_stage_backward_input(zb_ctx_t* ctx, int32_t mb, int32_t slot, const void* dy, void* dx);
 /* W of microbatch mb: dW += dY^T X for the four linears of every
@@ -176,7 +179,9 @@ zb_status_t zb_stage_backward_weight(zb_ctx_t* ctx, int32_t mb, int32_t slot);
 /* ------------------------------------------------------------------------ */
 
 enum { ZB_RUN_HOST_INPUTS = 1, /* tokens / labels are host pointers: H2D inside the call */
-       ZB_RUN_TIMING = 2       /* record CUDA events at every pass boundary               */ };
+       ZB_RUN_TIMING = 2,      /* record CUDA events at every pass boundary               */
+       ZB_RUN_FUSED_BW = 4     /* 1F1B: send the input gradient after the W that follows  */
+                               /* its B (the monolithic backward of the baseline, C5)     */ };
 
 typedef struct {
   int32_t n_passes;
@@ -248,10 +253,17 @@ zb_status_t zb_ctx_read_pv_report(zb_ctx_t* ctx, zb_pv_report_t* rep);
 /* 128-byte ncclUniqueId, created on rank 0 and broadcast by the caller
  * (torch.distributed).  ZB_ENCCL if libnccl.so.2 cannot be loaded. */
 zb_status_t zb_nccl_unique_id(void* id128);
-/* Attach a communicator (rank = stage, world = p) used by zb_run_iteration
- * for activation / gradient send-recv on two side streams and by the
- * post-validation chain. */
-zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* id128, int32_t rank, int32_t world);
+/* Attach the P2P communicators of this stage (rank = stage, world = p).
+ * ids: 2*(world-1) unique ids of 128 bytes (identical on every rank): ids[k]
+ * for the activation channel of the pair (k, k+1), ids[world-1+k] for its
+ * gradient channel.  Each channel is a 2-rank communicator driven by its own
+ * stream.  zb_run_iteration then exchanges activations after F and
+ * gradients after B; zb_post_validate_step sends the partial
+ * state down the activation channel; in ZB_OPT_PV mode the validation of
+ * the step happens inside the NEXT zb_run_iteration (after the stage's
+ * speculative warm-up Fs, which are replayed if the weights change — plan.h)
+ * or in zb_post_validate_finish when no iteration follows. */
+zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* ids, int32_t rank, int32_t world);
 
 const char* zb_last_error(void);
 const char* zb_version(void);

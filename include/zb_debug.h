@@ -44,6 +44,17 @@ zb_status_t zb_dbg_attention_bwd(int32_t dtype, int32_t b, int32_t s, int32_t a,
 zb_status_t zb_dbg_kernel_timing(int32_t enable, int32_t reset);
 zb_status_t zb_dbg_kernel_timing_read(int32_t cls, double* total_ms, double* total_flops, int64_t* launches);
 
+/* The host-side P2P plan the NCCL runner executes for `stage` in one
+ * iteration (csrc/plan.h): out_ops[4*i .. 4*i+3] = {type, microbatch,
+ * message index, slot}; types 0 F, 1 B, 2 W, 3 RECV_ACT, 4 SEND_ACT,
+ * 5 RECV_GRAD, 6 SEND_GRAD, 7 VALIDATE, 8 DISCARD_ACT, 9 REPLAY_F.
+ * passes: zb_schedule output of every stage.  Pure host code (no GPU). */
+zb_status_t zb_dbg_stage_plan(const zb_pass_t* passes, int32_t n, int32_t p, int32_t m, int32_t stage,
+                              int32_t pv_pending, int32_t amend, int32_t fused, int32_t* out_ops, int32_t cap,
+                              int32_t* n_out);
+/* n'_s, the number of speculative warm-up Fs of each stage (plan.h). */
+zb_status_t zb_dbg_speculative_counts(const zb_pass_t* passes, int32_t n, int32_t p, int32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,9 @@ _SIGS = {
                     _I32),
     "zb_dbg_attention_fwd": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P], _I32),
     "zb_dbg_attention_bwd": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "zb_dbg_stage_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, _I32, _I32, _I32, C.POINTER(_I32), _I32,
+                           C.POINTER(_I32)], _I32),
+    "zb_dbg_speculative_counts": ([C.POINTER(zb_pass_t), _I32, _I32, C.POINTER(_I32)], _I32),
     "zb_dbg_kernel_timing": ([_I32, _I32], _I32),
     "zb_dbg_kernel_timing_read": ([_I32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(_I64)], _I32),
     "zb_ctx_arena_bytes": ([C.POINTER(zb_model_cfg_t), C.POINTER(C.c_size_t)], _I32),

@@ -199,7 +199,7 @@ extern "C" zb_status_t zb_ctx_slot_ptr(zb_ctx_t* ctx, int32_t slot, int32_t whic
     Ctx* c = C_(ctx);
     if (slot < 0 || slot >= static_cast<int32_t>(c->slots.size()) || !ptr) return set_error(ZB_EINVAL, "bad slot");
     if (which == 0) *ptr = c->slots[slot].L[0].x;
-    else if (which == 1) *ptr = c->slots[slot].dy;
+    else if (which == 1) *ptr = c->slots[slot].dy32;
     else return set_error(ZB_EINVAL, "which must be 0 (input) or 1 (gradient)");
     return ZB_OK;
   }
@@ -357,8 +357,8 @@ extern "C" zb_status_t zb_run_iteration_local(zb_ctx_t* const* ctxs, int32_t p, 
             void* out = s < p - 1 ? c[s + 1]->slots[slot[s + 1][j]].L[0].x : nullptr;
             cs.forward(j, q.slot, in, out, s == p - 1 ? labels + static_cast<int64_t>(j) * T : nullptr);
           } else if (q.kind == ZB_B) {
-            void* dx = s > 0 ? c[s - 1]->slots[slot[s - 1][j]].dy : nullptr;
-            cs.backward_input(j, q.slot, s < p - 1 ? cs.slots[q.slot].dy : nullptr, dx);
+            void* dx = s > 0 ? c[s - 1]->slots[slot[s - 1][j]].dy32 : nullptr;
+            cs.backward_input(j, q.slot, s < p - 1 ? cs.slots[q.slot].dy32 : nullptr, dx);
           } else {
             cs.backward_weight(j, q.slot);
           }
@@ -424,6 +424,12 @@ extern "C" zb_status_t zb_post_validate_step(zb_ctx_t* ctx, const zb_optim_cfg_t
       pv_decide_first(c->pv, o->clip, 0, c->stream);
     }
     pv_apply(*c, *o);
+    if (c->comm && o->mode == ZB_OPT_PV) {  // validated inside the next iteration (or by _finish)
+      c->pv_pending = true;
+      c->pv_clip = o->clip;
+      const float po[5] = {o->lr, o->beta1, o->beta2, o->eps, o->weight_decay};
+      std::memcpy(c->pv_opt, po, sizeof(po));
+    }
     return ZB_OK;
   }
   ZB_CATCH
@@ -435,8 +441,10 @@ extern "C" zb_status_t zb_post_validate_finish(zb_ctx_t* ctx, const zb_optim_cfg
     Ctx* c = C_(ctx);
     if (o->mode == ZB_OPT_SYNC) return ZB_OK;  // nothing to validate
     if (c->comm) {
+      if (!c->pv_pending) return ZB_OK;  // already validated inside an iteration
       pv_recv_full(*c);  // the last stage takes its own partial as the full state
       pv_send_full(*c);
+      c->pv_pending = false;
     } else {
       if (c->cfg.p != 1) return set_error(ZB_EINVAL, "p > 1 needs NCCL or zb_post_validate_local");
       copy_full(*c, *c, true);

@@ -1,0 +1,358 @@
+// NCCL transport and the multi-process iteration runner (see comm.h, plan.h).
+//
+// libnccl.so.2 is dlopen'ed on first use (torch's bundled NCCL is normally
+// already loaded, so the same library is shared).  Every adjacent pair has two
+// 2-rank communicators (ACT s->s+1, GRAD s+1->s), each driven by its own
+// stream on each side; cross-stream ordering uses CUDA events recorded on the
+// compute stream.  The runner executes plan::stage_plan op by op:
+//   RECV_ACT   act-recv stream waits for "compute reached here" (the slot's previous
+//              user W is enqueued before), receives into the slot input buffer;
+//              the compute stream waits for the receive
+//   F / REPLAY_F  forward into the activation send ring
+//   SEND_ACT   act-send stream waits for F, sends the ring buffer; the next F that
+//              reuses the buffer waits for the send
+//   RECV_GRAD  into the slot's gradient buffer;  B writes dX in the slot input buffer
+//   SEND_GRAD  grad-send stream waits for B (or W, 1F1B) and sends from the slot; the
+//              next writer of that slot input waits for the send
+//   VALIDATE   full state: receive from stage+1 (last stage: its own partial),
+//              forward to stage-1, predicated rollback / redo / deferred step, then
+//              the host reads the state (tiny D2H) to decide whether to replay.
+#include "comm.h"
+
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "abi_util.h"
+#include "ops.h"
+#include "plan.h"
+#include "stage.h"
+
+namespace zb {
+
+namespace {
+typedef struct {
+  char internal[128];
+} ncclUniqueId_t;
+typedef int (*PGetId)(ncclUniqueId_t*);
+typedef int (*PInit)(void**, int, ncclUniqueId_t, int);
+typedef int (*PSendRecv)(const void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*PRecv)(void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*PDestroy)(void*);
+typedef const char* (*PErr)(int);
+constexpr int kNcclUint8 = 1;
+
+struct Nccl {
+  void* h = nullptr;
+  PGetId get_id = nullptr;
+  PInit init = nullptr;
+  PSendRecv send = nullptr;
+  PRecv recv = nullptr;
+  PDestroy destroy = nullptr;
+  PErr err = nullptr;
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  if (n.h) return n;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* nm : names) {
+    n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (n.h) break;
+  }
+  if (!n.h) throw Error(ZB_ENCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+  n.get_id = reinterpret_cast<PGetId>(dlsym(n.h, "ncclGetUniqueId"));
+  n.init = reinterpret_cast<PInit>(dlsym(n.h, "ncclCommInitRank"));
+  n.send = reinterpret_cast<PSendRecv>(dlsym(n.h, "ncclSend"));
+  n.recv = reinterpret_cast<PRecv>(dlsym(n.h, "ncclRecv"));
+  n.destroy = reinterpret_cast<PDestroy>(dlsym(n.h, "ncclCommDestroy"));
+  n.err = reinterpret_cast<PErr>(dlsym(n.h, "ncclGetErrorString"));
+  if (!n.get_id || !n.init || !n.send || !n.recv || !n.destroy || !n.err) {
+    n.h = nullptr;
+    throw Error(ZB_ENCCL, "libnccl.so.2 lacks ncclSend / ncclRecv");
+  }
+  return n;
+}
+
+void nck(int r, const char* what) {
+  if (r != 0) throw Error(ZB_ENCCL, std::string(what) + ": " + nccl().err(r));
+}
+
+enum { C_ACT_TO = 0, C_ACT_FROM = 1, C_GRAD_TO = 2, C_GRAD_FROM = 3 };
+
+// peer index inside a 2-rank pair communicator: the lower stage is rank 0
+int peer_of(int which) { return (which == C_ACT_TO || which == C_GRAD_FROM) ? 1 : 0; }
+
+void sendb(Comm& cm, int which, const void* buf, size_t bytes) {
+  nck(nccl().send(buf, bytes, kNcclUint8, peer_of(which), cm.comm[which], cm.stream[which]), "ncclSend");
+}
+void recvb(Comm& cm, int which, void* buf, size_t bytes) {
+  nck(nccl().recv(buf, bytes, kNcclUint8, peer_of(which), cm.comm[which], cm.stream[which]), "ncclRecv");
+}
+
+// stream `a` waits for everything enqueued so far on stream `b`
+void order(Comm& cm, cudaStream_t a, cudaStream_t b) {
+  cudaEvent_t e = cm.event();
+  ZB_CUDA(cudaEventRecord(e, b));
+  ZB_CUDA(cudaStreamWaitEvent(a, e, 0));
+}
+}  // namespace
+
+Comm::~Comm() {
+  for (int i = 0; i < 4; ++i) {
+    if (comm[i]) nccl().destroy(comm[i]);
+    if (stream[i]) cudaStreamDestroy(stream[i]);
+  }
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  for (auto e : act_buf_free) cudaEventDestroy(e);
+  for (auto b : act_buf) cudaFree(b);
+  for (auto e : grad_buf_free) cudaEventDestroy(e);
+  for (auto b : grad_buf) cudaFree(b);
+  if (scalars) cudaFree(scalars);
+}
+
+cudaEvent_t Comm::event() {
+  // a ring of reusable events; 4096 outstanding is far beyond any dependency distance
+  if (ev_pool.size() < 4096) {
+    cudaEvent_t e;
+    ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev_pool.push_back(e);
+    return e;
+  }
+  cudaEvent_t e = ev_pool[ev_next];
+  ev_next = (ev_next + 1) % static_cast<int>(ev_pool.size());
+  return e;
+}
+
+void nccl_unique_id(void* id128) {
+  ncclUniqueId_t id;
+  nck(nccl().get_id(&id), "ncclGetUniqueId");
+  std::memcpy(id128, &id, 128);
+}
+
+void attach_nccl(Ctx& c, const void* ids, int rank, int world) {
+  auto cm = std::make_unique<Comm>();
+  cm->rank = rank;
+  cm->world = world;
+  const char* id = static_cast<const char*>(ids);
+  auto init = [&](int which, int pair, bool grad) {
+    ncclUniqueId_t u;
+    std::memcpy(&u, id + 128 * (grad ? (world - 1 + pair) : pair), 128);
+    const int r = (which == C_ACT_TO || which == C_GRAD_FROM) ? 0 : 1;
+    nck(nccl().init(&cm->comm[which], 2, u, r), "ncclCommInitRank");
+    ZB_CUDA(cudaStreamCreateWithFlags(&cm->stream[which], cudaStreamNonBlocking));
+  };
+  // increasing pair order on every rank: (s-1, s) before (s, s+1) -> no init deadlock
+  if (rank > 0) {
+    init(C_ACT_FROM, rank - 1, false);
+    init(C_GRAD_TO, rank - 1, true);
+  }
+  if (rank < world - 1) {
+    init(C_ACT_TO, rank, false);
+    init(C_GRAD_FROM, rank, true);
+  }
+  if (rank < world - 1) {
+    for (int i = 0; i < 2; ++i) {
+      void* b = nullptr;
+      ZB_CUDA(cudaMalloc(&b, c.esz * static_cast<size_t>(c.T) * c.h));
+      cm->act_buf.push_back(b);
+      cudaEvent_t e;
+      ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ZB_CUDA(cudaEventRecord(e, c.stream));
+      cm->act_buf_free.push_back(e);
+    }
+  }
+  if (rank > 0) {
+    for (int i = 0; i < 2; ++i) {
+      float* b = nullptr;
+      ZB_CUDA(cudaMalloc(&b, sizeof(float) * static_cast<size_t>(c.T) * c.h));
+      cm->grad_buf.push_back(b);
+      cudaEvent_t e;
+      ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ZB_CUDA(cudaEventRecord(e, c.stream));
+      cm->grad_buf_free.push_back(e);
+    }
+  }
+  ZB_CUDA(cudaMalloc(&cm->scalars, 64 + c.esz * static_cast<size_t>(c.T) * c.h));  // 2 PV messages + discard buffer
+  c.comm = std::move(cm);
+}
+
+// ---------------------------------------------------------------- post-validation messages
+// message layout: double sumsq, int32 nonfinite, pad (16 bytes)
+void pv_recv_partial(Ctx& c) {
+  Comm& cm = *c.comm;
+  if (c.cfg.stage == 0) {
+    ZB_CUDA(cudaMemsetAsync(&c.pv->partial_in_sumsq, 0, sizeof(double), c.stream));
+    ZB_CUDA(cudaMemsetAsync(&c.pv->partial_in_nf, 0, sizeof(int32_t), c.stream));
+    return;
+  }
+  char* msg = static_cast<char*>(cm.scalars);
+  order(cm, cm.stream[C_ACT_FROM], c.stream);
+  recvb(cm, C_ACT_FROM, msg, 16);
+  order(cm, c.stream, cm.stream[C_ACT_FROM]);
+  ZB_CUDA(cudaMemcpyAsync(&c.pv->partial_in_sumsq, msg, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  ZB_CUDA(cudaMemcpyAsync(&c.pv->partial_in_nf, msg + 8, sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+void pv_send_partial(Ctx& c) {
+  Comm& cm = *c.comm;
+  if (c.cfg.stage == c.cfg.p - 1) return;
+  char* msg = static_cast<char*>(cm.scalars) + 16;
+  ZB_CUDA(cudaMemcpyAsync(msg, &c.pv->partial_sumsq, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  ZB_CUDA(cudaMemcpyAsync(msg + 8, &c.pv->partial_nf, sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+  order(cm, cm.stream[C_ACT_TO], c.stream);
+  sendb(cm, C_ACT_TO, msg, 16);
+}
+
+void pv_recv_full(Ctx& c) {
+  Comm& cm = *c.comm;
+  if (c.cfg.stage == c.cfg.p - 1) {  // the last stage's partial state is the full state
+    ZB_CUDA(cudaMemcpyAsync(&c.pv->full_sumsq, &c.pv->partial_sumsq, sizeof(double), cudaMemcpyDeviceToDevice,
+                            c.stream));
+    ZB_CUDA(cudaMemcpyAsync(&c.pv->full_nf, &c.pv->partial_nf, sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+    return;
+  }
+  char* msg = static_cast<char*>(cm.scalars) + 32;
+  order(cm, cm.stream[C_GRAD_FROM], c.stream);
+  recvb(cm, C_GRAD_FROM, msg, 16);
+  order(cm, c.stream, cm.stream[C_GRAD_FROM]);
+  ZB_CUDA(cudaMemcpyAsync(&c.pv->full_sumsq, msg, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  ZB_CUDA(cudaMemcpyAsync(&c.pv->full_nf, msg + 8, sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+void pv_send_full(Ctx& c) {
+  Comm& cm = *c.comm;
+  if (c.cfg.stage == 0) return;
+  char* msg = static_cast<char*>(cm.scalars) + 48;
+  ZB_CUDA(cudaMemcpyAsync(msg, &c.pv->full_sumsq, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  ZB_CUDA(cudaMemcpyAsync(msg + 8, &c.pv->full_nf, sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+  order(cm, cm.stream[C_GRAD_TO], c.stream);
+  sendb(cm, C_GRAD_TO, msg, 16);
+}
+
+// ---------------------------------------------------------------- runner
+void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* tokens, const int32_t* labels,
+                        int flags) {
+  Comm& cm = *c.comm;
+  const int p = c.cfg.p, m = c.cfg.m, s = c.cfg.stage, T = c.T;
+  const size_t act_bytes = c.esz * static_cast<size_t>(T) * c.h;
+  const bool fused = (flags & ZB_RUN_FUSED_BW) != 0;
+  // inputs (host or device) are handled exactly as in the single-stage runner
+  const size_t nt = static_cast<size_t>(m) * T;
+  if (flags & ZB_RUN_HOST_INPUTS) {
+    if (c.first && tokens) {
+      ZB_CUDA(cudaMemcpyAsync(c.tok_stage, tokens, nt * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+      tokens = c.tok_stage;
+    }
+    if (c.last && labels) {
+      ZB_CUDA(cudaMemcpyAsync(c.lab_stage, labels, nt * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+      labels = c.lab_stage;
+    }
+  }
+  if (c.first && !tokens) throw Error(ZB_EINVAL, "tokens required on stage 0");
+  if (c.last && !labels) throw Error(ZB_EINVAL, "labels required on the last stage");
+  c.first_b_done = c.first_w_done = false;
+  ZB_CUDA(cudaMemsetAsync(c.loss_acc, 0, sizeof(double), c.stream));
+
+  const bool pending = c.pv_pending;
+  std::vector<plan::Op> ops = plan::stage_plan(passes, n, p, m, s, pending, false, fused);
+  std::vector<plan::Op> ops_amend;
+  if (pending) ops_amend = plan::stage_plan(passes, n, p, m, s, true, true, fused);
+  const size_t grad_bytes = sizeof(float) * static_cast<size_t>(T) * c.h;  // f32 gradient stream (R-grad32)
+  int act_ring = 0, grad_ring = 0;
+  int last_act_buf = -1, last_grad_buf = -1;
+  c.n_timed = 0;
+  bool switched = false;
+  for (size_t k = 0; k < ops.size(); ++k) {
+    const plan::Op op = ops[k];
+    Slot* sl = op.slot >= 0 ? &c.slots.at(op.slot) : nullptr;
+    switch (op.type) {
+      case plan::OP_RECV_ACT: {
+        order(cm, cm.stream[C_ACT_FROM], c.stream);  // the slot's previous user has finished
+        recvb(cm, C_ACT_FROM, sl->L[0].x, act_bytes);
+        order(cm, c.stream, cm.stream[C_ACT_FROM]);
+        break;
+      }
+      case plan::OP_DISCARD_ACT: {
+        recvb(cm, C_ACT_FROM, static_cast<char*>(cm.scalars) + 64, act_bytes);
+        break;
+      }
+      case plan::OP_F:
+      case plan::OP_REPLAY_F: {
+        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed);
+        void* out = nullptr;
+        if (!c.last) {
+          last_act_buf = act_ring;
+          ZB_CUDA(cudaStreamWaitEvent(c.stream, cm.act_buf_free[act_ring], 0));
+          out = cm.act_buf[act_ring];
+          act_ring = (act_ring + 1) % static_cast<int>(cm.act_buf.size());
+        }
+        const void* in = c.first ? static_cast<const void*>(tokens + static_cast<int64_t>(op.mb) * T) : sl->L[0].x;
+        c.forward(op.mb, op.slot, in, out, c.last ? labels + static_cast<int64_t>(op.mb) * T : nullptr);
+        if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
+        break;
+      }
+      case plan::OP_SEND_ACT: {
+        order(cm, cm.stream[C_ACT_TO], c.stream);
+        sendb(cm, C_ACT_TO, cm.act_buf[last_act_buf], act_bytes);
+        ZB_CUDA(cudaEventRecord(cm.act_buf_free[last_act_buf], cm.stream[C_ACT_TO]));
+        break;
+      }
+      case plan::OP_RECV_GRAD: {
+        order(cm, cm.stream[C_GRAD_FROM], c.stream);
+        recvb(cm, C_GRAD_FROM, sl->dy32, grad_bytes);
+        order(cm, c.stream, cm.stream[C_GRAD_FROM]);
+        break;
+      }
+      case plan::OP_B: {
+        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed);
+        float* dx = nullptr;
+        if (!c.first) {
+          last_grad_buf = grad_ring;
+          ZB_CUDA(cudaStreamWaitEvent(c.stream, cm.grad_buf_free[grad_ring], 0));
+          dx = cm.grad_buf[grad_ring];
+          grad_ring = (grad_ring + 1) % static_cast<int>(cm.grad_buf.size());
+        }
+        c.backward_input(op.mb, op.slot, c.last ? nullptr : sl->dy32, dx);
+        if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
+        break;
+      }
+      case plan::OP_SEND_GRAD: {
+        order(cm, cm.stream[C_GRAD_TO], c.stream);
+        sendb(cm, C_GRAD_TO, cm.grad_buf[last_grad_buf], grad_bytes);  // f32 dX of the stage input
+        ZB_CUDA(cudaEventRecord(cm.grad_buf_free[last_grad_buf], cm.stream[C_GRAD_TO]));
+        break;
+      }
+      case plan::OP_W: {
+        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed);
+        c.backward_weight(op.mb, op.slot);
+        if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
+        break;
+      }
+      case plan::OP_VALIDATE: {
+        pv_recv_full(c);
+        pv_send_full(c);
+        pv_decide_final(c.pv, c.pv_clip, c.stream);
+        adamw_apply(c.theta, c.m, c.v, c.grad, c.shadow, c.n_total, c.n_wd, c.shadow ? c.n_shadow : 0, c.pv_opt[0],
+                    c.pv_opt[1], c.pv_opt[2], c.pv_opt[3], c.pv_opt[4], c.pv, c.stream);
+        pv_finish_apply(c.pv, c.stream);
+        c.pv_pending = false;
+        // the host needs the outcome to know whether the speculative Fs must be replayed
+        PvState hst;
+        ZB_CUDA(cudaMemcpyAsync(&hst, c.pv, sizeof(PvState), cudaMemcpyDeviceToHost, c.stream));
+        ZB_CUDA(cudaStreamSynchronize(c.stream));
+        const double coef = c.pv_clip / (std::sqrt(hst.full_sumsq) + 1e-6);
+        const bool amend = hst.full_nf != 0 || coef < 1.0;  // identical on every stage
+        if (amend && !switched) {
+          ops = ops_amend;  // same prefix up to and including this VALIDATE
+          switched = true;
+        }
+        break;
+      }
+    }
+  }
+}
+
+}  // namespace zb

@@ -32,6 +32,9 @@ struct Comm {
   std::vector<void*> act_buf;
   std::vector<cudaEvent_t> act_buf_free;
   int act_next = 0;
+  // send staging ring for f32 input gradients (written by B, drained by the grad-send stream)
+  std::vector<float*> grad_buf;
+  std::vector<cudaEvent_t> grad_buf_free;
   std::vector<cudaEvent_t> ev_pool;
   int ev_next = 0;
   void* scalars = nullptr;  // 2 x 16 B device buffer for PV messages

@@ -93,73 +93,82 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_fwd(const T* __restrict__ x, 
 }
 
 // ---------------------------------------------------------------- LayerNorm backward
-template <typename T, int VPT, typename TD = T>
-__global__ void __launch_bounds__(LN_THREADS) k_ln_bwd(const TD* __restrict__ dy, const T* x, const float* __restrict__ mean,
-                                                      const float* __restrict__ rstd, const float* __restrict__ g,
-                                                      const T* resid, T* dx, float* __restrict__ dg_part,
-                                                      float* __restrict__ db_part, int rows, int h) {
+// dx only, one CTA per row (full parallelism over rows).  The residual-gradient
+// stream stays f32 (resid and dx32, may be null); dx (activation dtype, may
+// alias x) is the copy the dgrad / wgrad GEMMs consume.
+template <typename T, int VPT>
+__global__ void __launch_bounds__(LN_THREADS) k_ln_bwd_dx(const float* __restrict__ dy, const T* x,
+                                                         const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                         const float* __restrict__ g, const float* resid, float* dx32,
+                                                         T* dx, int h) {
   constexpr int NW = LN_THREADS / 32;
   __shared__ float red[2 * NW];
+  const int64_t r = blockIdx.x;
   const int nv = h / 8;
-  const int r0 = blockIdx.x * kRowsPerChunk;
-  const int r1 = min(rows, r0 + kRowsPerChunk);
-  float gw[VPT][8], adg[VPT][8], adb[VPT][8];
-#pragma unroll
-  for (int k = 0; k < VPT; ++k) {
-    const int vi = threadIdx.x + k * LN_THREADS;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) adg[k][i] = adb[k][i] = 0.f;
-    if (vi < nv) Vec8<float>::load(g + vi * 8, gw[k]);
-  }
-  for (int r = r0; r < r1; ++r) {
-    const float mu = mean[r], rs = rstd[r];
-    float xh[VPT][8], gh[VPT][8];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int vi = threadIdx.x + k * LN_THREADS;
-      if (vi < nv) {
-        float d[8];
-        Vec8<TD>::load(dy + static_cast<int64_t>(r) * h + vi * 8, d);
-        Vec8<T>::load(x + static_cast<int64_t>(r) * h + vi * 8, xh[k]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          xh[k][i] = (xh[k][i] - mu) * rs;
-          gh[k][i] = d[i] * gw[k][i];
-          s1 += gh[k][i];
-          s2 += gh[k][i] * xh[k][i];
-          adg[k][i] += d[i] * xh[k][i];
-          adb[k][i] += d[i];
-        }
-      }
-    }
-    block_sum2<NW>(s1, s2, red);  // also orders every read of row r before the writes below
-    const float m1 = s1 / h, m2 = s2 / h;
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int vi = threadIdx.x + k * LN_THREADS;
-      if (vi < nv) {
-        float o[8];
-        if (resid != nullptr) {
-          Vec8<T>::load(resid + static_cast<int64_t>(r) * h + vi * 8, o);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) o[i] = 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] += rs * (gh[k][i] - m1 - xh[k][i] * m2);
-        Vec8<T>::store(dx + static_cast<int64_t>(r) * h + vi * 8, o);
-      }
-    }
-  }
+  const float mu = mean[r], rs = rstd[r];
+  float xh[VPT][8], gh[VPT][8];
+  float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
     const int vi = threadIdx.x + k * LN_THREADS;
     if (vi < nv) {
-      Vec8<float>::store(dg_part + static_cast<int64_t>(blockIdx.x) * h + vi * 8, adg[k]);
-      Vec8<float>::store(db_part + static_cast<int64_t>(blockIdx.x) * h + vi * 8, adb[k]);
+      float d[8], gw[8];
+      Vec8<float>::load(dy + r * h + vi * 8, d);
+      Vec8<T>::load(x + r * h + vi * 8, xh[k]);
+      Vec8<float>::load(g + vi * 8, gw);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        xh[k][i] = (xh[k][i] - mu) * rs;
+        gh[k][i] = d[i] * gw[i];
+        s1 += gh[k][i];
+        s2 += gh[k][i] * xh[k][i];
+      }
     }
   }
+  block_sum2<NW>(s1, s2, red);  // orders every read of row r before the in-place writes
+  const float m1 = s1 / h, m2 = s2 / h;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int vi = threadIdx.x + k * LN_THREADS;
+    if (vi < nv) {
+      float o[8];
+      if (resid != nullptr) {
+        Vec8<float>::load(resid + r * h + vi * 8, o);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] += rs * (gh[k][i] - m1 - xh[k][i] * m2);
+      if (dx32 != nullptr) Vec8<float>::store(dx32 + r * h + vi * 8, o);
+      Vec8<T>::store(dx + r * h + vi * 8, o);
+    }
+  }
+}
+
+// gamma / beta partials: part[c, col] = sum over the rows of chunk c of dy * xhat (resp. dy).
+template <typename T>
+__global__ void k_ln_param_partials(const float* __restrict__ dy, const T* __restrict__ x,
+                                    const float* __restrict__ mean, const float* __restrict__ rstd,
+                                    float* __restrict__ dg_part, float* __restrict__ db_part, int rows, int h) {
+  const int vi = blockIdx.y * blockDim.x + threadIdx.x;
+  if (vi * 8 >= h) return;
+  const int r0 = blockIdx.x * kRowsPerChunk;
+  const int r1 = min(rows, r0 + kRowsPerChunk);
+  float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = r0; r < r1; ++r) {
+    const float mu = mean[r], rs = rstd[r];
+    float d[8], xv[8];
+    Vec8<float>::load(dy + static_cast<int64_t>(r) * h + vi * 8, d);
+    Vec8<T>::load(x + static_cast<int64_t>(r) * h + vi * 8, xv);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      ag[i] += d[i] * ((xv[i] - mu) * rs);
+      ab[i] += d[i];
+    }
+  }
+  Vec8<float>::store(dg_part + static_cast<int64_t>(blockIdx.x) * h + vi * 8, ag);
+  Vec8<float>::store(db_part + static_cast<int64_t>(blockIdx.x) * h + vi * 8, ab);
 }
 
 __global__ void k_reduce_chunks(const float* __restrict__ part, float* __restrict__ out, int nchunks, int n, int beta) {
@@ -554,19 +563,29 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
   ZB_LAUNCH_CHECK();
 }
 
-void layernorm_bwd(DType dt, const void* dy, const void* x, const float* mean, const float* rstd, const float* g,
-                   const void* resid, void* dx, float* dg_part, float* db_part, int rows, int h, cudaStream_t st) {
+void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
+                   const float* resid, float* dx32, void* dx, float* dg_part, float* db_part, int rows, int h,
+                   cudaStream_t st) {
   if (rows <= 0) return;
+  // 1) gamma / beta chunk partials (reads x before step 2 may overwrite it in place)
+  dim3 pg(n_chunks(rows), (h / 8 + 127) / 128);
+  if (dt == DT_BF16)
+    k_ln_param_partials<bf16><<<pg, 128, 0, st>>>(static_cast<const float*>(dy), static_cast<const bf16*>(x), mean,
+                                                   rstd, dg_part, db_part, rows, h);
+  else
+    k_ln_param_partials<float><<<pg, 128, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(x), mean,
+                                                    rstd, dg_part, db_part, rows, h);
+  ZB_LAUNCH_CHECK();
+  // 2) dx, one CTA per row (dy arrives in f32: the dLN GEMM epilogue keeps full precision)
   ln_dispatch<0>(h, [&](auto V) {
     constexpr int VPT = decltype(V)::value;
-    if (dt == DT_BF16)  // dy arrives in f32 (the dLN GEMM epilogue keeps full precision)
-      k_ln_bwd<bf16, VPT, float><<<n_chunks(rows), LN_THREADS, 0, st>>>(
-          static_cast<const float*>(dy), static_cast<const bf16*>(x), mean, rstd, g, static_cast<const bf16*>(resid),
-          static_cast<bf16*>(dx), dg_part, db_part, rows, h);
+    if (dt == DT_BF16)
+      k_ln_bwd_dx<bf16, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const float*>(dy), static_cast<const bf16*>(x),
+                                                          mean, rstd, g, resid, dx32, static_cast<bf16*>(dx), h);
     else
-      k_ln_bwd<float, VPT><<<n_chunks(rows), LN_THREADS, 0, st>>>(
-          static_cast<const float*>(dy), static_cast<const float*>(x), mean, rstd, g, static_cast<const float*>(resid),
-          static_cast<float*>(dx), dg_part, db_part, rows, h);
+      k_ln_bwd_dx<float, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const float*>(dy),
+                                                           static_cast<const float*>(x), mean, rstd, g, resid, dx32,
+                                                           static_cast<float*>(dx), h);
   });
   ZB_LAUNCH_CHECK();
 }
@@ -627,6 +646,10 @@ void cross_entropy(DType dt, const float* logits, const int32_t* labels, void* d
   ZB_LAUNCH_CHECK();
   k_loss_reduce<<<1, 1024, 0, st>>>(loss_rows, loss_acc, rows, inv_scale);
   ZB_LAUNCH_CHECK();
+}
+
+void convert_rows(DType dt, const float* src, void* dst, int64_t n, cudaStream_t st) {
+  convert_f32(dt, src, dst, n, st);
 }
 
 void convert_f32(DType dt, const float* src, void* dst, int64_t n, cudaStream_t st) {

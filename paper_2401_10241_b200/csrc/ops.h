@@ -20,8 +20,13 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
 //   dg_part[c, :] = sum over rows of chunk c of dy * xhat; db_part[c, :] = sum dy
 // dy is f32 in both modes; x / resid / dx are in the activation dtype.
 // resid may be null; dx may alias x or resid.
-void layernorm_bwd(DType dt, const void* dy, const void* x, const float* mean, const float* rstd, const float* g,
-                   const void* resid, void* dx, float* dg_part, float* db_part, int rows, int h, cudaStream_t st);
+// The residual-gradient stream is f32 (resid, dx32; either may be null) and dx
+// (activation dtype) receives the copy the GEMMs consume (DESIGN.md R-grad32).
+void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
+                   const float* resid, float* dx32, void* dx, float* dg_part, float* db_part, int rows, int h,
+                   cudaStream_t st);
+// f32 -> activation dtype row copy (received stage-boundary gradients)
+void convert_rows(DType dt, const float* src, void* dst, int64_t n, cudaStream_t st);
 // part [nchunks, n] f32 -> out[n] = (beta ? out : 0) + sum_c part[c]  (fixed order)
 void reduce_chunks(const float* part, float* out, int nchunks, int n, int beta, cudaStream_t st);
 // Column sums of y [rows, n] (activation dtype) into part [n_chunks(rows), n].

@@ -1,0 +1,84 @@
+#include "plan.h"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace zb {
+namespace plan {
+
+namespace {
+std::vector<std::vector<const zb_pass_t*>> by_stage(const zb_pass_t* passes, int n, int p) {
+  std::vector<std::vector<const zb_pass_t*>> L(p);
+  for (int i = 0; i < n; ++i) {
+    if (passes[i].stage < 0 || passes[i].stage >= p) throw std::invalid_argument("pass stage out of range");
+    L[passes[i].stage].push_back(&passes[i]);
+  }
+  return L;
+}
+int leading_f(const std::vector<const zb_pass_t*>& l) {
+  int k = 0;
+  while (k < static_cast<int>(l.size()) && l[k]->kind == ZB_F) ++k;
+  return k;
+}
+}  // namespace
+
+std::vector<int> speculative_counts(const zb_pass_t* passes, int n, int p) {
+  auto L = by_stage(passes, n, p);
+  std::vector<int> out(p);
+  for (int s = 0; s < p; ++s) {
+    int lead = leading_f(L[s]);
+    out[s] = s == 0 ? lead : std::min(lead, out[s - 1]);
+  }
+  return out;
+}
+
+std::vector<Op> stage_plan(const zb_pass_t* passes, int n, int p, int m, int stage, bool pv_pending, bool amend,
+                           bool fused) {
+  auto L = by_stage(passes, n, p);
+  const auto spec = speculative_counts(passes, n, p);
+  const int s = stage;
+  const int n_self = spec[s];
+  const int n_prev = s > 0 ? spec[s - 1] : 0;
+  const auto& mine = L[s];
+  std::vector<int> slot_of(m, -1);
+  for (auto* q : mine)
+    if (q->kind == ZB_F) slot_of[q->microbatch] = q->slot;
+  std::vector<Op> ops;
+  bool amended = false;
+  auto recv_msg = [&](int j) { return amended ? n_prev + j : j; };
+  auto send_msg = [&](int j) { return amended ? n_self + j : j; };
+  for (size_t i = 0; i <= mine.size(); ++i) {
+    if (pv_pending && static_cast<int>(i) == n_self) {
+      ops.push_back({OP_VALIDATE, -1, -1, -1});
+      if (amend) {
+        if (s > 0)
+          for (int msg = n_self; msg < n_prev; ++msg) ops.push_back({OP_DISCARD_ACT, -1, msg, -1});
+        for (int j = 0; j < n_self; ++j) {
+          if (s > 0) ops.push_back({OP_RECV_ACT, j, n_prev + j, slot_of[j]});
+          ops.push_back({OP_REPLAY_F, j, -1, slot_of[j]});
+          if (s < p - 1) ops.push_back({OP_SEND_ACT, j, n_self + j, slot_of[j]});
+        }
+        amended = true;
+      }
+    }
+    if (i == mine.size()) break;
+    const zb_pass_t& q = *mine[i];
+    const int j = q.microbatch;
+    if (q.kind == ZB_F) {
+      if (s > 0) ops.push_back({OP_RECV_ACT, j, recv_msg(j), q.slot});
+      ops.push_back({OP_F, j, -1, q.slot});
+      if (s < p - 1) ops.push_back({OP_SEND_ACT, j, send_msg(j), q.slot});
+    } else if (q.kind == ZB_B) {
+      if (s < p - 1) ops.push_back({OP_RECV_GRAD, j, j, q.slot});
+      ops.push_back({OP_B, j, -1, q.slot});
+      if (s > 0 && !fused) ops.push_back({OP_SEND_GRAD, j, j, q.slot});
+    } else {
+      ops.push_back({OP_W, j, -1, q.slot});
+      if (s > 0 && fused) ops.push_back({OP_SEND_GRAD, j, j, q.slot});
+    }
+  }
+  return ops;
+}
+
+}  // namespace plan
+}  // namespace zb

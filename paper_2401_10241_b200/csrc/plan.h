@@ -1,0 +1,50 @@
+// Per-stage operation plan of one iteration with P2P messages (host only).
+//
+// The NCCL runner (comm.cpp) executes exactly this sequence, and the gloo
+// multi-process test (tests/test_comm_plan_gloo.py) executes it on CPU, so the
+// message matching across ranks is tested without GPUs.
+//
+// Channels per adjacent pair: ACT (s -> s+1, activations after F, then the
+// post-validation partial state) and GRAD (s+1 -> s, input gradients after B,
+// then the full state).  Message order on each channel is the microbatch order.
+//
+// Post-validation speculation ("during the warm-up phase of the
+// next iteration ... a rollback will be issued ... and then we redo"; DESIGN.md
+// R-pv): stage s runs its first n'_s Fs of iteration i+1 on not-yet-validated
+// weights, with n'_0 = leading Fs of stage 0 and n'_s = min(leading Fs of s,
+// n'_{s-1}); then it VALIDATEs (receives the full state on GRAD, forwards it).
+// If the full state amends the weights (clip needed or non-finite) every stage
+// REPLAYs its n'_s speculative Fs.  On ACT, stage s-1 then emits its n'_{s-1}
+// speculative messages, its n'_{s-1} replays, then F(j >= n'_{s-1}); stage s
+// drains the stale messages [n'_s, n'_{s-1}) and maps F(j) -> message n'_{s-1}+j.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "zb.h"
+
+namespace zb {
+namespace plan {
+
+enum OpType : int32_t {
+  OP_F = 0, OP_B = 1, OP_W = 2,
+  OP_RECV_ACT = 3, OP_SEND_ACT = 4, OP_RECV_GRAD = 5, OP_SEND_GRAD = 6,
+  OP_VALIDATE = 7, OP_DISCARD_ACT = 8, OP_REPLAY_F = 9
+};
+
+struct Op {
+  int32_t type, mb, msg, slot;
+};
+
+// n'_s of every stage (see header comment)
+std::vector<int> speculative_counts(const zb_pass_t* passes, int n, int p);
+
+// Plan of `stage` for one iteration.  pv_pending: a post-validation of the
+// previous step is outstanding (validate at n'_stage); amend: the outcome of
+// that validation changes weights (replays).  fused: 1F1B's monolithic
+// backward (the gradient is sent after the W that follows its B).
+std::vector<Op> stage_plan(const zb_pass_t* passes, int n, int p, int m, int stage, bool pv_pending, bool amend,
+                           bool fused);
+
+}  // namespace plan
+}  // namespace zb

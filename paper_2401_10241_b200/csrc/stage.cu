@@ -166,6 +166,7 @@ size_t carve(Ctx& c, uint8_t* base) {
       A.lse = bp.take<float>(static_cast<size_t>(c.a) * T);
     }
     sl.dy = bp.take_bytes(T * h * e);
+    sl.dy32 = c.last ? nullptr : bp.take<float>(T * h);
     sl.tok = c.first ? bp.take<int32_t>(T) : nullptr;
     sl.lab = c.last ? bp.take<int32_t>(T) : nullptr;
     if (c.last) {
@@ -182,6 +183,8 @@ size_t carve(Ctx& c, uint8_t* base) {
   c.spare_qkv = bp.take_bytes(T * 3 * h * e);
   c.d_o = bp.take_bytes(T * h * e);
   c.d_ln = bp.take<float>(T * h);  // f32 in both modes (LayerNorm-input gradient)
+  c.g32_dx = bp.take<float>(T * h);
+  c.g32_dx1 = bp.take<float>(T * h);
   c.delta = bp.take<float>(static_cast<size_t>(c.a) * T);
   c.part_a = bp.take<float>(static_cast<size_t>(n_chunks(c.T)) * 4 * h);
   c.part_b = bp.take<float>(static_cast<size_t>(n_chunks(c.T)) * h);
@@ -247,9 +250,9 @@ static void bias_grad(Ctx& c, const void* dY, float* db, int N, int beta) {
   colsum_partials(c.dt, dY, N, c.part_a, c.T, N, c.stream);
   reduce_chunks(c.part_a, db, n_chunks(c.T), N, beta, c.stream);
 }
-static void ln_bwd(Ctx& c, const void* dy, const void* x, const float* mu, const float* rs, const float* g,
-                   const void* resid, void* dx, float* gg, float* gb, int beta) {
-  layernorm_bwd(c.dt, dy, x, mu, rs, g, resid, dx, c.part_a, c.part_b, c.T, c.h, c.stream);
+static void ln_bwd(Ctx& c, const float* dy, const void* x, const float* mu, const float* rs, const float* g,
+                   const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta) {
+  layernorm_bwd(c.dt, dy, x, mu, rs, g, resid, dx32, dx, c.part_a, c.part_b, c.T, c.h, c.stream);
   reduce_chunks(c.part_a, gg, n_chunks(c.T), c.h, beta, c.stream);
   reduce_chunks(c.part_b, gb, n_chunks(c.T), c.h, beta, c.stream);
 }
@@ -291,16 +294,24 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
   Slot& sl = slots.at(slot_idx);
   const int H = h;
   const int beta = first_b_done ? 1 : 0;
+  // The residual-gradient stream (dX', dX1, dX) is carried in f32 (g32_dx / g32_dx1,
+  // DESIGN.md R-grad32); the activation-dtype copies written into the slot feed the
+  // dgrad GEMMs now and the wgrad GEMMs in W.
+  const float* dx2_32;
   if (last) {
     lin_fwd(*this, sl.lnf, head_w, nullptr, logits, T, V, H, EPI_F32_STORE, nullptr);
     cross_entropy(dt, logits, sl.lab, dlogits, loss_rows, loss_acc, T, V,
                   1.0f / (static_cast<float>(T) * static_cast<float>(cfg.m)), stream);
     lin_wgrad(*this, dlogits, sl.lnf, g_head_w, V, H, T, beta);  // head W eagerly (C8 reading)
     lin_dgrad(*this, dlogits, head_w, d_ln, T, H, V, EPI_F32_STORE, nullptr);
-    ln_bwd(*this, d_ln, sl.xl, sl.muf, sl.rsf, lnf_g, nullptr, sl.dy, g_lnf_g, g_lnf_b, beta);
+    ln_bwd(*this, d_ln, sl.xl, sl.muf, sl.rsf, lnf_g, nullptr, g32_dx, sl.dy, g_lnf_g, g_lnf_b, beta);
+    dx2_32 = g32_dx;
   } else {
     if (dy_in == nullptr) throw std::invalid_argument("zb_stage_backward_input: dy is required on stages < p-1");
-    if (dy_in != sl.dy) ZB_CUDA(cudaMemcpyAsync(sl.dy, dy_in, esz * T * H, cudaMemcpyDeviceToDevice, stream));
+    const float* dyf = static_cast<const float*>(dy_in);
+    if (dyf != sl.dy32) ZB_CUDA(cudaMemcpyAsync(sl.dy32, dyf, sizeof(float) * T * H, cudaMemcpyDeviceToDevice, stream));
+    convert_rows(dt, sl.dy32, sl.dy, static_cast<int64_t>(T) * H, stream);
+    dx2_32 = sl.dy32;
   }
   AttnShape ash{b, s, a, d};
   for (int l = Ls - 1; l >= 0; --l) {
@@ -309,15 +320,16 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
     void* dx2 = l == Ls - 1 ? sl.dy : sl.L[l + 1].x;
     lin_dgrad(*this, dx2, w.fc2_w, A.u, T, 4 * H, H, EPI_GELU_BWD, A.u);  // dU over U
     lin_dgrad(*this, A.u, w.fc1_w, d_ln, T, H, 4 * H, EPI_F32_STORE, nullptr);
-    ln_bwd(*this, d_ln, A.x1, A.mu2, A.rs2, w.ln2_g, dx2, A.x1, w.g_ln2_g, w.g_ln2_b, beta);  // dX1 over X1
+    ln_bwd(*this, d_ln, A.x1, A.mu2, A.rs2, w.ln2_g, dx2_32, g32_dx1, A.x1, w.g_ln2_g, w.g_ln2_b, beta);  // dX1
     lin_dgrad(*this, A.x1, w.proj_w, d_o, T, H, H, EPI_STORE, nullptr);
     attention_bwd(ash, dt, A.qkv, A.o, d_o, A.lse, spare_qkv, delta, stream);
-    std::swap(A.qkv, spare_qkv);                                                         // dQKV in the slot
+    std::swap(A.qkv, spare_qkv);                                                              // dQKV in the slot
     lin_dgrad(*this, A.qkv, w.qkv_w, d_ln, T, H, 3 * H, EPI_F32_STORE, nullptr);
-    ln_bwd(*this, d_ln, A.x, A.mu1, A.rs1, w.ln1_g, A.x1, A.x, w.g_ln1_g, w.g_ln1_b, beta);   // dX over X
+    // the stage's input gradient (l == 0) goes straight to the caller's f32 buffer
+    float* out32 = (l == 0 && !first && dx_out != nullptr) ? static_cast<float*>(dx_out) : g32_dx;
+    ln_bwd(*this, d_ln, A.x, A.mu1, A.rs1, w.ln1_g, g32_dx1, out32, A.x, w.g_ln1_g, w.g_ln1_b, beta);     // dX
+    dx2_32 = g32_dx;
   }
-  if (!first && dx_out != nullptr && dx_out != sl.L[0].x)
-    ZB_CUDA(cudaMemcpyAsync(dx_out, sl.L[0].x, esz * T * H, cudaMemcpyDeviceToDevice, stream));
   first_b_done = true;
 }
 

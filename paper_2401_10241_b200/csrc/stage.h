@@ -40,7 +40,8 @@ struct LayerAct {
 
 struct Slot {
   std::vector<LayerAct> L;
-  void* dy;
+  void* dy;       // gradient of the stage output, activation dtype (GEMM operand in B and W)
+  float* dy32;    // the same gradient in f32 as received from stage+1 (residual chain, R-grad32)
   void* xl;
   void* lnf;
   float *muf, *rsf;
@@ -72,8 +73,10 @@ struct Ctx {
 
   // stash and scratch
   std::vector<Slot> slots;
-  void *spare_qkv = nullptr, *d_o = nullptr, *d_ln = nullptr, *dlogits = nullptr;
+  void *spare_qkv = nullptr, *d_o = nullptr, *dlogits = nullptr;
+  float* d_ln = nullptr;  // LayerNorm-input gradient, f32 in both modes
   float *delta = nullptr, *part_a = nullptr, *part_b = nullptr, *logits = nullptr, *loss_rows = nullptr;
+  float *g32_dx = nullptr, *g32_dx1 = nullptr;  // f32 residual-gradient stream of B (R-grad32)
   uint32_t* keys = nullptr;
   int32_t *tok_stage = nullptr, *lab_stage = nullptr;
   double* loss_acc = nullptr;
@@ -82,6 +85,11 @@ struct Ctx {
   PvState* pv = nullptr;
 
   bool first_b_done = false, first_w_done = false;
+
+  // post-validation with NCCL: a validation of the last step is outstanding
+  bool pv_pending = false;
+  float pv_clip = 1.f;
+  float pv_opt[5] = {0, 0, 0, 0, 0};  // lr, beta1, beta2, eps, weight_decay of the pending step
 
   // timing (ZB_RUN_TIMING)
   std::vector<cudaEvent_t> ev_start, ev_end;
