@@ -321,7 +321,98 @@ def predicted_bubbles(cfg, t_pass):
 
 
 def run_pipeline(args, cfg, rank, world, local):
-    raise SystemExit("multi-GPU pipeline runner: see DESIGN.md (NCCL transport not built in this version)")
+    """p = N stages, one per GPU, NCCL P2P (zb_ctx_attach_nccl).  Times are
+    taken on each rank with CUDA events and the MAX over ranks is reported."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2401_10241_b200 import api
+    from paper_2401_10241_b200._lib import lib
+    import ctypes as C
+
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p, m = world, cfg.m
+    mc = api.model_cfg(cfg, p, rank, m, 1, "bf16")
+    slot_b = api.slot_bytes(mc)
+    passes, sim = api.schedule(args.family, p, m, 10, 10, 10, 0,
+                               M_limit=(cfg.mem_factor * p * slot_b if args.family == "auto" else 0),
+                               M_B=slot_b, M_W=slot_b)
+    ids = [api.nccl_unique_ids(2 * (p - 1)) if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    stream = torch.cuda.Stream()
+    ctx = api.Context(cfg, p, rank, m, max(1, sim.n_slots[rank]), dtype="bf16", stream=stream)
+    params = zb_synth.make_stage_params(cfg, p, rank)
+    ctx.set_params([params[n] for n, _, _ in zb_synth.param_specs(cfg, p, rank)])
+    del params
+    ctx.attach_nccl(ids[0], rank, p)
+    n_steps = args.warmup + args.steps
+    toks = [zb_synth.make_tokens(cfg, i) for i in range(n_steps)]
+    tok_d = [torch.from_numpy(np.ascontiguousarray(t[..., :cfg.s])).cuda() for t in toks]
+    lab_d = [torch.from_numpy(np.ascontiguousarray(t[..., 1:])).cuda() for t in toks]
+    opt = api.optim_cfg(lr=1e-4, mode="pv", clip=1.0)
+
+    def run(family_passes, fused, steps, first, timing=False):
+        for i in range(first, first + steps):
+            ctx.run_iteration(family_passes, tok_d[i % n_steps] if rank == 0 else None,
+                              lab_d[i % n_steps] if rank == p - 1 else None, timing=timing, fused=fused)
+            ctx.post_validate_step(opt)
+
+    def timed(family_passes, fused):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run(family_passes, fused, args.steps, args.warmup)
+        ctx.post_validate_finish(opt)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    run(passes, False, args.warmup, 0)
+    ctx.post_validate_finish(opt)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = timed(passes, False)
+    tokens_per_step = cfg.T * m
+    value = tokens_per_step / (ms / 1000.0)
+    # measured per-stage busy / span of one iteration (scheduling bubble, SURVEY §8(d))
+    run(passes, False, 1, 0, timing=True)
+    ctx.post_validate_finish(opt)
+    starts, ends = ctx.stats()
+    busy = sum(e - s for s, e in zip(starts, ends))
+    span = ends[-1] - starts[0] if starts else 0.0
+    stat = torch.tensor([busy, span], device="cuda")
+    gathered = [torch.zeros_like(stat) for _ in range(p)]
+    dist.all_gather(gathered, stat)
+    busys = [float(g[0]) for g in gathered]
+    spans = [float(g[1]) for g in gathered]
+    cost = max(spans)
+    bubble = {"measured_scheduling": (cost - max(busys)) / cost if cost else None,
+              "imbalance": 1 - (sum(busys) / len(busys)) / max(busys) if busys else None,
+              "stage_busy_ms": busys, "stage_span_ms": spans, "predicted": sim.bubble_rate}
+    # 1F1B on the same kernels (SURVEY §8(d): "vs 1F1B")
+    p1, s1 = api.schedule("1f1b", p, m, 10, 10, 10, 0)
+    ms_1f1b = None
+    if args.family != "1f1b" and s1.n_slots[rank] <= max(1, sim.n_slots[rank]):
+        run(p1, True, 1, 0)
+        ctx.post_validate_finish(opt)
+        ms_1f1b = timed(p1, True)
+    if rank == 0:
+        peaks, src = read_peaks()
+        flops_token = cfg.L * (72 * cfg.h ** 2 + 12 * cfg.s * cfg.h) + 6 * cfg.h * cfg.V
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": p, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (zb_synth seeded weights and tokens)",
+                "config": workload_config(cfg, p, args.family), "clocks": clk.summary(), "e2e": None,
+                "bubble": bubble,
+                "vs_1f1b": {"tokens_per_s_1f1b": tokens_per_step / (ms_1f1b / 1000.0) if ms_1f1b else None,
+                            "speedup": ms_1f1b / ms if ms_1f1b else None},
+                "model_flops_utilization": round(value * flops_token / (p * peaks.get("bf16_tflops", 1680.3) * 1e12), 4)}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

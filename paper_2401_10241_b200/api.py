@@ -175,8 +175,13 @@ class Context:
     def backward_weight(self, mb, slot):
         check(lib.zb_stage_backward_weight(self.h, mb, slot))
 
-    def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False):
-        flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0)
+    def attach_nccl(self, ids: bytes, rank: int, world: int):
+        """ids: 2*(world-1) x 128-byte NCCL unique ids, identical on every rank."""
+        buf = C.create_string_buffer(ids, len(ids))
+        check(lib.zb_ctx_attach_nccl(self.h, buf, rank, world))
+
+    def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False, fused=False):
+        flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0) | (4 if fused else 0)
         tp = tokens.ctypes.data if host_inputs and tokens is not None else _ptr(tokens)
         lp = labels.ctypes.data if host_inputs and labels is not None else _ptr(labels)
         check(lib.zb_run_iteration(self.h, passes, len(passes), tp, lp, flags))
@@ -209,6 +214,15 @@ class Context:
                     local_nonfinite=r.local_nonfinite, partial_nonfinite=r.partial_nonfinite,
                     full_nonfinite=r.full_nonfinite, first=ACTIONS[r.first_action], final=ACTIONS[r.final_action],
                     t=r.t)
+
+
+def nccl_unique_ids(n: int) -> bytes:
+    out = b""
+    for _ in range(n):
+        buf = C.create_string_buffer(128)
+        check(lib.zb_nccl_unique_id(buf))
+        out += buf.raw
+    return out
 
 
 def optim_cfg(lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, clip=1.0, mode="pv") -> zb_optim_cfg_t:
