@@ -93,6 +93,22 @@ __device__ __forceinline__ float gelu_f(float x) {
   float t = tanhf(c * (x + 0.044715f * x * x * x));
   return 0.5f * x * (1.f + t);
 }
+// Hardware tanh (MUFU.TANH, |rel err| ~ 2^-11): used only where the result is
+// rounded to bf16 (2^-9) anyway; the f32 parity mode keeps tanhf.
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float c = 0.7978845608028654f;
+  return 0.5f * x * (1.f + tanh_approx(c * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+  const float c = 0.7978845608028654f;
+  const float t = tanh_approx(c * (x + 0.044715f * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * x * x);
+}
 __device__ __forceinline__ float gelu_grad_f(float x) {
   const float c = 0.7978845608028654f;
   float t = tanhf(c * (x + 0.044715f * x * x * x));

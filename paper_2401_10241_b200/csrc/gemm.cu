@@ -13,6 +13,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "gemm.h"
 #include "ktimer.h"
@@ -47,7 +48,7 @@ __device__ __forceinline__ void epi8(const EpiArgs& e, int64_t row, int col, flo
     Vec8<TO>::store(c, v);
     float g[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) g[i] = gelu_f(v[i]);
+    for (int i = 0; i < 8; ++i) g[i] = std::is_same<TO, bf16>::value ? gelu_fast(v[i]) : gelu_f(v[i]);
     Vec8<TO>::store(reinterpret_cast<TO*>(e.aux) + row * e.ldaux + col, g);
   } else if (EPI == EPI_RESID) {
     float r[8];
@@ -59,7 +60,7 @@ __device__ __forceinline__ void epi8(const EpiArgs& e, int64_t row, int col, flo
     float u[8];
     Vec8<TO>::load(reinterpret_cast<const TO*>(e.aux) + row * e.ldaux + col, u);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] *= gelu_grad_f(u[i]);
+    for (int i = 0; i < 8; ++i) v[i] *= std::is_same<TO, bf16>::value ? gelu_grad_fast(u[i]) : gelu_grad_f(u[i]);
     Vec8<TO>::store(c, v);
   }
 }
@@ -67,6 +68,8 @@ __device__ __forceinline__ void epi8(const EpiArgs& e, int64_t row, int col, flo
 // ------------------------------------------------------------------ tcgen05 kernel
 namespace tc {
 constexpr int BM = 128, BK = 64;
+constexpr int kThreads = 384;     // warps 0-3: TMA, MMA, TMEM alloc, idle; warps 4-11: epilogue
+constexpr int kEpiThreads = 256;
 constexpr int A_BYTES = BM * BK * 2;
 template <int BN> struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
@@ -88,7 +91,7 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mt
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI, typename TO>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const EpiArgs ep,
               int M, int N, int K) {
   using C = Cfg<BN>;
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], 128);
+      sm100::mbar_init(&tempty[i], kEpiThreads);
     }
     sm100::fence_mbar_init();
   }
@@ -194,7 +197,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
-    const int ew = warp - 4;
+    // 8 epilogue warps: warp w reads TMEM lanes 32*(w%4).. (hardware lane quadrant) and
+    // one half of the tile's columns, so two warps per SMSP hide each other's latency
+    const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;
     int acc = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(256, 1)
       sm100::mbar_wait(&tfull[acc], aph);
       sm100::tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
         uint32_t r[32];
         sm100::tmem_ld32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
         sm100::tmem_ld_wait();
@@ -228,6 +233,174 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   sm100::tc_fence_after();
   if (warp == 2) sm100::tmem_dealloc<C::TMEM_COLS>(tbase);
+}
+
+// ------------------------------------------------------------------ tcgen05 kernel, CTA pair
+// Two CTAs of a cluster (one TPC) compute a 256 x BN tile with tcgen05.mma.cta_group::2:
+// CTA r holds rows [128r, 128r+128) of A and D and columns [r BN/2, (r+1) BN/2) of B,
+// so each SM stages only half of the B tile (32 KB / stage at BN = 256, 6 stages) and
+// L2 -> SM traffic per output element drops by a third versus the 1-CTA kernel.
+// The leader (rank 0) issues every MMA; both CTAs' TMA transactions land on the
+// leader's full barrier; the leader's commits multicast to both CTAs' barriers; both
+// CTAs' epilogues release the accumulator on the leader's tempty barrier.
+template <int BN> struct Cfg2 {
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN >= 256) ? 6 : 8;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+template <int BN, bool A_MN, bool B_MN, int EPI, typename TO>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const EpiArgs ep,
+               int M, int N, int K) {
+  using C = Cfg2<BN>;
+  constexpr int BM2 = 2 * BM;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+  const bool leader = rank == 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      sm100::mbar_init(&full[i], 2);  // one arrival per CTA (+ both CTAs' TMA bytes)
+      sm100::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&tfull[i], 1);
+      sm100::mbar_init(&tempty[i], 2 * kEpiThreads);  // both CTAs' epilogue threads
+    }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmA);
+    sm100::tma_prefetch(&tmB);
+  }
+  if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tslot);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  const int num_m = (M + BM2 - 1) / BM2, num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n, nk = (K + BK - 1) / BK;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int t = cid; t < tiles; t += ncl) {
+        int mt, nt;
+        tile_coords(t, num_m, num_n, mt, nt);
+        const int m0 = mt * BM2 + static_cast<int>(rank) * BM, n0 = nt * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < nk; ++kb) {
+          sm100::mbar_wait(&empty[stage], ph ^ 1);
+          const uint32_t fbar = sm100::map_to_cta(&full[stage], 0);
+          if (leader)
+            sm100::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE);
+          else
+            sm100::mbar_arrive_cluster(fbar);
+          uint8_t* sa = smem + stage * C::STAGE;
+          uint8_t* sb = sa + A_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            sm100::tma_load_2d_pair(sa, &tmA, fbar, k0, m0);
+          } else {
+            sm100::tma_load_2d_pair(sa, &tmA, fbar, m0, k0);
+            sm100::tma_load_2d_pair(sa + 8192, &tmA, fbar, m0 + 64, k0);
+          }
+          if (!B_MN) {
+            sm100::tma_load_2d_pair(sb, &tmB, fbar, k0, n0);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 128; ++i) sm100::tma_load_2d_pair(sb + i * 8192, &tmB, fbar, n0 + 64 * i, k0);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = sm100::idesc_bf16(BM2, BN, A_MN, B_MN);
+      int stage = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int t = cid; t < tiles; t += ncl) {
+        sm100::mbar_wait(&tempty[acc], aph ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d = tbase + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          sm100::mbar_wait(&full[stage], ph);
+          sm100::tc_fence_after();
+          const uint32_t sa = sm100::smem_addr(smem + stage * C::STAGE);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = A_MN ? sm100::smem_desc(sa + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
+                                     : sm100::smem_desc(sa + kk * 32, 16, 1024, sm100::kSwizzle128B);
+            const uint64_t bd = B_MN ? sm100::smem_desc(sb + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
+                                     : sm100::smem_desc(sb + kk * 32, 16, 1024, sm100::kSwizzle128B);
+            sm100::mma_bf16_ss_pair(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          sm100::mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+        sm100::mma_commit_pair(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows)
+    const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;  // see the 1-CTA kernel
+    const uint32_t te0 = sm100::map_to_cta(&tempty[0], 0), te1 = sm100::map_to_cta(&tempty[1], 0);
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = cid; t < tiles; t += ncl) {
+      int mt, nt;
+      tile_coords(t, num_m, num_n, mt, nt);
+      const int64_t row = static_cast<int64_t>(mt) * BM2 + static_cast<int>(rank) * BM + ew * 32 + lane;
+      sm100::mbar_wait(&tfull[acc], aph);
+      sm100::tc_fence_after();
+#pragma unroll 1
+      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
+        uint32_t r[32];
+        sm100::tmem_ld32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
+        sm100::tmem_ld_wait();
+        const int col0 = nt * BN + c * 32;
+        if (row < M) {
+          float* v = reinterpret_cast<float*>(r);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (col0 + g * 8 < N) epi8<EPI, TO>(ep, row, col0 + g * 8, v + g * 8);
+        }
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive_cluster(acc == 0 ? te0 : te1);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  sm100::cluster_sync();
+  sm100::tc_fence_after();
+  if (warp == 2) sm100::tmem_dealloc_pair<C::TMEM_COLS>(tbase);
 }
 }  // namespace tc
 
@@ -343,19 +516,55 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap tb = B_MN ? make_tmap(g.B, g.N, g.K, g.ldb, 64, 64) : make_tmap(g.B, g.K, g.N, g.ldb, 64, BN);
   const int tiles = static_cast<int>(ceil_div(g.M, tc::BM) * ceil_div(g.N, BN));
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, 256, C::SMEM, st>>>(ta, tb, g.ep, g.M, g.N, g.K);
+  kern<<<grid, tc::kThreads, C::SMEM, st>>>(ta, tb, g.ep, g.M, g.N, g.K);
   ZB_LAUNCH_CHECK();
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
+  using C = tc::Cfg2<BN>;
+  auto kern = tc::k_gemm_tc2<BN, A_MN, B_MN, EPI, bf16>;
+  static bool attr = false;
+  if (!attr) {
+    ZB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  CUtensorMap ta = A_MN ? make_tmap(g.A, g.M, g.K, g.lda, 64, 64) : make_tmap(g.A, g.K, g.M, g.lda, 64, tc::BM);
+  CUtensorMap tb = B_MN ? make_tmap(g.B, g.N, g.K, g.ldb, 64, 64) : make_tmap(g.B, g.K, g.N, g.ldb, 64, BN / 2);
+  const int tiles = static_cast<int>(ceil_div(g.M, 2 * tc::BM) * ceil_div(g.N, BN));
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  kern<<<grid, tc::kThreads, C::SMEM, st>>>(ta, tb, g.ep, g.M, g.N, g.K);
+  ZB_LAUNCH_CHECK();
+}
+
+// 2-CTA tiles when the problem fills at least one 256 x 256 pair tile; env ZB_GEMM_1CTA=1 forces 1-CTA.
+static bool use_pair(const GemmArgs& g) {
+  static int force1 = -1;
+  if (force1 < 0) {
+    const char* e = getenv("ZB_GEMM_1CTA");
+    force1 = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !force1 && g.M >= 256 && g.N >= 256;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static void launch_any(const GemmArgs& g, cudaStream_t st) {
+  if (BN == 256 && use_pair(g))
+    launch_tc2<BN, A_MN, B_MN, EPI>(g, st);
+  else
+    launch_tc<BN, A_MN, B_MN, EPI>(g, st);
 }
 
 template <int BN, bool A_MN, bool B_MN>
 static void dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
   switch (g.epi) {
-    case EPI_STORE: return launch_tc<BN, A_MN, B_MN, EPI_STORE>(g, st);
-    case EPI_BIAS_GELU: return launch_tc<BN, A_MN, B_MN, EPI_BIAS_GELU>(g, st);
-    case EPI_RESID: return launch_tc<BN, A_MN, B_MN, EPI_RESID>(g, st);
-    case EPI_GELU_BWD: return launch_tc<BN, A_MN, B_MN, EPI_GELU_BWD>(g, st);
-    case EPI_F32_ACC: return launch_tc<BN, A_MN, B_MN, EPI_F32_ACC>(g, st);
-    case EPI_F32_STORE: return launch_tc<BN, A_MN, B_MN, EPI_F32_STORE>(g, st);
+    case EPI_STORE: return launch_any<BN, A_MN, B_MN, EPI_STORE>(g, st);
+    case EPI_BIAS_GELU: return launch_any<BN, A_MN, B_MN, EPI_BIAS_GELU>(g, st);
+    case EPI_RESID: return launch_any<BN, A_MN, B_MN, EPI_RESID>(g, st);
+    case EPI_GELU_BWD: return launch_any<BN, A_MN, B_MN, EPI_GELU_BWD>(g, st);
+    case EPI_F32_ACC: return launch_any<BN, A_MN, B_MN, EPI_F32_ACC>(g, st);
+    case EPI_F32_STORE: return launch_any<BN, A_MN, B_MN, EPI_F32_STORE>(g, st);
   }
   throw CudaError("gemm: bad epilogue");
 }
