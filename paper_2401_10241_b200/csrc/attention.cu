@@ -18,6 +18,16 @@
 namespace zb {
 void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const void* o, const void* dout,
                         const float* lse, void* dqkv, float* delta, cudaStream_t st);
+bool attention_fwd_tc(const AttnShape& sh, const void* qkv, void* o, float* lse, cudaStream_t st);
+// ZB_ATTN_LEGACY=1 selects the mma.sync kernels (comparison / debugging)
+static bool legacy_attention() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZB_ATTN_LEGACY");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
 namespace attn {
 
 constexpr int TILE = 64;
@@ -580,6 +590,10 @@ void attention_fwd(const AttnShape& sh, DType dt, const void* qkv, void* o, floa
   if (sh.b <= 0 || sh.s <= 0 || sh.a <= 0) return;
   // algorithmic causal FLOPs: Q K^T and P V over the lower triangle
   const int tk = ktimer::start(ktimer::ATTN_FWD, 2.0 * sh.b * sh.a * static_cast<double>(sh.s) * sh.s * sh.d, st);
+  if (dt == DT_BF16 && !legacy_attention() && attention_fwd_tc(sh, qkv, o, lse, st)) {
+    ktimer::stop(tk, st);
+    return;
+  }
   switch (sh.d) {
     case 64: dt == DT_BF16 ? attn::fwd_bf16<64>(sh, qkv, o, lse, st) : attn::fwd_f32<64>(sh, qkv, o, lse, st); break;
     case 96: dt == DT_BF16 ? attn::fwd_bf16<96>(sh, qkv, o, lse, st) : attn::fwd_f32<96>(sh, qkv, o, lse, st); break;

@@ -487,7 +487,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D bf16 tensor map over a row-major [outer, inner] view with leading dim ld.
-static CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
                              uint32_t box_outer) {
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15))
     throw CudaError("gemm: operand must be 16-byte aligned with a 16-byte multiple row pitch");

@@ -9,7 +9,8 @@ from zbtest_util import cuda_available
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA GPU")]
 
-CASES = [(1, 1024, 1, 64), (2, 256, 3, 64), (2, 192, 2, 96), (1, 256, 2, 128), (2, 200, 2, 96), (1, 130, 1, 128)]
+CASES = [(1, 1024, 1, 64), (2, 256, 3, 64), (2, 192, 2, 96), (1, 256, 2, 128), (2, 200, 2, 96), (1, 130, 1, 128),
+         (2, 384, 2, 96), (1, 1024, 2, 128), (3, 128, 1, 96)]
 
 
 def rel(x, ref):
