@@ -19,6 +19,8 @@ namespace zb {
 void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const void* o, const void* dout,
                         const float* lse, void* dqkv, float* delta, cudaStream_t st);
 bool attention_fwd_tc(const AttnShape& sh, const void* qkv, void* o, float* lse, cudaStream_t st);
+bool attention_bwd_tc(const AttnShape& sh, const void* qkv, const void* dout, const float* lse, void* dqkv,
+                      const float* delta, cudaStream_t st);
 // ZB_ATTN_LEGACY=1 selects the mma.sync kernels (comparison / debugging)
 static bool legacy_attention() {
   static int v = -1;
@@ -626,6 +628,7 @@ void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const vo
     attn::k_delta<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(o), static_cast<const float*>(dout), delta,
                                                  sh.s, sh.a, sh.d, rows);
   ZB_LAUNCH_CHECK();
+  if (dt == DT_BF16 && !legacy_attention() && attention_bwd_tc(sh, qkv, dout, lse, dqkv, delta, st)) return;
   switch (sh.d) {
     case 64:
       return dt == DT_BF16 ? attn::bwd_bf16<64>(sh, qkv, dout, lse, dqkv, delta, st)

@@ -1,0 +1,456 @@
+// Causal flash-attention BACKWARD on tcgen05 (bf16, s % 128 == 0), deterministic:
+// one kernel owns dK / dV of a 128-key block, another owns dQ of a 128-query block.
+//
+// dK/dV kernel (per key block kb, loop over 64-query blocks i >= 2 kb):
+//   MMA   S^T = K Q_i^T, dP^T = V dO_i^T             (SS, M = 128 keys, N = 64 queries)
+//   warps 4-11 (key row per thread pair, one query half each):
+//         P^T = exp2(S^T c - lse_q log2 e) (causal), dS^T = P^T (dP^T - D_q),
+//         both written back as bf16 into TMEM over their own S^T / dP^T columns
+//   MMA   dV += P^T dO_i, dK += dS^T Q_i              (TS: A from TMEM, B = dO_i / Q_i MN-major)
+//   S^T / dP^T are double-buffered (2 x 128 columns) so block i+1's products overlap
+//   block i's elementwise work; dK, dV accumulate in TMEM (2 x D columns).
+// dQ kernel (per query block, loop over 64-key blocks j <= 2 qb + 1):
+//   MMA   S = Q K_j^T, dP = dO V_j^T;  dS = P (dP - D) -> TMEM;  dQ += dS K_j (TS).
+// Q, dO, L, D of a query block arrive by TMA / bulk copy in a 3-stage ring.
+#include <math.h>
+
+#include "attention.h"
+#include "gemm.h"
+#include "sm100.cuh"
+
+namespace zb {
+namespace attn_bwd_tc {
+
+constexpr float LOG2E = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ================================================================== dK / dV
+template <int D> struct DkdvCfg {
+  static constexpr int ATOMS = (D + 63) / 64;
+  static constexpr int KV_TILE = ATOMS * 16384;  // 128 rows
+  static constexpr int Q_TILE = ATOMS * 8192;    // 64 rows
+  static constexpr int ST = 3;
+  static constexpr int STAGE = 2 * Q_TILE + 1024;  // Q_i, dO_i, L_i[64], D_i[64] (1024-aligned)
+  static constexpr int OFF_K = 0, OFF_V = KV_TILE, OFF_ST = 2 * KV_TILE;
+  static constexpr int OFF_BAR = OFF_ST + ST * STAGE;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    k_dkdv_tc(const __grid_constant__ CUtensorMap tmKV, const __grid_constant__ CUtensorMap tmQ,
+              const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse,
+              const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2) {
+  using C = DkdvCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* st_full = bar + 1;   // [3]
+  uint64_t* st_empty = bar + 4;  // [3]
+  uint64_t* sp_full = bar + 7;   // [2]
+  uint64_t* sp_empty = bar + 9;  // [2]
+  uint64_t* ds_full = bar + 11;  // [2]
+  uint64_t* o_final = bar + 13;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x, hd = blockIdx.y, bb = blockIdx.z;
+  const int h = a * D;
+  const int i0 = 2 * kb, nq = s / 64 - i0;
+  const int row0 = bb * s;
+  const int64_t stat0 = (static_cast<int64_t>(bb) * a + hd) * s;
+
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(kv_full, 1);
+    for (int i = 0; i < C::ST; ++i) {
+      sm100::mbar_init(&st_full[i], 1);
+      sm100::mbar_init(&st_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&sp_full[i], 1);
+      sm100::mbar_init(&sp_empty[i], 1);
+      sm100::mbar_init(&ds_full[i], 256);
+    }
+    sm100::mbar_init(o_final, 1);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmKV);
+    sm100::tma_prefetch(&tmQ);
+    sm100::tma_prefetch(&tmDO);
+  }
+  if (warp == 2) sm100::tmem_alloc<512>(tslot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t t_dk = tbase + 256, t_dv = tbase + 256 + D;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA / bulk copies
+      sm100::mbar_arrive_expect_tx(kv_full, 2 * C::KV_TILE);
+      for (int at = 0; at < C::ATOMS; ++at) {
+        sm100::tma_load_2d(smem + C::OFF_K + at * 16384, &tmKV, kv_full, h + hd * D + 64 * at, row0 + kb * 128);
+        sm100::tma_load_2d(smem + C::OFF_V + at * 16384, &tmKV, kv_full, 2 * h + hd * D + 64 * at, row0 + kb * 128);
+      }
+      for (int n = 0; n < nq; ++n) {
+        const int i = i0 + n, st = n % C::ST;
+        sm100::mbar_wait(&st_empty[st], ((n / C::ST) & 1) ^ 1);
+        uint8_t* sg = smem + C::OFF_ST + st * C::STAGE;
+        sm100::mbar_arrive_expect_tx(&st_full[st], 2 * C::Q_TILE + 512);
+        for (int at = 0; at < C::ATOMS; ++at) {
+          sm100::tma_load_2d(sg + at * 8192, &tmQ, &st_full[st], hd * D + 64 * at, row0 + i * 64);
+          sm100::tma_load_2d(sg + C::Q_TILE + at * 8192, &tmDO, &st_full[st], hd * D + 64 * at, row0 + i * 64);
+        }
+        sm100::bulk_load(sg + 2 * C::Q_TILE, lse + stat0 + i * 64, 256, &st_full[st]);
+        sm100::bulk_load(sg + 2 * C::Q_TILE + 256, delta + stat0 + i * 64, 256, &st_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA
+      constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idesc_g = sm100::idesc_bf16(128, D, false, true);
+      const uint32_t sk = sm100::smem_addr(smem + C::OFF_K), sv = sm100::smem_addr(smem + C::OFF_V);
+      auto issue_grad = [&](int n) {
+        const int b = n & 1, st = n % C::ST;
+        sm100::mbar_wait(&ds_full[b], (n >> 1) & 1);
+        sm100::tc_fence_after();
+        const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+        const uint32_t sdo = sq + C::Q_TILE;
+        const uint32_t tp = tbase + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries: halves live at columns [0,16) and [32,48)
+          const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
+          sm100::mma_bf16_ts(t_dv, tp + acol, sm100::smem_desc(sdo + kk * 2048, 8192, 1024, sm100::kSwizzle128B),
+                             idesc_g, (n | kk) != 0 ? 1u : 0u);
+          sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::smem_desc(sq + kk * 2048, 8192, 1024, sm100::kSwizzle128B),
+                             idesc_g, (n | kk) != 0 ? 1u : 0u);
+        }
+        sm100::mma_commit(&sp_empty[b]);
+        sm100::mma_commit(&st_empty[st]);
+        if (n == nq - 1) sm100::mma_commit(o_final);
+      };
+      sm100::mbar_wait(kv_full, 0);
+      for (int n = 0; n < nq; ++n) {
+        const int b = n & 1, st = n % C::ST;
+        sm100::mbar_wait(&st_full[st], (n / C::ST) & 1);
+        sm100::mbar_wait(&sp_empty[b], ((n >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+        const uint32_t sdo = sq + C::Q_TILE;
+        const uint32_t tp = tbase + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+          sm100::mma_bf16_ss(tp, sm100::smem_desc(sk + oa, 16, 1024, sm100::kSwizzle128B),
+                             sm100::smem_desc(sq + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
+          sm100::mma_bf16_ss(tp + 64, sm100::smem_desc(sv + oa, 16, 1024, sm100::kSwizzle128B),
+                             sm100::smem_desc(sdo + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
+        }
+        sm100::mma_commit(&sp_full[b]);
+        if (n > 0) issue_grad(n - 1);
+      }
+      issue_grad(nq - 1);
+    }
+  } else if (warp >= 4) {  // ---------------- elementwise: P^T, dS^T
+    const int qw = warp & 3, hf = (warp - 4) >> 2;
+    const int r = qw * 32 + lane;
+    const int key = kb * 128 + r;
+    const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    for (int n = 0; n < nq; ++n) {
+      const int i = i0 + n, b = n & 1, st = n % C::ST;
+      const float* Ls = reinterpret_cast<const float*>(smem + C::OFF_ST + st * C::STAGE + 2 * C::Q_TILE);
+      const float* Ds = Ls + 64;
+      sm100::mbar_wait(&sp_full[b], (n >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t sr[32], dr[32];
+      const uint32_t tp = tbase + b * 128 + lane_off;
+      sm100::tmem_ld32(tp + 32 * hf, sr);
+      sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
+      sm100::tmem_ld_wait();
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        float pv[2], dv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int qc = 32 * hf + c + e;
+          const int q = i * 64 + qc;
+          const float p = q >= key ? sm100::ex2(__uint_as_float(sr[c + e]) * scale_log2 - Ls[qc] * LOG2E) : 0.f;
+          pv[e] = p;
+          dv[e] = p * (__uint_as_float(dr[c + e]) - Ds[qc]);
+        }
+        pk[c >> 1] = pack_bf16(pv[0], pv[1]);
+        dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+      }
+      sm100::tmem_st16(tp + 32 * hf, pk);       // P^T over this half's S^T columns
+      sm100::tmem_st16(tp + 64 + 32 * hf, dk);  // dS^T over this half's dP^T columns
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&ds_full[b]);
+    }
+    sm100::mbar_wait(o_final, 0);
+    sm100::tc_fence_after();
+    bf16* row = dqkv + (static_cast<int64_t>(row0) + key) * (3 * h) + hd * D;
+#pragma unroll 1
+    for (int c = hf; c < D / 32; c += 2) {
+      uint32_t v[32];
+      sm100::tmem_ld32(t_dk + lane_off + c * 32, v);
+      sm100::tmem_ld_wait();
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
+        u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
+        u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
+        u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
+        *reinterpret_cast<uint4*>(row + h + c * 32 + g * 8) = u;
+      }
+      sm100::tmem_ld32(t_dv + lane_off + c * 32, v);
+      sm100::tmem_ld_wait();
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(v[8 * g]), __uint_as_float(v[8 * g + 1]));
+        u.y = pack_bf16(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
+        u.z = pack_bf16(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
+        u.w = pack_bf16(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
+        *reinterpret_cast<uint4*>(row + 2 * h + c * 32 + g * 8) = u;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 2) sm100::tmem_dealloc<512>(tbase);
+}
+
+// ================================================================== dQ
+template <int D> struct DqCfg {
+  static constexpr int ATOMS = (D + 63) / 64;
+  static constexpr int Q_TILE = ATOMS * 16384;   // 128 rows
+  static constexpr int KV_TILE = ATOMS * 8192;   // 64 rows
+  static constexpr int ST = 3;
+  static constexpr int STAGE = 2 * KV_TILE;      // K_j, V_j
+  static constexpr int OFF_Q = 0, OFF_DO = Q_TILE, OFF_ST = 2 * Q_TILE;
+  static constexpr int OFF_BAR = OFF_ST + ST * STAGE;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    k_dq_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+            const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse, const float* __restrict__ delta,
+            bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2) {
+  using C = DqCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* st_full = bar + 1;   // [3]
+  uint64_t* st_empty = bar + 4;  // [3]
+  uint64_t* sp_full = bar + 7;   // [2]
+  uint64_t* sp_empty = bar + 9;  // [2]
+  uint64_t* ds_full = bar + 11;  // [2]
+  uint64_t* o_final = bar + 13;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = s / 128;
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
+  const int hd = blockIdx.y, bb = blockIdx.z;
+  const int h = a * D;
+  const int nkv = 2 * qb + 2;
+  const int row0 = bb * s;
+
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(q_full, 1);
+    for (int i = 0; i < C::ST; ++i) {
+      sm100::mbar_init(&st_full[i], 1);
+      sm100::mbar_init(&st_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&sp_full[i], 1);
+      sm100::mbar_init(&sp_empty[i], 1);
+      sm100::mbar_init(&ds_full[i], 256);
+    }
+    sm100::mbar_init(o_final, 1);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tmQ);
+    sm100::tma_prefetch(&tmKV);
+    sm100::tma_prefetch(&tmDO);
+  }
+  if (warp == 2) sm100::tmem_alloc<512>(tslot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t t_dq = tbase + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA
+      sm100::mbar_arrive_expect_tx(q_full, 2 * C::Q_TILE);
+      for (int at = 0; at < C::ATOMS; ++at) {
+        sm100::tma_load_2d(smem + C::OFF_Q + at * 16384, &tmQ, q_full, hd * D + 64 * at, row0 + qb * 128);
+        sm100::tma_load_2d(smem + C::OFF_DO + at * 16384, &tmDO, q_full, hd * D + 64 * at, row0 + qb * 128);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % C::ST;
+        sm100::mbar_wait(&st_empty[st], ((j / C::ST) & 1) ^ 1);
+        uint8_t* sg = smem + C::OFF_ST + st * C::STAGE;
+        sm100::mbar_arrive_expect_tx(&st_full[st], 2 * C::KV_TILE);
+        for (int at = 0; at < C::ATOMS; ++at) {
+          sm100::tma_load_2d(sg + at * 8192, &tmKV, &st_full[st], h + hd * D + 64 * at, row0 + j * 64);
+          sm100::tma_load_2d(sg + C::KV_TILE + at * 8192, &tmKV, &st_full[st], 2 * h + hd * D + 64 * at,
+                             row0 + j * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA
+      constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idesc_g = sm100::idesc_bf16(128, D, false, true);
+      const uint32_t sq = sm100::smem_addr(smem + C::OFF_Q), sdo = sm100::smem_addr(smem + C::OFF_DO);
+      auto issue_dq = [&](int j) {
+        const int b = j & 1, st = j % C::ST;
+        sm100::mbar_wait(&ds_full[b], (j >> 1) & 1);
+        sm100::tc_fence_after();
+        const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+        const uint32_t tp = tbase + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
+          sm100::mma_bf16_ts(t_dq, tp + acol, sm100::smem_desc(skj + kk * 2048, 8192, 1024, sm100::kSwizzle128B),
+                             idesc_g, (j | kk) != 0 ? 1u : 0u);
+        }
+        sm100::mma_commit(&sp_empty[b]);
+        sm100::mma_commit(&st_empty[st]);
+        if (j == nkv - 1) sm100::mma_commit(o_final);
+      };
+      sm100::mbar_wait(q_full, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int b = j & 1, st = j % C::ST;
+        sm100::mbar_wait(&st_full[st], (j / C::ST) & 1);
+        sm100::mbar_wait(&sp_empty[b], ((j >> 1) & 1) ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+        const uint32_t svj = skj + C::KV_TILE;
+        const uint32_t tp = tbase + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+          sm100::mma_bf16_ss(tp, sm100::smem_desc(sq + oa, 16, 1024, sm100::kSwizzle128B),
+                             sm100::smem_desc(skj + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
+          sm100::mma_bf16_ss(tp + 64, sm100::smem_desc(sdo + oa, 16, 1024, sm100::kSwizzle128B),
+                             sm100::smem_desc(svj + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
+        }
+        sm100::mma_commit(&sp_full[b]);
+        if (j > 0) issue_dq(j - 1);
+      }
+      issue_dq(nkv - 1);
+    }
+  } else if (warp >= 4) {  // ---------------- elementwise: dS
+    const int qw = warp & 3, hf = (warp - 4) >> 2;
+    const int r = qw * 32 + lane;
+    const int q = qb * 128 + r;
+    const int64_t si = (static_cast<int64_t>(bb) * a + hd) * s + q;
+    const float L2 = lse[si] * LOG2E, Dq = delta[si];
+    const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    for (int j = 0; j < nkv; ++j) {
+      const int b = j & 1;
+      sm100::mbar_wait(&sp_full[b], (j >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t sr[32], dr[32];
+      const uint32_t tp = tbase + b * 128 + lane_off;
+      sm100::tmem_ld32(tp + 32 * hf, sr);
+      sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
+      sm100::tmem_ld_wait();
+      uint32_t dk[16];
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) {
+        float dv[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = j * 64 + 32 * hf + c + e;
+          const float p = key <= q ? sm100::ex2(__uint_as_float(sr[c + e]) * scale_log2 - L2) : 0.f;
+          dv[e] = p * (__uint_as_float(dr[c + e]) - Dq);
+        }
+        dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+      }
+      sm100::tmem_st16(tp + 32 * hf, dk);  // dS over this half's S columns
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&ds_full[b]);
+    }
+    sm100::mbar_wait(o_final, 0);
+    sm100::tc_fence_after();
+    bf16* row = dqkv + (static_cast<int64_t>(row0) + q) * (3 * h) + hd * D;
+#pragma unroll 1
+    for (int c = hf; c < D / 32; c += 2) {
+      uint32_t v[32];
+      sm100::tmem_ld32(t_dq + lane_off + c * 32, v);
+      sm100::tmem_ld_wait();
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
+        u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
+        u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
+        u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
+        *reinterpret_cast<uint4*>(row + c * 32 + g * 8) = u;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 2) sm100::tmem_dealloc<512>(tbase);
+}
+
+}  // namespace attn_bwd_tc
+
+template <int D>
+static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout, const float* lse, void* dqkv,
+                          const float* delta, cudaStream_t st) {
+  using C1 = attn_bwd_tc::DkdvCfg<D>;
+  using C2 = attn_bwd_tc::DqCfg<D>;
+  static bool attr = false;
+  if (!attr) {
+    ZB_CUDA(cudaFuncSetAttribute(attn_bwd_tc::k_dkdv_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
+    ZB_CUDA(cudaFuncSetAttribute(attn_bwd_tc::k_dq_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
+    attr = true;
+  }
+  const int h = sh.a * D, rows = sh.b * sh.s;
+  const CUtensorMap kv128 = make_tmap(qkv, 3 * h, rows, 3 * h, 64, 128);
+  const CUtensorMap kv64 = make_tmap(qkv, 3 * h, rows, 3 * h, 64, 64);
+  const CUtensorMap do64 = make_tmap(dout, h, rows, h, 64, 64);
+  const CUtensorMap do128 = make_tmap(dout, h, rows, h, 64, 128);
+  const float scale = 1.f / sqrtf(static_cast<float>(D));
+  dim3 grid(sh.s / 128, sh.a, sh.b);
+  attn_bwd_tc::k_dkdv_tc<D><<<grid, 384, C1::SMEM, st>>>(kv128, kv64, do64, lse, delta, static_cast<bf16*>(dqkv),
+                                                         sh.s, sh.a, scale, scale * attn_bwd_tc::LOG2E);
+  ZB_LAUNCH_CHECK();
+  attn_bwd_tc::k_dq_tc<D><<<grid, 384, C2::SMEM, st>>>(kv128, kv64, do128, lse, delta, static_cast<bf16*>(dqkv),
+                                                       sh.s, sh.a, scale, scale * attn_bwd_tc::LOG2E);
+  ZB_LAUNCH_CHECK();
+}
+
+bool attention_bwd_tc(const AttnShape& sh, const void* qkv, const void* dout, const float* lse, void* dqkv,
+                      const float* delta, cudaStream_t st) {
+  if (sh.s % 128 != 0) return false;
+  switch (sh.d) {
+    case 64: bwd_tc_launch<64>(sh, qkv, dout, lse, dqkv, delta, st); return true;
+    case 96: bwd_tc_launch<96>(sh, qkv, dout, lse, dqkv, delta, st); return true;
+    case 128: bwd_tc_launch<128>(sh, qkv, dout, lse, dqkv, delta, st); return true;
+  }
+  return false;
+}
+
+}  // namespace zb
