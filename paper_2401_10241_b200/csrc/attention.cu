@@ -241,17 +241,21 @@ __global__ void __launch_bounds__(NT) k_fwd_bf16(const bf16* __restrict__ qkv, b
 template <typename T>
 __global__ void k_delta(const T* __restrict__ o, const T* __restrict__ dout, float* __restrict__ delta, int s, int a,
                         int d, int rows) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= rows * a) return;
-  const int row = w / a, hd = w % a;  // row in [0, b*s)
-  const int64_t off = static_cast<int64_t>(row) * a * d + hd * d;
+  // one thread per (row, head): d/8 vector loads of each operand summed in order
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(rows) * a) return;
+  const int row = static_cast<int>(t / a), hd = static_cast<int>(t % a);  // row in [0, b*s)
+  const int64_t off = t * d;
   float acc = 0.f;
-  for (int i = lane; i < d; i += 32) acc += to_f(o[off + i]) * to_f(dout[off + i]);
-  acc = warp_sum(acc);
-  if (lane == 0) {
-    const int bb = row / s, q = row % s;
-    delta[(static_cast<int64_t>(bb) * a + hd) * s + q] = acc;
+  for (int i = 0; i < d; i += 8) {
+    float x[8], y[8];
+    Vec8<T>::load(o + off + i, x);
+    Vec8<T>::load(dout + off + i, y);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += x[k] * y[k];
   }
+  const int bb = row / s, q = row % s;
+  delta[(static_cast<int64_t>(bb) * a + hd) * s + q] = acc;
 }
 
 // ------------------------------------------------------------------ backward: dQ
@@ -619,8 +623,7 @@ void attention_bwd(const AttnShape& sh, DType dt, const void* qkv, const void* o
 void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const void* o, const void* dout,
                         const float* lse, void* dqkv, float* delta, cudaStream_t st) {
   const int rows = sh.b * sh.s;
-  const int warps = rows * sh.a;
-  const int blocks = (warps * 32 + 255) / 256;
+  const int blocks = static_cast<int>((static_cast<int64_t>(rows) * sh.a + 255) / 256);
   if (dt == DT_BF16)
     attn::k_delta<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(o), static_cast<const bf16*>(dout), delta,
                                                 sh.s, sh.a, sh.d, rows);

@@ -92,6 +92,58 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_fwd(const T* __restrict__ x, 
   }
 }
 
+// warp-per-row variant for h <= 3072: no block barriers, 4 rows per 128-thread CTA
+template <typename T, int VPL>
+__global__ void __launch_bounds__(128) k_ln_fwd_warp(const T* __restrict__ x, const float* __restrict__ g,
+                                                    const float* __restrict__ b, T* __restrict__ y,
+                                                    float* __restrict__ mean, float* __restrict__ rstd, int rows, int h,
+                                                    float eps) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int nv = h / 8;
+  float v[VPL][8];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv) {
+      Vec8<T>::load(x + row * h + vi * 8, v[k]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += v[k][i];
+    }
+  }
+  const float mu = warp_sum(sum) / h;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    if (lane + 32 * k < nv) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = v[k][i] - mu;
+        q += d * d;
+      }
+    }
+  }
+  const float rs = rsqrtf(warp_sum(q) / h + eps);
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv) {
+      float gg[8], bb[8], o[8];
+      Vec8<float>::load(g + vi * 8, gg);
+      Vec8<float>::load(b + vi * 8, bb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (v[k][i] - mu) * rs * gg[i] + bb[i];
+      Vec8<T>::store(y + row * h + vi * 8, o);
+    }
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
 // ---------------------------------------------------------------- LayerNorm backward
 // dx only, one CTA per row (full parallelism over rows).  The residual-gradient
 // stream stays f32 (resid and dx32, may be null); dx (activation dtype, may
@@ -146,53 +198,138 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_bwd_dx(const float* __restric
   }
 }
 
-// gamma / beta partials: part[c, col] = sum over the rows of chunk c of dy * xhat (resp. dy).
-template <typename T>
-__global__ void k_ln_param_partials(const float* __restrict__ dy, const T* __restrict__ x,
-                                    const float* __restrict__ mean, const float* __restrict__ rstd,
-                                    float* __restrict__ dg_part, float* __restrict__ db_part, int rows, int h) {
-  const int vi = blockIdx.y * blockDim.x + threadIdx.x;
-  if (vi * 8 >= h) return;
-  const int r0 = blockIdx.x * kRowsPerChunk;
-  const int r1 = min(rows, r0 + kRowsPerChunk);
-  float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r = r0; r < r1; ++r) {
-    const float mu = mean[r], rs = rstd[r];
-    float d[8], xv[8];
-    Vec8<float>::load(dy + static_cast<int64_t>(r) * h + vi * 8, d);
-    Vec8<T>::load(x + static_cast<int64_t>(r) * h + vi * 8, xv);
+// Column reductions in one pass: a CTA owns VPC 8-column groups over ALL rows
+// (kColThreads / VPC row lanes, each summing rows lane, lane + RL, ... in order),
+// then a fixed binary tree over the row lanes in shared memory. Deterministic
+// (fixed partition and order), no partial buffers, one launch. VPC is chosen so
+// the grid covers the SMs (colred_vpc).
+constexpr int kColThreads = 512;
+
+template <int VPC, int NACC>
+__device__ __forceinline__ void colred_tree(float (&acc)[NACC][8], float* sm) {
+  constexpr int RL = kColThreads / VPC, W = VPC * 8 + 4;  // +4: spread banks
+  const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      ag[i] += d[i] * ((xv[i] - mu) * rs);
-      ab[i] += d[i];
+  for (int q = 0; q < NACC; ++q)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sm[(q * RL + rl) * W + vec * 8 + i] = acc[q][i];
+  __syncthreads();
+#pragma unroll
+  for (int stride = RL / 2; stride > 0; stride >>= 1) {
+    if (rl < stride) {
+#pragma unroll
+      for (int q = 0; q < NACC; ++q)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[q][i] += sm[(q * RL + rl + stride) * W + vec * 8 + i];
+          sm[(q * RL + rl) * W + vec * 8 + i] = acc[q][i];
+        }
+    }
+    __syncthreads();
+  }
+}
+
+// gamma / beta: gg (+)= sum_r dy * xhat, gb (+)= sum_r dy
+template <typename T, int VPC>
+__global__ void __launch_bounds__(kColThreads) k_ln_param_grads(const float* __restrict__ dy, const T* __restrict__ x,
+                                                                const float* __restrict__ mean,
+                                                                const float* __restrict__ rstd, float* __restrict__ gg,
+                                                                float* __restrict__ gb, int rows, int h, int beta) {
+  constexpr int RL = kColThreads / VPC;
+  extern __shared__ float colsm[];
+  const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
+  const int col = (blockIdx.x * VPC + vec) * 8;
+  const bool valid = col < h;
+  float acc[2][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[0][i] = acc[1][i] = 0.f;
+  if (valid) {
+    int r = rl;
+    for (; r + 3 * RL < rows; r += 4 * RL) {  // four rows of loads in flight per thread
+      float d[4][8], xv[4][8], mu[4], rs[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t rr = r + u * RL;
+        Vec8<float>::load(dy + rr * h + col, d[u]);
+        Vec8<T>::load(x + rr * h + col, xv[u]);
+        mu[u] = mean[rr];
+        rs[u] = rstd[rr];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[0][i] += d[u][i] * ((xv[u][i] - mu[u]) * rs[u]);
+          acc[1][i] += d[u][i];
+        }
+    }
+    for (; r < rows; r += RL) {
+      float d[8], xv[8];
+      Vec8<float>::load(dy + static_cast<int64_t>(r) * h + col, d);
+      Vec8<T>::load(x + static_cast<int64_t>(r) * h + col, xv);
+      const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc[0][i] += d[i] * ((xv[i] - mu) * rs);
+        acc[1][i] += d[i];
+      }
     }
   }
-  Vec8<float>::store(dg_part + static_cast<int64_t>(blockIdx.x) * h + vi * 8, ag);
-  Vec8<float>::store(db_part + static_cast<int64_t>(blockIdx.x) * h + vi * 8, ab);
-}
-
-__global__ void k_reduce_chunks(const float* __restrict__ part, float* __restrict__ out, int nchunks, int n, int beta) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  float acc = 0.f;
-  for (int i = 0; i < nchunks; ++i) acc += part[static_cast<int64_t>(i) * n + c];
-  out[c] = beta ? out[c] + acc : acc;
-}
-
-template <typename T>
-__global__ void k_colsum(const T* __restrict__ y, int64_t ldy, float* __restrict__ part, int rows, int n) {
-  const int vi = blockIdx.y * blockDim.x + threadIdx.x;  // 8-column group
-  if (vi * 8 >= n) return;
-  const int r0 = blockIdx.x * kRowsPerChunk;
-  const int r1 = min(rows, r0 + kRowsPerChunk);
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r = r0; r < r1; ++r) {
-    float v[8];
-    Vec8<T>::load(y + static_cast<int64_t>(r) * ldy + vi * 8, v);
+  colred_tree<VPC, 2>(acc, colsm);
+  if (rl == 0 && valid) {
+    if (beta) {
+      float o[8];
+      Vec8<float>::load(gg + col, o);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] += v[i];
+      for (int i = 0; i < 8; ++i) acc[0][i] += o[i];
+      Vec8<float>::load(gb + col, o);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[1][i] += o[i];
+    }
+    Vec8<float>::store(gg + col, acc[0]);
+    Vec8<float>::store(gb + col, acc[1]);
   }
-  Vec8<float>::store(part + static_cast<int64_t>(blockIdx.x) * n + vi * 8, acc);
+}
+
+template <typename T, int VPC>
+__global__ void __launch_bounds__(kColThreads) k_colsum(const T* __restrict__ y, int64_t ldy, float* __restrict__ out,
+                                                        int rows, int n, int beta) {
+  constexpr int RL = kColThreads / VPC;
+  extern __shared__ float colsm[];
+  const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
+  const int col = (blockIdx.x * VPC + vec) * 8;
+  const bool valid = col < n;
+  float acc[1][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[0][i] = 0.f;
+  if (valid) {
+    int r = rl;
+    for (; r + 7 * RL < rows; r += 8 * RL) {
+      float v[8][8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) Vec8<T>::load(y + static_cast<int64_t>(r + u * RL) * ldy + col, v[u]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[0][i] += v[u][i];
+    }
+    for (; r < rows; r += RL) {
+      float v[8];
+      Vec8<T>::load(y + static_cast<int64_t>(r) * ldy + col, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[0][i] += v[i];
+    }
+  }
+  colred_tree<VPC, 1>(acc, colsm);
+  if (rl == 0 && valid) {
+    if (beta) {
+      float o[8];
+      Vec8<float>::load(out + col, o);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[0][i] += o[i];
+    }
+    Vec8<float>::store(out + col, acc[0]);
+  }
 }
 
 // ---------------------------------------------------------------- embedding
@@ -547,62 +684,121 @@ void ln_dispatch(int h, F&& f) {
 }  // namespace
 
 // ---------------------------------------------------------------- host wrappers
+template <int VPL>
+static void ln_fwd_warp(DType dt, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
+                        int rows, int h, float eps, cudaStream_t st) {
+  const int blocks = (rows + 3) / 4;
+  if (dt == DT_BF16)
+    k_ln_fwd_warp<bf16, VPL><<<blocks, 128, 0, st>>>(static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean,
+                                                     rstd, rows, h, eps);
+  else
+    k_ln_fwd_warp<float, VPL><<<blocks, 128, 0, st>>>(static_cast<const float*>(x), g, b, static_cast<float*>(y),
+                                                      mean, rstd, rows, h, eps);
+}
+
 void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
                    int rows, int h, float eps, cudaStream_t st) {
   if (rows <= 0) return;
   if (h % 8) throw CudaError("layernorm: h must be a multiple of 8");
-  ln_dispatch<0>(h, [&](auto V) {
-    constexpr int VPT = decltype(V)::value;
-    if (dt == DT_BF16)
-      k_ln_fwd<bf16, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean,
-                                                       rstd, h, eps);
-    else
-      k_ln_fwd<float, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const float*>(x), g, b, static_cast<float*>(y),
-                                                        mean, rstd, h, eps);
-  });
+  const int vpl = (h / 8 + 31) / 32;
+  if (vpl <= 2) {
+    ln_fwd_warp<2>(dt, x, g, b, y, mean, rstd, rows, h, eps, st);
+  } else if (vpl <= 6) {
+    ln_fwd_warp<6>(dt, x, g, b, y, mean, rstd, rows, h, eps, st);
+  } else if (vpl <= 9) {
+    ln_fwd_warp<9>(dt, x, g, b, y, mean, rstd, rows, h, eps, st);
+  } else if (vpl <= 12) {
+    ln_fwd_warp<12>(dt, x, g, b, y, mean, rstd, rows, h, eps, st);
+  } else {
+    ln_dispatch<0>(h, [&](auto V) {
+      constexpr int VPT = decltype(V)::value;
+      if (dt == DT_BF16)
+        k_ln_fwd<bf16, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y),
+                                                         mean, rstd, h, eps);
+      else
+        k_ln_fwd<float, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const float*>(x), g, b, static_cast<float*>(y),
+                                                          mean, rstd, h, eps);
+    });
+  }
   ZB_LAUNCH_CHECK();
 }
 
+// 8-column groups per CTA: the widest of 1, 2, 4, 8 that still gives >= ~1 CTA per SM
+static int colred_vpc(int n) {
+  const int groups = n / 8;
+  int vpc = 8;
+  while (vpc > 1 && groups / vpc < 140) vpc >>= 1;
+  return vpc;
+}
+
+template <int VPC>
+static size_t colred_smem(int nacc) {
+  return static_cast<size_t>(nacc) * (kColThreads / VPC) * (VPC * 8 + 4) * sizeof(float);
+}
+
+template <typename F>
+static void colred_dispatch(int vpc, F&& f) {
+  switch (vpc) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    default: return f(std::integral_constant<int, 8>{});
+  }
+}
+
+template <typename K>
+static void allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) ZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
 void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
-                   const float* resid, float* dx32, void* dx, float* dg_part, float* db_part, int rows, int h,
+                   const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta, int rows, int h,
                    cudaStream_t st) {
   if (rows <= 0) return;
-  // 1) gamma / beta chunk partials (reads x before step 2 may overwrite it in place)
-  dim3 pg(n_chunks(rows), (h / 8 + 127) / 128);
-  if (dt == DT_BF16)
-    k_ln_param_partials<bf16><<<pg, 128, 0, st>>>(static_cast<const float*>(dy), static_cast<const bf16*>(x), mean,
-                                                   rstd, dg_part, db_part, rows, h);
-  else
-    k_ln_param_partials<float><<<pg, 128, 0, st>>>(static_cast<const float*>(dy), static_cast<const float*>(x), mean,
-                                                    rstd, dg_part, db_part, rows, h);
+  // 1) gamma / beta grads (reads x before step 2 may overwrite it in place)
+  const int vpc = colred_vpc(h);
+  colred_dispatch(vpc, [&](auto V) {
+    constexpr int VPC = decltype(V)::value;
+    const int grid = (h / 8 + VPC - 1) / VPC;
+    const size_t sm = colred_smem<VPC>(2);
+    if (dt == DT_BF16) {
+      allow_smem(k_ln_param_grads<bf16, VPC>, sm);
+      k_ln_param_grads<bf16, VPC><<<grid, kColThreads, sm, st>>>(dy, static_cast<const bf16*>(x), mean, rstd, gg, gb,
+                                                                 rows, h, beta);
+    } else {
+      allow_smem(k_ln_param_grads<float, VPC>, sm);
+      k_ln_param_grads<float, VPC><<<grid, kColThreads, sm, st>>>(dy, static_cast<const float*>(x), mean, rstd, gg,
+                                                                  gb, rows, h, beta);
+    }
+  });
   ZB_LAUNCH_CHECK();
   // 2) dx, one CTA per row (dy arrives in f32: the dLN GEMM epilogue keeps full precision)
   ln_dispatch<0>(h, [&](auto V) {
     constexpr int VPT = decltype(V)::value;
     if (dt == DT_BF16)
-      k_ln_bwd_dx<bf16, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const float*>(dy), static_cast<const bf16*>(x),
-                                                          mean, rstd, g, resid, dx32, static_cast<bf16*>(dx), h);
+      k_ln_bwd_dx<bf16, VPT><<<rows, LN_THREADS, 0, st>>>(dy, static_cast<const bf16*>(x), mean, rstd, g, resid, dx32,
+                                                          static_cast<bf16*>(dx), h);
     else
-      k_ln_bwd_dx<float, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const float*>(dy),
-                                                           static_cast<const float*>(x), mean, rstd, g, resid, dx32,
-                                                           static_cast<float*>(dx), h);
+      k_ln_bwd_dx<float, VPT><<<rows, LN_THREADS, 0, st>>>(dy, static_cast<const float*>(x), mean, rstd, g, resid,
+                                                           dx32, static_cast<float*>(dx), h);
   });
   ZB_LAUNCH_CHECK();
 }
 
-void reduce_chunks(const float* part, float* out, int nchunks, int n, int beta, cudaStream_t st) {
-  if (n <= 0) return;
-  k_reduce_chunks<<<(n + 255) / 256, 256, 0, st>>>(part, out, nchunks, n, beta);
-  ZB_LAUNCH_CHECK();
-}
-
-void colsum_partials(DType dt, const void* y, int64_t ldy, float* part, int rows, int n, cudaStream_t st) {
+void bias_grad(DType dt, const void* y, int64_t ldy, float* out, int rows, int n, int beta, cudaStream_t st) {
   if (rows <= 0 || n <= 0) return;
-  dim3 grid(n_chunks(rows), (n / 8 + 127) / 128);
-  if (dt == DT_BF16)
-    k_colsum<bf16><<<grid, 128, 0, st>>>(static_cast<const bf16*>(y), ldy, part, rows, n);
-  else
-    k_colsum<float><<<grid, 128, 0, st>>>(static_cast<const float*>(y), ldy, part, rows, n);
+  colred_dispatch(colred_vpc(n), [&](auto V) {
+    constexpr int VPC = decltype(V)::value;
+    const int grid = (n / 8 + VPC - 1) / VPC;
+    const size_t sm = colred_smem<VPC>(1);
+    if (dt == DT_BF16) {
+      allow_smem(k_colsum<bf16, VPC>, sm);
+      k_colsum<bf16, VPC><<<grid, kColThreads, sm, st>>>(static_cast<const bf16*>(y), ldy, out, rows, n, beta);
+    } else {
+      allow_smem(k_colsum<float, VPC>, sm);
+      k_colsum<float, VPC><<<grid, kColThreads, sm, st>>>(static_cast<const float*>(y), ldy, out, rows, n, beta);
+    }
+  });
   ZB_LAUNCH_CHECK();
 }
 

@@ -9,28 +9,23 @@
 
 namespace zb {
 
-constexpr int kRowsPerChunk = 64;  // row chunk of the column-reduction partials
-inline int n_chunks(int rows) { return (rows + kRowsPerChunk - 1) / kRowsPerChunk; }
-
 // LayerNorm forward: y = g * (x - mean) * rstd + b; mean / rstd saved (f32).
 void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
                    int rows, int h, float eps, cudaStream_t st);
-// LayerNorm backward, input part (B) plus per-chunk parameter-grad partials:
+// LayerNorm backward (B) and its parameter grads:
 //   dx = resid + rstd * (gh - mean(gh) - xhat * mean(gh * xhat)), gh = dy * g
-//   dg_part[c, :] = sum over rows of chunk c of dy * xhat; db_part[c, :] = sum dy
-// dy is f32 in both modes; x / resid / dx are in the activation dtype.
-// resid may be null; dx may alias x or resid.
+// dy is f32 in both modes; x is in the activation dtype; dx may alias x.
 // The residual-gradient stream is f32 (resid, dx32; either may be null) and dx
 // (activation dtype) receives the copy the GEMMs consume (DESIGN.md R-grad32).
+// gg / gb (+)= column sums of dy * xhat / dy (beta: accumulate), deterministic
+// (fixed row partition and fixed reduction tree).
 void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
-                   const float* resid, float* dx32, void* dx, float* dg_part, float* db_part, int rows, int h,
+                   const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta, int rows, int h,
                    cudaStream_t st);
 // f32 -> activation dtype row copy (received stage-boundary gradients)
 void convert_rows(DType dt, const float* src, void* dst, int64_t n, cudaStream_t st);
-// part [nchunks, n] f32 -> out[n] = (beta ? out : 0) + sum_c part[c]  (fixed order)
-void reduce_chunks(const float* part, float* out, int nchunks, int n, int beta, cudaStream_t st);
-// Column sums of y [rows, n] (activation dtype) into part [n_chunks(rows), n].
-void colsum_partials(DType dt, const void* y, int64_t ldy, float* part, int rows, int n, cudaStream_t st);
+// out[n] (+)= column sums of y [rows, n] (activation dtype), deterministic (fixed order).
+void bias_grad(DType dt, const void* y, int64_t ldy, float* out, int rows, int n, int beta, cudaStream_t st);
 
 // Embedding: x0[t] = wte[tok[t]] + wpe[t % s]  (wte / wpe f32 master copies)
 void embed_fwd(DType dt, const int32_t* tok, const float* wte, const float* wpe, void* x0, int rows, int s, int h,

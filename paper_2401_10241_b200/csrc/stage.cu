@@ -186,8 +186,6 @@ size_t carve(Ctx& c, uint8_t* base) {
   c.g32_dx = bp.take<float>(T * h);
   c.g32_dx1 = bp.take<float>(T * h);
   c.delta = bp.take<float>(static_cast<size_t>(c.a) * T);
-  c.part_a = bp.take<float>(static_cast<size_t>(n_chunks(c.T)) * 4 * h);
-  c.part_b = bp.take<float>(static_cast<size_t>(n_chunks(c.T)) * h);
   if (c.last) {
     c.logits = bp.take<float>(T * V);
     c.dlogits = bp.take_bytes(T * V * e);
@@ -247,14 +245,12 @@ static void lin_wgrad(Ctx& c, const void* dY, const void* X, float* dW, int M, i
   gemm(g, c.dt, c.stream);
 }
 static void bias_grad(Ctx& c, const void* dY, float* db, int N, int beta) {
-  colsum_partials(c.dt, dY, N, c.part_a, c.T, N, c.stream);
-  reduce_chunks(c.part_a, db, n_chunks(c.T), N, beta, c.stream);
+  zb::bias_grad(c.dt, dY, N, db, c.T, N, beta, c.stream);
 }
 static void ln_bwd(Ctx& c, const float* dy, const void* x, const float* mu, const float* rs, const float* g,
                    const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta) {
-  layernorm_bwd(c.dt, dy, x, mu, rs, g, resid, dx32, dx, c.part_a, c.part_b, c.T, c.h, c.stream);
-  reduce_chunks(c.part_a, gg, n_chunks(c.T), c.h, beta, c.stream);
-  reduce_chunks(c.part_b, gb, n_chunks(c.T), c.h, beta, c.stream);
+  layernorm_bwd(c.dt, dy, x, mu, rs, g, resid, dx32, dx, gg, gb, beta, c.T, c.h,
+                c.stream);
 }
 
 // ------------------------------------------------------------------ F

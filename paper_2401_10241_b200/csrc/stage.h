@@ -8,7 +8,7 @@
 //            X1, LN2, U, G [T, *] + f32 stats; per slot DY [T,h], tokens,
 //            labels; last stage XL, LNF [T,h]
 //   scratch  spare QKV [T,3h] (pointer-swapped with a slot's QKV in B),
-//            dO / dLN [T,h], attention delta, column-sum partials, logits f32
+//            dO / dLN [T,h], attention delta, logits f32
 //            [T,V] + dlogits [T,V] (last stage), loss rows, sort keys,
 //            token / label staging [m,T], optimizer scratch.
 #pragma once
@@ -75,7 +75,7 @@ struct Ctx {
   std::vector<Slot> slots;
   void *spare_qkv = nullptr, *d_o = nullptr, *dlogits = nullptr;
   float* d_ln = nullptr;  // LayerNorm-input gradient, f32 in both modes
-  float *delta = nullptr, *part_a = nullptr, *part_b = nullptr, *logits = nullptr, *loss_rows = nullptr;
+  float *delta = nullptr, *logits = nullptr, *loss_rows = nullptr;
   float *g32_dx = nullptr, *g32_dx1 = nullptr;  // f32 residual-gradient stream of B (R-grad32)
   uint32_t* keys = nullptr;
   int32_t *tok_stage = nullptr, *lab_stage = nullptr;
