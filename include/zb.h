@@ -41,7 +41,8 @@ enum {
   ZB_ECAP = -3,    /* output capacity too small (out_cap < 3*p*m, arena too small)   */
   ZB_ECUDA = -4,   /* CUDA runtime / launch error                                    */
   ZB_ENCCL = -5,   /* NCCL error or libnccl unavailable                              */
-  ZB_ESTATE = -6   /* invalid state: rollback at t = 0, lr*wd == 1, missing passes   */
+  ZB_ESTATE = -6,  /* invalid state: rollback at t = 0, lr*wd == 1, missing passes   */
+  ZB_ETIMEOUT = -7 /* a loopback-transport receive waited longer than 300 s          */
 };
 
 /* ------------------------------------------------------------------------ */
@@ -264,6 +265,21 @@ zb_status_t zb_nccl_unique_id(void* id128);
  * speculative warm-up Fs, which are replayed if the weights change — plan.h)
  * or in zb_post_validate_finish when no iteration follows. */
 zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* ids, int32_t rank, int32_t world);
+
+/* In-process loopback group (test transport for one GPU): world stage
+ * contexts of ONE process attach to the same group and are then driven
+ * exactly like NCCL-attached contexts, each by its own host thread
+ * (zb_run_iteration, zb_post_validate_step / _finish; the calls block only
+ * while waiting for a message from a neighbour, up to 300 s, or
+ * $ZB_LOOPBACK_TIMEOUT_S, -> ZB_ETIMEOUT).
+ * Messages move through device staging buffers owned by the group.  The
+ * group is reference counted: zb_loopback_destroy releases the caller's
+ * reference; attached contexts keep it alive. */
+typedef struct zb_loopback zb_loopback_t;
+zb_status_t zb_loopback_create(int32_t world, zb_loopback_t** out);
+zb_status_t zb_loopback_destroy(zb_loopback_t* group);
+/* rank = the context's stage; world = its p. */
+zb_status_t zb_ctx_attach_loopback(zb_ctx_t* ctx, zb_loopback_t* group, int32_t rank);
 
 const char* zb_last_error(void);
 const char* zb_version(void);

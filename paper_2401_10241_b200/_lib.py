@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libzb.so")
 
-ZB_OK, ZB_EINVAL, ZB_ELIMIT, ZB_ECAP, ZB_ECUDA, ZB_ENCCL, ZB_ESTATE = 0, -1, -2, -3, -4, -5, -6
+ZB_OK, ZB_EINVAL, ZB_ELIMIT, ZB_ECAP, ZB_ECUDA, ZB_ENCCL, ZB_ESTATE, ZB_ETIMEOUT = 0, -1, -2, -3, -4, -5, -6, -7
 ZB_F, ZB_B, ZB_W = 0, 1, 2
 ZB_1F1B, ZB_H1, ZB_H2, ZB_AUTO = 0, 1, 2, 3
 FAMILY = {"1f1b": ZB_1F1B, "zbh1": ZB_H1, "zbh2": ZB_H2, "auto": ZB_AUTO}
@@ -116,6 +116,9 @@ _SIGS = {
     "zb_ctx_read_pv_report": ([_P, C.POINTER(zb_pv_report_t)], _I32),
     "zb_nccl_unique_id": ([_P], _I32),
     "zb_ctx_attach_nccl": ([_P, _P, _I32, _I32], _I32),
+    "zb_loopback_create": ([_I32, C.POINTER(_P)], _I32),
+    "zb_loopback_destroy": ([_P], _I32),
+    "zb_ctx_attach_loopback": ([_P, _P, _I32], _I32),
 }
 
 for _name, (_args, _res) in _SIGS.items():

@@ -180,6 +180,11 @@ class Context:
         buf = C.create_string_buffer(ids, len(ids))
         check(lib.zb_ctx_attach_nccl(self.h, buf, rank, world))
 
+    def attach_loopback(self, group: "Loopback"):
+        """Attach to an in-process loopback group (rank = this context's stage)."""
+        check(lib.zb_ctx_attach_loopback(self.h, group.h, self.stage))
+        self._group = group
+
     def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False, fused=False):
         flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0) | (4 if fused else 0)
         tp = tokens.ctypes.data if host_inputs and tokens is not None else _ptr(tokens)
@@ -214,6 +219,26 @@ class Context:
                     local_nonfinite=r.local_nonfinite, partial_nonfinite=r.partial_nonfinite,
                     full_nonfinite=r.full_nonfinite, first=ACTIONS[r.first_action], final=ACTIONS[r.final_action],
                     t=r.t)
+
+
+class Loopback:
+    """In-process loopback transport group (zb_loopback_t) for p stage contexts on one GPU."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(lib.zb_loopback_create(world, C.byref(h)))
+        self.h, self.world = h, world
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib.zb_loopback_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def nccl_unique_ids(n: int) -> bytes:

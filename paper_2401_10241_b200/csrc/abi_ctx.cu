@@ -531,6 +531,35 @@ extern "C" zb_status_t zb_nccl_unique_id(void* id128) {
   ZB_CATCH
 }
 
+struct zb_loopback {
+  std::shared_ptr<zb::LoopbackGroup> g;
+};
+
+extern "C" zb_status_t zb_loopback_create(int32_t world, zb_loopback_t** out) {
+  ZB_TRY {
+    if (!out || world < 1) return set_error(ZB_EINVAL, "bad loopback arguments");
+    *out = new zb_loopback{loopback_create(world)};
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_loopback_destroy(zb_loopback_t* group) {
+  delete group;
+  return ZB_OK;
+}
+
+extern "C" zb_status_t zb_ctx_attach_loopback(zb_ctx_t* ctx, zb_loopback_t* group, int32_t rank) {
+  ZB_TRY {
+    Ctx* c = C_(ctx);
+    if (!group) return set_error(ZB_EINVAL, "null loopback group");
+    if (rank != c->cfg.stage) return set_error(ZB_EINVAL, "rank must be the context's stage");
+    attach_loopback(*c, group->g, rank);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 extern "C" zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* ids, int32_t rank, int32_t world) {
   ZB_TRY {
     Ctx* c = C_(ctx);

@@ -1,10 +1,11 @@
-// NCCL transport and the multi-process iteration runner (see comm.h, plan.h).
+// Transports (NCCL, in-process loopback) and the multi-stage iteration runner
+// (see comm.h, plan.h).
 //
 // libnccl.so.2 is dlopen'ed on first use (torch's bundled NCCL is normally
 // already loaded, so the same library is shared).  Every adjacent pair has two
 // 2-rank communicators (ACT s->s+1, GRAD s+1->s), each driven by its own
 // stream on each side; cross-stream ordering uses CUDA events recorded on the
-// compute stream.  The runner executes plan::stage_plan op by op:
+// compute stream.  The loopback transport keeps the same channels and streams.  The runner executes plan::stage_plan op by op:
 //   RECV_ACT   act-recv stream waits for "compute reached here" (the slot's previous
 //              user W is enqueued before), receives into the slot input buffer;
 //              the compute stream waits for the receive
@@ -21,8 +22,13 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <string>
 
 #include "abi_util.h"
@@ -85,12 +91,22 @@ enum { C_ACT_TO = 0, C_ACT_FROM = 1, C_GRAD_TO = 2, C_GRAD_FROM = 3 };
 // peer index inside a 2-rank pair communicator: the lower stage is rank 0
 int peer_of(int which) { return (which == C_ACT_TO || which == C_GRAD_FROM) ? 1 : 0; }
 
-void sendb(Comm& cm, int which, const void* buf, size_t bytes) {
-  nck(nccl().send(buf, bytes, kNcclUint8, peer_of(which), cm.comm[which], cm.stream[which]), "ncclSend");
-}
-void recvb(Comm& cm, int which, void* buf, size_t bytes) {
-  nck(nccl().recv(buf, bytes, kNcclUint8, peer_of(which), cm.comm[which], cm.stream[which]), "ncclRecv");
-}
+struct NcclTransport : Transport {
+  void* comm[4] = {nullptr, nullptr, nullptr, nullptr};
+  ~NcclTransport() override {
+    for (auto cm : comm)
+      if (cm) nccl().destroy(cm);
+  }
+  void send(int which, const void* buf, size_t bytes, cudaStream_t st) override {
+    nck(nccl().send(buf, bytes, kNcclUint8, peer_of(which), comm[which], st), "ncclSend");
+  }
+  void recv(int which, void* buf, size_t bytes, cudaStream_t st) override {
+    nck(nccl().recv(buf, bytes, kNcclUint8, peer_of(which), comm[which], st), "ncclRecv");
+  }
+};
+
+void sendb(Comm& cm, int which, const void* buf, size_t bytes) { cm.tx->send(which, buf, bytes, cm.stream[which]); }
+void recvb(Comm& cm, int which, void* buf, size_t bytes) { cm.tx->recv(which, buf, bytes, cm.stream[which]); }
 
 // stream `a` waits for everything enqueued so far on stream `b`
 void order(Comm& cm, cudaStream_t a, cudaStream_t b) {
@@ -101,10 +117,11 @@ void order(Comm& cm, cudaStream_t a, cudaStream_t b) {
 }  // namespace
 
 Comm::~Comm() {
-  for (int i = 0; i < 4; ++i) {
-    if (comm[i]) nccl().destroy(comm[i]);
+  for (int i = 0; i < 4; ++i)
+    if (stream[i]) cudaStreamSynchronize(stream[i]);
+  tx.reset();
+  for (int i = 0; i < 4; ++i)
     if (stream[i]) cudaStreamDestroy(stream[i]);
-  }
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto e : act_buf_free) cudaEventDestroy(e);
   for (auto b : act_buf) cudaFree(b);
@@ -132,17 +149,50 @@ void nccl_unique_id(void* id128) {
   std::memcpy(id128, &id, 128);
 }
 
+namespace {
+// channel streams and the send staging rings of one stage (both transports)
+void setup_comm(Ctx& c, Comm& cm) {
+  const int rank = cm.rank, world = cm.world;
+  const int chans[4] = {rank < world - 1, rank > 0, rank > 0, rank < world - 1};
+  for (int w = 0; w < 4; ++w)
+    if (chans[w] && !cm.stream[w]) ZB_CUDA(cudaStreamCreateWithFlags(&cm.stream[w], cudaStreamNonBlocking));
+  if (rank < world - 1) {
+    for (int i = 0; i < 2; ++i) {
+      void* b = nullptr;
+      ZB_CUDA(cudaMalloc(&b, c.esz * static_cast<size_t>(c.T) * c.h));
+      cm.act_buf.push_back(b);
+      cudaEvent_t e;
+      ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ZB_CUDA(cudaEventRecord(e, c.stream));
+      cm.act_buf_free.push_back(e);
+    }
+  }
+  if (rank > 0) {
+    for (int i = 0; i < 2; ++i) {
+      float* b = nullptr;
+      ZB_CUDA(cudaMalloc(&b, sizeof(float) * static_cast<size_t>(c.T) * c.h));
+      cm.grad_buf.push_back(b);
+      cudaEvent_t e;
+      ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ZB_CUDA(cudaEventRecord(e, c.stream));
+      cm.grad_buf_free.push_back(e);
+    }
+  }
+  ZB_CUDA(cudaMalloc(&cm.scalars, 64 + c.esz * static_cast<size_t>(c.T) * c.h));  // 4 PV messages + discard buffer
+}
+}  // namespace
+
 void attach_nccl(Ctx& c, const void* ids, int rank, int world) {
   auto cm = std::make_unique<Comm>();
   cm->rank = rank;
   cm->world = world;
+  auto tx = std::make_unique<NcclTransport>();
   const char* id = static_cast<const char*>(ids);
   auto init = [&](int which, int pair, bool grad) {
     ncclUniqueId_t u;
     std::memcpy(&u, id + 128 * (grad ? (world - 1 + pair) : pair), 128);
     const int r = (which == C_ACT_TO || which == C_GRAD_FROM) ? 0 : 1;
-    nck(nccl().init(&cm->comm[which], 2, u, r), "ncclCommInitRank");
-    ZB_CUDA(cudaStreamCreateWithFlags(&cm->stream[which], cudaStreamNonBlocking));
+    nck(nccl().init(&tx->comm[which], 2, u, r), "ncclCommInitRank");
   };
   // increasing pair order on every rank: (s-1, s) before (s, s+1) -> no init deadlock
   if (rank > 0) {
@@ -153,29 +203,144 @@ void attach_nccl(Ctx& c, const void* ids, int rank, int world) {
     init(C_ACT_TO, rank, false);
     init(C_GRAD_FROM, rank, true);
   }
-  if (rank < world - 1) {
-    for (int i = 0; i < 2; ++i) {
-      void* b = nullptr;
-      ZB_CUDA(cudaMalloc(&b, c.esz * static_cast<size_t>(c.T) * c.h));
-      cm->act_buf.push_back(b);
-      cudaEvent_t e;
-      ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      ZB_CUDA(cudaEventRecord(e, c.stream));
-      cm->act_buf_free.push_back(e);
+  cm->tx = std::move(tx);
+  setup_comm(c, *cm);
+  c.comm = std::move(cm);
+}
+
+// ---------------------------------------------------------------- in-process loopback transport
+namespace {
+struct LbBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ready = nullptr, freed = nullptr;
+};
+struct LbMsg {
+  int buf;
+  size_t bytes;
+};
+struct LbChannel {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<LbMsg> queue;
+  std::deque<LbBuf> bufs;  // deque: stable references while the channel grows
+  std::vector<int> free_list;
+  ~LbChannel() {
+    for (auto& b : bufs) {
+      if (b.p) cudaFree(b.p);
+      if (b.ready) cudaEventDestroy(b.ready);
+      if (b.freed) cudaEventDestroy(b.freed);
     }
   }
-  if (rank > 0) {
-    for (int i = 0; i < 2; ++i) {
-      float* b = nullptr;
-      ZB_CUDA(cudaMalloc(&b, sizeof(float) * static_cast<size_t>(c.T) * c.h));
-      cm->grad_buf.push_back(b);
-      cudaEvent_t e;
-      ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      ZB_CUDA(cudaEventRecord(e, c.stream));
-      cm->grad_buf_free.push_back(e);
+};
+}  // namespace
+
+struct LoopbackGroup {
+  int world = 1;
+  std::vector<std::unique_ptr<LbChannel>> act, grad;  // [k]: pair (k, k+1)
+};
+
+std::shared_ptr<LoopbackGroup> loopback_create(int world) {
+  auto g = std::make_shared<LoopbackGroup>();
+  g->world = world;
+  for (int k = 0; k + 1 < world; ++k) {
+    g->act.push_back(std::make_unique<LbChannel>());
+    g->grad.push_back(std::make_unique<LbChannel>());
+  }
+  return g;
+}
+
+namespace {
+int loopback_timeout_s() {  // ZB_LOOPBACK_TIMEOUT_S overrides the default 300 s
+  static const int t = [] {
+    const char* e = std::getenv("ZB_LOOPBACK_TIMEOUT_S");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 300;
+  }();
+  return t;
+}
+
+struct LoopbackTransport : Transport {
+  std::shared_ptr<LoopbackGroup> g;
+  int rank = 0;
+  LbChannel& chan(int which) {
+    switch (which) {
+      case C_ACT_TO: return *g->act.at(rank);
+      case C_ACT_FROM: return *g->act.at(rank - 1);
+      case C_GRAD_TO: return *g->grad.at(rank - 1);
+      default: return *g->grad.at(rank);
     }
   }
-  ZB_CUDA(cudaMalloc(&cm->scalars, 64 + c.esz * static_cast<size_t>(c.T) * c.h));  // 2 PV messages + discard buffer
+  void send(int which, const void* buf, size_t bytes, cudaStream_t st) override {
+    LbChannel& ch = chan(which);
+    LbBuf* b = nullptr;
+    int idx = -1;
+    {
+      std::lock_guard<std::mutex> lk(ch.mu);
+      for (size_t i = 0; i < ch.free_list.size(); ++i) {
+        if (ch.bufs[ch.free_list[i]].cap >= bytes) {
+          idx = ch.free_list[i];
+          ch.free_list.erase(ch.free_list.begin() + static_cast<long>(i));
+          break;
+        }
+      }
+      if (idx < 0) {
+        ch.bufs.emplace_back();
+        idx = static_cast<int>(ch.bufs.size()) - 1;
+        LbBuf& nb = ch.bufs.back();
+        nb.cap = bytes < 64 ? 64 : bytes;
+        ZB_CUDA(cudaMalloc(&nb.p, nb.cap));
+        ZB_CUDA(cudaEventCreateWithFlags(&nb.ready, cudaEventDisableTiming));
+        ZB_CUDA(cudaEventCreateWithFlags(&nb.freed, cudaEventDisableTiming));
+      }
+      b = &ch.bufs[idx];
+    }
+    ZB_CUDA(cudaStreamWaitEvent(st, b->freed, 0));  // the previous receiver has copied it out
+    ZB_CUDA(cudaMemcpyAsync(b->p, buf, bytes, cudaMemcpyDeviceToDevice, st));
+    ZB_CUDA(cudaEventRecord(b->ready, st));
+    {
+      std::lock_guard<std::mutex> lk(ch.mu);
+      ch.queue.push_back({idx, bytes});
+    }
+    ch.cv.notify_all();
+  }
+  void recv(int which, void* buf, size_t bytes, cudaStream_t st) override {
+    LbChannel& ch = chan(which);
+    LbMsg msg;
+    LbBuf* b = nullptr;
+    {
+      std::unique_lock<std::mutex> lk(ch.mu);
+      if (!ch.cv.wait_for(lk, std::chrono::seconds(loopback_timeout_s()), [&] { return !ch.queue.empty(); }))
+        throw Error(ZB_ETIMEOUT, "loopback receive timed out (rank " + std::to_string(rank) + ", channel " +
+                                     std::to_string(which) + ")");
+      msg = ch.queue.front();
+      ch.queue.pop_front();
+      b = &ch.bufs[msg.buf];
+    }
+    if (msg.bytes != bytes)
+      throw Error(ZB_EINVAL, "loopback message size mismatch: sent " + std::to_string(msg.bytes) + ", expected " +
+                                 std::to_string(bytes));
+    ZB_CUDA(cudaStreamWaitEvent(st, b->ready, 0));
+    ZB_CUDA(cudaMemcpyAsync(buf, b->p, bytes, cudaMemcpyDeviceToDevice, st));
+    ZB_CUDA(cudaEventRecord(b->freed, st));
+    {
+      std::lock_guard<std::mutex> lk(ch.mu);
+      ch.free_list.push_back(msg.buf);
+    }
+  }
+};
+}  // namespace
+
+void attach_loopback(Ctx& c, const std::shared_ptr<LoopbackGroup>& g, int rank) {
+  if (g->world != c.cfg.p) throw Error(ZB_EINVAL, "loopback group size must equal the context's p");
+  auto cm = std::make_unique<Comm>();
+  cm->rank = rank;
+  cm->world = g->world;
+  auto tx = std::make_unique<LoopbackTransport>();
+  tx->g = g;
+  tx->rank = rank;
+  cm->tx = std::move(tx);
+  setup_comm(c, *cm);
   c.comm = std::move(cm);
 }
 

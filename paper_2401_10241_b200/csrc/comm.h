@@ -1,4 +1,5 @@
-// NCCL P2P transport between adjacent pipeline stages (one process per GPU).
+// P2P transport between adjacent pipeline stages: NCCL (one process per GPU)
+// or an in-process loopback group (p stages on one GPU, one host thread each).
 //
 // libnccl.so.2 is loaded lazily with dlopen (the single-GPU path never needs
 // it).  Every adjacent pair (s, s+1) gets two 2-rank communicators: one for
@@ -14,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "zb.h"
@@ -22,12 +24,33 @@ namespace zb {
 
 struct Ctx;
 
+// Point-to-point transport of one stage.  Channels (which):
+//   0 activations to stage+1, 1 activations from stage-1,
+//   2 gradients to stage-1,   3 gradients from stage+1.
+// send / recv are enqueued on the channel's stream (stream[which]) and are
+// asynchronous with respect to the host; messages on a channel are matched
+// in order.
+struct Transport {
+  virtual ~Transport() = default;
+  virtual void send(int which, const void* buf, size_t bytes, cudaStream_t st) = 0;
+  virtual void recv(int which, void* buf, size_t bytes, cudaStream_t st) = 0;
+};
+
+// In-process loopback group: p contexts of one process (each driven by its
+// own host thread) exchange messages through device staging buffers, so the
+// multi-stage runner below executes unchanged on one GPU.  A send copies the
+// payload into a staging buffer on the sender's channel stream and queues it
+// (never blocks the host: eager semantics); a recv blocks the calling host
+// thread until the matching message is queued (bounded wait, then ZB_EINTERNAL),
+// then copies it out on the receiver's channel stream.
+struct LoopbackGroup;
+std::shared_ptr<LoopbackGroup> loopback_create(int world);
+void attach_loopback(Ctx& c, const std::shared_ptr<LoopbackGroup>& g, int rank);
+
 struct Comm {
   int rank = 0, world = 1;
-  // [0] activations to stage+1, [1] activations from stage-1,
-  // [2] gradients to stage-1,   [3] gradients from stage+1   (nullptr where absent)
-  void* comm[4] = {nullptr, nullptr, nullptr, nullptr};
-  cudaStream_t stream[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::unique_ptr<Transport> tx;
+  cudaStream_t stream[4] = {nullptr, nullptr, nullptr, nullptr};  // per channel (nullptr where absent)
   // send staging ring for activations (written by F, drained by the act-send stream)
   std::vector<void*> act_buf;
   std::vector<cudaEvent_t> act_buf_free;
