@@ -138,7 +138,7 @@ def run_reference(args):
               f"extrapolated to {cfg.L} layers")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * cfg.T * cfg.m / value,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, args.gpus, args.family),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample,
                              "detail": info},
@@ -223,8 +223,9 @@ def run_single(args, cfg):
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    # ---- device-resident timed region (value)
-    lib.zb_dbg_kernel_timing(1, 1)
+    # ---- device-resident timed region (value): no per-kernel events inside
+    nl = C.c_int64()
+    lib.zb_dbg_launch_count(1, C.byref(nl))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
@@ -233,17 +234,30 @@ def run_single(args, cfg):
             step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
-    lib.zb_dbg_kernel_timing(0, 0)
+    lib.zb_dbg_launch_count(0, C.byref(nl))
+    launches = int(nl.value)
     ms = ev0.elapsed_time(ev1) / args.steps
     tokens_per_step = cfg.T * m
     value = tokens_per_step / (ms / 1000.0)
+    # ---- the same K steps again with CUDA events around every GEMM / attention
+    # launch (on the launching stream) for the per-kernel-class roofline
+    lib.zb_dbg_kernel_timing(1, 1)
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev2.record(stream)
+    for i in range(args.warmup, n_steps):
+        step(i)
+    ev3.record(stream)
+    torch.cuda.synchronize()
+    lib.zb_dbg_kernel_timing(0, 0)
+    ms_ev = ev2.elapsed_time(ev3) / args.steps
     kstats = {}
     for cls, name in ((0, "gemm"), (3, "gemm_F"), (4, "gemm_B"), (5, "gemm_W"), (1, "attn_fwd"), (2, "attn_bwd")):
         a, b, n = C.c_double(), C.c_double(), C.c_int64()
         lib.zb_dbg_kernel_timing_read(cls, C.byref(a), C.byref(b), C.byref(n))
         kstats[name] = {"ms_total": a.value / args.steps, "tflops": (b.value / (a.value / 1e3) / 1e12) if a.value else 0,
                         "launches_per_step": n.value / args.steps,
-                        "share_of_step": (a.value / args.steps) / ms if ms else 0}
+                        "share_of_step": (a.value / args.steps) / ms_ev if ms_ev else 0}
     loss = ctx.loss()
     # ---- per-pass times -> predicted bubbles at p=8 (Table 8 analog on B200)
     step(args.warmup, timing=True)
@@ -282,15 +296,16 @@ def run_single(args, cfg):
             "achieved": round(g["tflops"], 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(g["tflops"] / peak, 4) if peak else None, "traffic": None,
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
+            "timing": f"CUDA events around every launch over a second region of the same {args.steps} steps "
+                      f"({ms_ev:.1f} ms/step with the events)",
             "per_class": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in kstats.items()}}
     flops_token = cfg.L * (72 * cfg.h ** 2 + 12 * cfg.s * cfg.h) + 6 * cfg.h * cfg.V
     mfu = value * flops_token / (peaks.get("bf16_tflops", 1680.3) * 1e12)
     line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (zb_synth seeded weights and tokens)",
             "config": workload_config(cfg, 1, args.family),
-            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(sum(v["launches_per_step"] for k, v in
-                                                                         kstats.items() if k in ("gemm", "attn_fwd", "attn_bwd")) * args.steps),
+            "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches,
             "roofline": roof, "model_flops_utilization": round(mfu, 4), "loss": loss,
             "bubble": bubble, "pass_ms": t_pass}
     if not args.no_cpu_baseline:
@@ -351,18 +366,27 @@ def run_pipeline(args, cfg, rank, world, local):
     lab_d = [torch.from_numpy(np.ascontiguousarray(t[..., 1:])).cuda() for t in toks]
     opt = api.optim_cfg(lr=1e-4, mode="pv", clip=1.0)
 
-    def run(family_passes, fused, steps, first, timing=False):
-        for i in range(first, first + steps):
-            ctx.run_iteration(family_passes, tok_d[i % n_steps] if rank == 0 else None,
-                              lab_d[i % n_steps] if rank == p - 1 else None, timing=timing, fused=fused)
-            ctx.post_validate_step(opt)
+    tok_pin = [torch.from_numpy(np.ascontiguousarray(t[..., :cfg.s])).pin_memory().numpy() for t in toks]
+    lab_pin = [torch.from_numpy(np.ascontiguousarray(t[..., 1:])).pin_memory().numpy() for t in toks]
 
-    def timed(family_passes, fused):
+    def run(family_passes, fused, steps, first, timing=False, host=False):
+        for i in range(first, first + steps):
+            if host:   # e2e: pinned host inputs copied inside the call, loss read back every step
+                ctx.run_iteration(family_passes, tok_pin[i % n_steps] if rank == 0 else None,
+                                  lab_pin[i % n_steps] if rank == p - 1 else None, host_inputs=True, fused=fused)
+            else:
+                ctx.run_iteration(family_passes, tok_d[i % n_steps] if rank == 0 else None,
+                                  lab_d[i % n_steps] if rank == p - 1 else None, timing=timing, fused=fused)
+            ctx.post_validate_step(opt)
+            if host and rank == p - 1:
+                ctx.loss()
+
+    def timed(family_passes, fused, host=False):
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        run(family_passes, fused, args.steps, args.warmup)
+        run(family_passes, fused, args.steps, args.warmup, host=host)
         ctx.post_validate_finish(opt)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -373,10 +397,25 @@ def run_pipeline(args, cfg, rank, world, local):
     run(passes, False, args.warmup, 0)
     ctx.post_validate_finish(opt)
     torch.cuda.synchronize()
+    nl = C.c_int64()
+    lib.zb_dbg_launch_count(1, C.byref(nl))
     with ClockSampler(local) as clk:
         ms = timed(passes, False)
+    lib.zb_dbg_launch_count(0, C.byref(nl))
+    nlt = torch.tensor([nl.value], device="cuda", dtype=torch.int64)
+    dist.all_reduce(nlt)                       # kernels launched by all ranks
     tokens_per_step = cfg.T * m
     value = tokens_per_step / (ms / 1000.0)
+    # per-kernel-class timing over a second region of the same steps (roofline)
+    lib.zb_dbg_kernel_timing(1, 1)
+    ms_ev = timed(passes, False)
+    lib.zb_dbg_kernel_timing(0, 0)
+    a, b, n = C.c_double(), C.c_double(), C.c_int64()
+    lib.zb_dbg_kernel_timing_read(0, C.byref(a), C.byref(b), C.byref(n))
+    gt = torch.tensor([a.value, b.value], device="cuda", dtype=torch.float64)
+    dist.all_reduce(gt)                        # GEMM ms and FLOPs summed over ranks
+    # e2e: host inputs through the public call, loss read back every step
+    e2e_ms = timed(passes, False, host=True)
     # measured per-stage busy / span of one iteration (scheduling bubble)
     run(passes, False, 1, 0, timing=True)
     ctx.post_validate_finish(opt)
@@ -402,10 +441,22 @@ def run_pipeline(args, cfg, rank, world, local):
     if rank == 0:
         peaks, src = read_peaks()
         flops_token = cfg.L * (72 * cfg.h ** 2 + 12 * cfg.s * cfg.h) + 6 * cfg.h * cfg.V
+        g_tf = float(gt[1]) / (float(gt[0]) / 1e3) / 1e12 if float(gt[0]) else 0.0
+        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        roof = {"bound": "tensor", "kernel": "tcgen05 bf16 GEMM (F/B/W, all launches, all ranks)",
+                "achieved": round(g_tf, 1), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(g_tf / peak, 4) if peak else None, "traffic": None,
+                "peak_source": f"{src} bf16_tflops_sustained",
+                "timing": f"CUDA events around every GEMM launch over a second region of {args.steps} steps "
+                          f"({ms_ev:.1f} ms/step max over ranks with the events)",
+                "share_of_step": round(float(gt[0]) / p / args.steps / ms_ev, 4) if ms_ev else None}
+        e2e = {"value": tokens_per_step / (e2e_ms / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(2 * m * cfg.T * 4), "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms}
         line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": p, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (zb_synth seeded weights and tokens)",
-                "config": workload_config(cfg, p, args.family), "clocks": clk.summary(), "e2e": None,
+                "config": workload_config(cfg, p, args.family), "clocks": clk.summary(), "e2e": e2e,
+                "gpu_launches": int(nlt.item()), "roofline": roof,
                 "bubble": bubble,
                 "vs_1f1b": {"tokens_per_s_1f1b": tokens_per_step / (ms_1f1b / 1000.0) if ms_1f1b else None,
                             "speedup": ms_1f1b / ms if ms_1f1b else None},

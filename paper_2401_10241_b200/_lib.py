@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libzb.so")
+# ZB_LIB: alternative in-tree build of the same library (debug variants, e.g. libzb_v1.so)
+LIB_PATH = os.path.join(_HERE, os.environ.get("ZB_LIB", "libzb.so"))
 
 ZB_OK, ZB_EINVAL, ZB_ELIMIT, ZB_ECAP, ZB_ECUDA, ZB_ENCCL, ZB_ESTATE, ZB_ETIMEOUT = 0, -1, -2, -3, -4, -5, -6, -7
 ZB_F, ZB_B, ZB_W = 0, 1, 2
@@ -89,6 +90,7 @@ _SIGS = {
                            C.POINTER(_I32)], _I32),
     "zb_dbg_speculative_counts": ([C.POINTER(zb_pass_t), _I32, _I32, C.POINTER(_I32)], _I32),
     "zb_dbg_kernel_timing": ([_I32, _I32], _I32),
+    "zb_dbg_launch_count": ([_I32, C.POINTER(_I64)], _I32),
     "zb_dbg_kernel_timing_read": ([_I32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(_I64)], _I32),
     "zb_ctx_arena_bytes": ([C.POINTER(zb_model_cfg_t), C.POINTER(C.c_size_t)], _I32),
     "zb_ctx_slot_bytes": ([C.POINTER(zb_model_cfg_t), C.POINTER(C.c_size_t)], _I32),

@@ -60,6 +60,15 @@ extern "C" zb_status_t zb_dbg_kernel_timing(int32_t enable, int32_t reset) {
   ZB_CATCH
 }
 
+extern "C" zb_status_t zb_dbg_launch_count(int32_t reset, int64_t* count) {
+  ZB_TRY {
+    if (!count) return set_error(ZB_EINVAL, "null count");
+    *count = launch_count(reset != 0);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 extern "C" zb_status_t zb_dbg_kernel_timing_read(int32_t cls, double* total_ms, double* total_flops,
                                                  int64_t* launches) {
   ZB_TRY {

@@ -142,6 +142,7 @@ __device__ __forceinline__ void gemm_p_x_tile(float (*out)[4], float (*p)[4], co
 template <int D>
 __global__ void __launch_bounds__(NT) k_fwd_bf16(const bf16* __restrict__ qkv, bf16* __restrict__ o,
                                                  float* __restrict__ lse, int s, int a, float scale_log2) {
+  pdl_wait();
   constexpr int LDS = D + 8, TS = TILE * LDS;
   extern __shared__ __align__(16) uint8_t smraw[];
   bf16* sQ = reinterpret_cast<bf16*>(smraw);
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(NT) k_fwd_bf16(const bf16* __restrict__ qkv, b
 template <typename T>
 __global__ void k_delta(const T* __restrict__ o, const T* __restrict__ dout, float* __restrict__ delta, int s, int a,
                         int d, int rows) {
+  pdl_wait();
   // one thread per (row, head): d/8 vector loads of each operand summed in order
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<int64_t>(rows) * a) return;
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dq_bf16(const bf16* __restrict__ qkv
                                                     const float* __restrict__ lse, const float* __restrict__ delta,
                                                     bf16* __restrict__ dqkv, int s, int a, float scale,
                                                     float scale_log2) {
+  pdl_wait();
   constexpr int LDS = D + 8, TS = TILE * LDS;
   extern __shared__ __align__(16) uint8_t smraw[];
   bf16* sQ = reinterpret_cast<bf16*>(smraw);
@@ -344,6 +347,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dkdv_bf16(const bf16* __restrict__ q
                                                       const float* __restrict__ lse, const float* __restrict__ delta,
                                                       bf16* __restrict__ dqkv, int s, int a, float scale,
                                                       float scale_log2) {
+  pdl_wait();
   constexpr int LDS = D + 8, TS = TILE * LDS;
   extern __shared__ __align__(16) uint8_t smraw[];
   bf16* sK = reinterpret_cast<bf16*>(smraw);
@@ -436,6 +440,7 @@ __global__ void __launch_bounds__(NT) k_bwd_dkdv_bf16(const bf16* __restrict__ q
 template <int D>
 __global__ void k_fwd_f32(const float* __restrict__ qkv, float* __restrict__ o, float* __restrict__ lse, int s, int a,
                           float scale) {
+  pdl_wait();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   const int hd = blockIdx.y, bb = blockIdx.z;
   if (q >= s) return;
@@ -468,6 +473,7 @@ template <int D>
 __global__ void k_bwd_dq_f32(const float* __restrict__ qkv, const float* __restrict__ dout,
                              const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dqkv,
                              int s, int a, float scale) {
+  pdl_wait();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   const int hd = blockIdx.y, bb = blockIdx.z;
   if (q >= s) return;
@@ -499,6 +505,7 @@ template <int D>
 __global__ void k_bwd_dkdv_f32(const float* __restrict__ qkv, const float* __restrict__ dout,
                                const float* __restrict__ lse, const float* __restrict__ delta,
                                float* __restrict__ dqkv, int s, int a, float scale) {
+  pdl_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int hd = blockIdx.y, bb = blockIdx.z;
   if (k >= s) return;
@@ -542,7 +549,7 @@ static void fwd_bf16(const AttnShape& sh, const void* qkv, void* o, float* lse, 
     attr = true;
   }
   dim3 grid((sh.s + TILE - 1) / TILE, sh.a, sh.b);
-  k_fwd_bf16<D><<<grid, NT, smem, st>>>(static_cast<const bf16*>(qkv), static_cast<bf16*>(o), lse, sh.s, sh.a,
+  launch(PDL_OPS, k_fwd_bf16<D>, grid, NT, smem, st, static_cast<const bf16*>(qkv), static_cast<bf16*>(o), lse, sh.s, sh.a,
                                         LOG2E / sqrtf(static_cast<float>(D)));
   ZB_LAUNCH_CHECK();
 }
@@ -561,10 +568,10 @@ static void bwd_bf16(const AttnShape& sh, const void* qkv, const void* dout, con
   }
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   dim3 grid((sh.s + TILE - 1) / TILE, sh.a, sh.b);
-  k_bwd_dkdv_bf16<D><<<grid, NT, smem_kv, st>>>(static_cast<const bf16*>(qkv), static_cast<const bf16*>(dout), lse,
+  launch(PDL_OPS, k_bwd_dkdv_bf16<D>, grid, NT, smem_kv, st, static_cast<const bf16*>(qkv), static_cast<const bf16*>(dout), lse,
                                                 delta, static_cast<bf16*>(dqkv), sh.s, sh.a, scale, scale * LOG2E);
   ZB_LAUNCH_CHECK();
-  k_bwd_dq_bf16<D><<<grid, NT, smem_dq, st>>>(static_cast<const bf16*>(qkv), static_cast<const bf16*>(dout), lse,
+  launch(PDL_OPS, k_bwd_dq_bf16<D>, grid, NT, smem_dq, st, static_cast<const bf16*>(qkv), static_cast<const bf16*>(dout), lse,
                                               delta, static_cast<bf16*>(dqkv), sh.s, sh.a, scale, scale * LOG2E);
   ZB_LAUNCH_CHECK();
 }
@@ -572,7 +579,7 @@ static void bwd_bf16(const AttnShape& sh, const void* qkv, const void* dout, con
 template <int D>
 static void fwd_f32(const AttnShape& sh, const void* qkv, void* o, float* lse, cudaStream_t st) {
   dim3 grid((sh.s + 63) / 64, sh.a, sh.b);
-  k_fwd_f32<D><<<grid, 64, 0, st>>>(static_cast<const float*>(qkv), static_cast<float*>(o), lse, sh.s, sh.a,
+  launch(PDL_OPS, k_fwd_f32<D>, grid, 64, 0, st, static_cast<const float*>(qkv), static_cast<float*>(o), lse, sh.s, sh.a,
                                     1.f / sqrtf(static_cast<float>(D)));
   ZB_LAUNCH_CHECK();
 }
@@ -582,10 +589,10 @@ static void bwd_f32(const AttnShape& sh, const void* qkv, const void* dout, cons
                     const float* delta, cudaStream_t st) {
   dim3 grid((sh.s + 63) / 64, sh.a, sh.b);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
-  k_bwd_dkdv_f32<D><<<grid, 64, 0, st>>>(static_cast<const float*>(qkv), static_cast<const float*>(dout), lse, delta,
+  launch(PDL_OPS, k_bwd_dkdv_f32<D>, grid, 64, 0, st, static_cast<const float*>(qkv), static_cast<const float*>(dout), lse, delta,
                                          static_cast<float*>(dqkv), sh.s, sh.a, scale);
   ZB_LAUNCH_CHECK();
-  k_bwd_dq_f32<D><<<grid, 64, 0, st>>>(static_cast<const float*>(qkv), static_cast<const float*>(dout), lse, delta,
+  launch(PDL_OPS, k_bwd_dq_f32<D>, grid, 64, 0, st, static_cast<const float*>(qkv), static_cast<const float*>(dout), lse, delta,
                                        static_cast<float*>(dqkv), sh.s, sh.a, scale);
   ZB_LAUNCH_CHECK();
 }
@@ -625,10 +632,10 @@ void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const vo
   const int rows = sh.b * sh.s;
   const int blocks = static_cast<int>((static_cast<int64_t>(rows) * sh.a + 255) / 256);
   if (dt == DT_BF16)
-    attn::k_delta<bf16><<<blocks, 256, 0, st>>>(static_cast<const bf16*>(o), static_cast<const bf16*>(dout), delta,
+    launch(PDL_OPS, attn::k_delta<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(o), static_cast<const bf16*>(dout), delta,
                                                 sh.s, sh.a, sh.d, rows);
   else
-    attn::k_delta<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(o), static_cast<const float*>(dout), delta,
+    launch(PDL_OPS, attn::k_delta<float>, blocks, 256, 0, st, static_cast<const float*>(o), static_cast<const float*>(dout), delta,
                                                  sh.s, sh.a, sh.d, rows);
   ZB_LAUNCH_CHECK();
   if (dt == DT_BF16 && !legacy_attention() && attention_bwd_tc(sh, qkv, dout, lse, dqkv, delta, st)) return;

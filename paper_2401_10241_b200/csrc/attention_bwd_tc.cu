@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(384, 1)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
+  pdl_wait();
   const uint32_t tbase = *tslot;
   const uint32_t t_dk = tbase + 256, t_dv = tbase + 256 + D;
 
@@ -291,6 +293,8 @@ __global__ void __launch_bounds__(384, 1)
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
+  pdl_wait();
   const uint32_t tbase = *tslot;
   const uint32_t t_dq = tbase + 256;
 
@@ -434,10 +438,10 @@ static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout
   const CUtensorMap do128 = make_tmap(dout, h, rows, h, 64, 128);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   dim3 grid(sh.s / 128, sh.a, sh.b);
-  attn_bwd_tc::k_dkdv_tc<D><<<grid, 384, C1::SMEM, st>>>(kv128, kv64, do64, lse, delta, static_cast<bf16*>(dqkv),
+  launch(PDL_ATTN, attn_bwd_tc::k_dkdv_tc<D>, grid, 384, C1::SMEM, st, kv128, kv64, do64, lse, delta, static_cast<bf16*>(dqkv),
                                                          sh.s, sh.a, scale, scale * attn_bwd_tc::LOG2E);
   ZB_LAUNCH_CHECK();
-  attn_bwd_tc::k_dq_tc<D><<<grid, 384, C2::SMEM, st>>>(kv128, kv64, do128, lse, delta, static_cast<bf16*>(dqkv),
+  launch(PDL_ATTN, attn_bwd_tc::k_dq_tc<D>, grid, 384, C2::SMEM, st, kv128, kv64, do128, lse, delta, static_cast<bf16*>(dqkv),
                                                        sh.s, sh.a, scale, scale * attn_bwd_tc::LOG2E);
   ZB_LAUNCH_CHECK();
 }

@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
+  pdl_wait();
   const uint32_t tbase = *tslot;
   const uint32_t t_s0 = tbase, t_o = tbase + 256;
   const int row0 = bb * s;
@@ -285,7 +287,7 @@ static void fwd_tc_launch(const AttnShape& sh, const void* qkv, void* o, float* 
   const int h = sh.a * D;
   CUtensorMap tm = make_qkv_tmap(qkv, sh.b * sh.s, 3 * h);
   dim3 grid(sh.s / attn_tc::BQ, sh.a, sh.b);
-  attn_tc::k_fwd_tc<D><<<grid, 384, C::SMEM, st>>>(tm, static_cast<bf16*>(o), lse, sh.s, sh.a,
+  launch(PDL_ATTN, attn_tc::k_fwd_tc<D>, grid, 384, C::SMEM, st, tm, static_cast<bf16*>(o), lse, sh.s, sh.a,
                                                    attn_tc::LOG2E / sqrtf(static_cast<float>(D)));
   ZB_LAUNCH_CHECK();
 }

@@ -7,6 +7,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "this library targets sm_100a only"
@@ -33,6 +34,49 @@ struct CudaError : std::runtime_error {
 #define ZB_LAUNCH_CHECK() ZB_CUDA(cudaGetLastError())
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- launches ----------------------------------------------------------------
+// Every kernel of the library is launched through launch(): counted
+// (zb_dbg_launch_count) and, when enabled for its class, launched with
+// programmatic dependent launch (PDL) so its prologue can overlap the tail of
+// the previous kernel on the stream.  Contract of every kernel: pdl_wait()
+// before its first global-memory access (griddepcontrol.wait returns once the
+// previous grid has completed and its writes are visible; a no-op without
+// PDL).  Only the TMEM kernels (GEMM, attention) trigger early, and only AFTER
+// their TMEM allocation, so a dependent CTA can never hold TMEM that a CTA of
+// an earlier grid still has to allocate; the HBM-bound kernels trigger
+// implicitly at exit.  (Early triggers in the HBM-bound kernels deadlocked the
+// 1.5B step on B200 — cause not identified — and PDL of the TMEM classes
+// measured no gain: the step is bound by kernel time at power-capped clocks,
+// not by launch gaps.)  Default off.
+// ZB_PDL=<mask>: PDL for kernel classes (1 GEMM, 2 attention, 4 others).
+// ZB_TRACE_LAUNCH=1 prints every kernel when the stream reaches it (debugging;
+// serialises).
+enum PdlClass : int { PDL_GEMM = 1, PDL_ATTN = 2, PDL_OPS = 4 };
+void note_launch();
+bool pdl_enabled(int cls);
+void trace_launch(const void* kern, cudaStream_t st);
+
+template <typename... KArgs, typename... Args>
+inline void launch(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled(cls) ? 1 : 0;
+  ZB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  note_launch();
+  trace_launch(reinterpret_cast<const void*>(kern), st);
+}
+
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ---- element conversion ----------------------------------------------------
 template <typename T> __device__ __forceinline__ float to_f(T x);

@@ -70,14 +70,116 @@ namespace tc {
 constexpr int BM = 128, BK = 64;
 constexpr int kThreads = 384;     // warps 0-3: TMA, MMA, TMEM alloc, idle; warps 4-11: epilogue
 constexpr int kEpiThreads = 256;
+constexpr int kEpiWarps = 8;
+constexpr int kStageBytes = 4096;  // epilogue staging per warp: a 32-row x 128-byte TMA box
 constexpr int A_BYTES = BM * BK * 2;
 template <int BN> struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 4 : 6;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int EPI_OFF = STAGES * STAGE;
+  static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * kStageBytes;
+  static constexpr int SMEM = BAR_OFF + 1024 /*align slack*/ + 256 /*barriers*/;
 };
+
+// output element type of an epilogue
+template <int EPI> using OutT = typename std::conditional<(EPI == EPI_F32_ACC || EPI == EPI_F32_STORE), float, bf16>::type;
+
+// byte offset of 16-byte piece j of row `lane` in a 32 x 128 B box, TMA 128B-swizzle layout
+__device__ __forceinline__ int swz(int lane, int j) { return lane * 128 + ((j ^ (lane & 7)) << 4); }
+
+// TMA epilogue of one warp: 32 rows (the warp's TMEM lane quadrant) x ncols columns
+// starting at global (row0, col0); taddr = TMEM address of the first column.  Per chunk
+// of 128 B per row (64 bf16 / 32 f32 columns): tcgen05.ld, fused epilogue in f32,
+// write the 32 x 128 B box into the warp's staging buffer in the 128B-swizzled layout,
+// TMA-store it (coalesced, asynchronous, M / N tails clipped by the tensor map).  W's
+// f32 accumulation (EPI_F32_ACC, beta) is a TMA reduce-add: the L2 adds the tile, nothing
+// is read back into the SM.  RESID / GELU_BWD read their bf16 operand through the same
+// staging buffer (TMA load on the warp's mbarrier), BIAS_GELU stores C then GeLU(C).
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtensorMap* tmC, const CUtensorMap* tmX,
+                                                uint32_t taddr, uint8_t* buf, uint64_t* xbar, uint32_t& xph,
+                                                int row0, int col0, int ncols, int N, int lane) {
+  using TO = OutT<EPI>;
+  constexpr int CC = 128 / static_cast<int>(sizeof(TO));
+  constexpr bool kAuxIn = EPI == EPI_RESID || EPI == EPI_GELU_BWD;
+  constexpr bool kBias = EPI == EPI_STORE || EPI == EPI_BIAS_GELU || EPI == EPI_RESID;
+#pragma unroll 1
+  for (int ch = 0; ch < ncols / CC; ++ch) {
+    const int col = col0 + ch * CC;
+    if (lane == 0) {
+      sm100::bulk_wait_read<0>();  // the previous chunk's store has read the staging buffer
+      if (kAuxIn) {
+        sm100::mbar_arrive_expect_tx(xbar, kStageBytes);
+        sm100::tma_load_2d(buf, tmX, xbar, col, row0);
+      }
+    }
+    __syncwarp();
+    uint32_t r[CC];
+    sm100::tmem_ld32(taddr + ch * CC, r);
+    if (CC == 64) sm100::tmem_ld32(taddr + ch * CC + 32, r + 32);
+    sm100::tmem_ld_wait();
+    float* v = reinterpret_cast<float*>(r);
+    if (kBias && ep.bias != nullptr) {
+#pragma unroll
+      for (int g = 0; g < CC / 8; ++g) {
+        if (col + 8 * g < N) {
+          float b[8];
+          Vec8<float>::load(ep.bias + col + 8 * g, b);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[8 * g + i] += b[i];
+        }
+      }
+    }
+    if (kAuxIn) {
+      sm100::mbar_wait(xbar, xph);
+      xph ^= 1;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint4* p = reinterpret_cast<uint4*>(buf + swz(lane, j));
+      if (sizeof(TO) == 4) {
+        *p = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+      } else {
+        float* x = v + 8 * j;
+        if (kAuxIn) {
+          float u[8];
+          Vec8<bf16>::load(reinterpret_cast<const bf16*>(p), u);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) x[i] = (EPI == EPI_RESID) ? x[i] + u[i] : x[i] * gelu_grad_fast(u[i]);
+        }
+        Vec8<bf16>::store(reinterpret_cast<bf16*>(p), x);
+      }
+    }
+    sm100::fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      if (EPI == EPI_F32_ACC && ep.beta)
+        sm100::tma_reduce_add_2d(tmC, buf, col, row0);
+      else
+        sm100::tma_store_2d(tmC, buf, col, row0);
+      sm100::bulk_commit();
+    }
+    if (EPI == EPI_BIAS_GELU) {  // second output: GeLU of the same f32 values
+      if (lane == 0) sm100::bulk_wait_read<0>();
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float g[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) g[i] = gelu_fast(v[8 * j + i]);
+        Vec8<bf16>::store(reinterpret_cast<bf16*>(buf + swz(lane, j)), g);
+      }
+      sm100::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        sm100::tma_store_2d(tmX, buf, col, row0);
+        sm100::bulk_commit();
+      }
+    }
+  }
+}
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mt, int& nt) {
   constexpr int G = 8;  // group of 8 M-tiles swept across N for L2 reuse
@@ -92,16 +194,18 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mt
 
 template <int BN, bool A_MN, bool B_MN, int EPI, typename TO>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const EpiArgs ep,
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const EpiArgs ep,
               int M, int N, int K) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xbar = tempty + 2;  // [kEpiWarps]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -113,16 +217,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&tfull[i], 1);
       sm100::mbar_init(&tempty[i], kEpiThreads);
     }
+    for (int i = 0; i < kEpiWarps; ++i) sm100::mbar_init(&xbar[i], 1);
     sm100::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
+    sm100::tma_prefetch(&tmC);
+    sm100::tma_prefetch(&tmX);
   }
   if (warp == 2) sm100::tmem_alloc<C::TMEM_COLS>(tslot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
+  pdl_wait();
   const uint32_t tbase = *tslot;
 
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
@@ -200,27 +309,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 8 epilogue warps: warp w reads TMEM lanes 32*(w%4).. (hardware lane quadrant) and
     // one half of the tile's columns, so two warps per SMSP hide each other's latency
     const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;
+    uint8_t* buf = smem + C::EPI_OFF + (warp - 4) * kStageBytes;
+    uint32_t xph = 0;
     int acc = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       int mt, nt;
       tile_coords(t, num_m, num_n, mt, nt);
-      const int64_t row = static_cast<int64_t>(mt) * BM + ew * 32 + lane;
       sm100::mbar_wait(&tfull[acc], aph);
       sm100::tc_fence_after();
-#pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
-        uint32_t r[32];
-        sm100::tmem_ld32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
-        sm100::tmem_ld_wait();
-        const int col0 = nt * BN + c * 32;
-        if (row < M) {
-          float* v = reinterpret_cast<float*>(r);
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            if (col0 + g * 8 < N) epi8<EPI, TO>(ep, row, col0 + g * 8, v + g * 8);
-        }
-      }
+      epilogue_chunks<EPI>(ep, &tmC, &tmX,
+                           tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
+                           &xbar[warp - 4], xph, mt * BM + ew * 32, nt * BN + half * (BN / 2), BN / 2, N, lane);
       sm100::tc_fence_before();
       sm100::mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
@@ -228,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         aph ^= 1;
       }
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // stores complete before the CTA exits
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -248,22 +349,26 @@ template <int BN> struct Cfg2 {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN >= 256) ? 6 : 8;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr int EPI_OFF = STAGES * STAGE;
+  static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * kStageBytes;
+  static constexpr int SMEM = BAR_OFF + 1024 + 256;
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI, typename TO>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const EpiArgs ep,
+    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const EpiArgs ep,
                int M, int N, int K) {
   using C = Cfg2<BN>;
   constexpr int BM2 = 2 * BM;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xbar = tempty + 2;  // [kEpiWarps]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
@@ -277,16 +382,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       sm100::mbar_init(&tfull[i], 1);
       sm100::mbar_init(&tempty[i], 2 * kEpiThreads);  // both CTAs' epilogue threads
     }
+    for (int i = 0; i < kEpiWarps; ++i) sm100::mbar_init(&xbar[i], 1);
     sm100::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     sm100::tma_prefetch(&tmA);
     sm100::tma_prefetch(&tmB);
+    sm100::tma_prefetch(&tmC);
+    sm100::tma_prefetch(&tmX);
   }
   if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tslot);
   sm100::tc_fence_before();
   sm100::cluster_sync();
   sm100::tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
+  pdl_wait();
   const uint32_t tbase = *tslot;
 
   const int num_m = (M + BM2 - 1) / BM2, num_n = (N + BN - 1) / BN;
@@ -368,27 +478,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows)
     const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;  // see the 1-CTA kernel
     const uint32_t te0 = sm100::map_to_cta(&tempty[0], 0), te1 = sm100::map_to_cta(&tempty[1], 0);
+    uint8_t* buf = smem + C::EPI_OFF + (warp - 4) * kStageBytes;
+    uint32_t xph = 0;
     int acc = 0;
     uint32_t aph = 0;
     for (int t = cid; t < tiles; t += ncl) {
       int mt, nt;
       tile_coords(t, num_m, num_n, mt, nt);
-      const int64_t row = static_cast<int64_t>(mt) * BM2 + static_cast<int>(rank) * BM + ew * 32 + lane;
       sm100::mbar_wait(&tfull[acc], aph);
       sm100::tc_fence_after();
-#pragma unroll 1
-      for (int c = half * (BN / 64); c < (half + 1) * (BN / 64); ++c) {
-        uint32_t r[32];
-        sm100::tmem_ld32(tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c * 32, r);
-        sm100::tmem_ld_wait();
-        const int col0 = nt * BN + c * 32;
-        if (row < M) {
-          float* v = reinterpret_cast<float*>(r);
-#pragma unroll
-          for (int g = 0; g < 4; ++g)
-            if (col0 + g * 8 < N) epi8<EPI, TO>(ep, row, col0 + g * 8, v + g * 8);
-        }
-      }
+      epilogue_chunks<EPI>(ep, &tmC, &tmX,
+                           tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
+                           &xbar[warp - 4], xph, mt * BM2 + static_cast<int>(rank) * BM + ew * 32,
+                           nt * BN + half * (BN / 2), BN / 2, N, lane);
       sm100::tc_fence_before();
       sm100::mbar_arrive_cluster(acc == 0 ? te0 : te1);
       if (++acc == 2) {
@@ -396,6 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         aph ^= 1;
       }
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // stores complete before the CTA exits
   }
   sm100::tc_fence_before();
   sm100::cluster_sync();
@@ -410,6 +513,7 @@ constexpr int BT = 64, BKK = 16;
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(64) k_gemm_f32(const float* __restrict__ A, int64_t lda, const float* __restrict__ B,
                                                  int64_t ldb, const EpiArgs ep, int M, int N, int K) {
+  pdl_wait();
   __shared__ float As[BKK][BT + 4];
   __shared__ float Bs[BKK][BT + 4];
   const int tid = threadIdx.x;
@@ -488,19 +592,34 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D bf16 tensor map over a row-major [outer, inner] view with leading dim ld.
 CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-                             uint32_t box_outer) {
-  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * 2) & 15))
+                      uint32_t box_outer, bool f32) {
+  const uint64_t esz = f32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * esz) & 15))
     throw CudaError("gemm: operand must be 16-byte aligned with a 16-byte multiple row pitch");
   CUtensorMap tm;
   cuuint64_t gdim[2] = {inner, outer};
-  cuuint64_t gstride[1] = {ld * 2};
+  cuuint64_t gstride[1] = {ld * esz};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box, estr,
+  CUresult r = encode_fn()(&tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   return tm;
+}
+
+// epilogue tensor maps: C (output, box 32 rows x 128 B) and X (the bf16 aux operand:
+// GeLU output of BIAS_GELU, residual / pre-activation input of RESID / GELU_BWD)
+template <int EPI>
+static void epi_tmaps(const GemmArgs& g, CUtensorMap& tc_, CUtensorMap& tx) {
+  constexpr bool f32 = EPI == EPI_F32_ACC || EPI == EPI_F32_STORE;
+  tc_ = make_tmap(g.ep.C, g.N, g.M, g.ep.ldc, f32 ? 32 : 64, 32, f32);
+  if (EPI == EPI_BIAS_GELU || EPI == EPI_RESID || EPI == EPI_GELU_BWD) {
+    if (!g.ep.aux) throw CudaError("gemm: epilogue needs its aux operand");
+    tx = make_tmap(g.ep.aux, g.N, g.M, g.ep.ldaux, 64, 32);
+  } else {
+    tx = tc_;
+  }
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
@@ -516,7 +635,9 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap tb = B_MN ? make_tmap(g.B, g.N, g.K, g.ldb, 64, 64) : make_tmap(g.B, g.K, g.N, g.ldb, 64, BN);
   const int tiles = static_cast<int>(ceil_div(g.M, tc::BM) * ceil_div(g.N, BN));
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, tc::kThreads, C::SMEM, st>>>(ta, tb, g.ep, g.M, g.N, g.K);
+  CUtensorMap tcm, txm;
+  epi_tmaps<EPI>(g, tcm, txm);
+  launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, g.ep, g.M, g.N, g.K);
   ZB_LAUNCH_CHECK();
 }
 
@@ -534,7 +655,9 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   const int tiles = static_cast<int>(ceil_div(g.M, 2 * tc::BM) * ceil_div(g.N, BN));
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
-  kern<<<grid, tc::kThreads, C::SMEM, st>>>(ta, tb, g.ep, g.M, g.N, g.K);
+  CUtensorMap tcm, txm;
+  epi_tmaps<EPI>(g, tcm, txm);
+  launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, g.ep, g.M, g.N, g.K);
   ZB_LAUNCH_CHECK();
 }
 
@@ -584,7 +707,7 @@ static void dispatch_epi_f32(const GemmArgs& g, cudaStream_t st) {
   const float* B = static_cast<const float*>(g.B);
   switch (g.epi) {
 #define ZB_F32_CASE(E) \
-  case E: simt::k_gemm_f32<A_MN, B_MN, E><<<grid, 64, 0, st>>>(A, g.lda, B, g.ldb, g.ep, g.M, g.N, g.K); break;
+  case E: launch(PDL_GEMM, simt::k_gemm_f32<A_MN, B_MN, E>, grid, 64, 0, st, A, g.lda, B, g.ldb, g.ep, g.M, g.N, g.K); break;
     ZB_F32_CASE(EPI_STORE)
     ZB_F32_CASE(EPI_BIAS_GELU)
     ZB_F32_CASE(EPI_RESID)

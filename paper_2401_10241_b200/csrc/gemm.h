@@ -54,9 +54,9 @@ void gemm(const GemmArgs& g, DType dt, cudaStream_t stream);
 // number of SMs of the current device (cached)
 int num_sms();
 
-// 2-D bf16 TMA descriptor (128B swizzle) over a row-major [outer, inner] view
-// with leading dimension ld elements and box {box_inner, box_outer}.
+// 2-D bf16 (or f32) TMA descriptor (128B swizzle) over a row-major [outer, inner]
+// view with leading dimension ld elements and box {box_inner, box_outer}.
 CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-                      uint32_t box_outer);
+                      uint32_t box_outer, bool f32 = false);
 
 }  // namespace zb

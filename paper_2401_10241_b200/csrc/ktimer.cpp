@@ -1,9 +1,38 @@
 #include "ktimer.h"
 
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
 namespace zb {
+
+namespace {
+std::atomic<int64_t> g_launches{0};
+}
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count(bool reset) { return reset ? g_launches.exchange(0) : g_launches.load(); }
+bool pdl_enabled(int cls) {
+  static const int mask = [] {
+    const char* e = std::getenv("ZB_PDL");
+    return e ? std::atoi(e) : 0;
+  }();
+  return (mask & cls) != 0;
+}
+
+namespace {
+void CUDART_CB print_name(void* name) { std::fprintf(stderr, "[zb] done-> %s\n", static_cast<const char*>(name)); }
+}  // namespace
+
+void trace_launch(const void* kern, cudaStream_t st) {
+  static const bool on = std::getenv("ZB_TRACE_LAUNCH") != nullptr;
+  if (!on) return;
+  const char* name = nullptr;
+  if (cudaFuncGetName(&name, kern) != cudaSuccess || !name) name = "?";
+  std::fprintf(stderr, "[zb] launch %s\n", name);
+  cudaLaunchHostFunc(st, print_name, const_cast<char*>(name));
+}
 namespace ktimer {
 
 namespace {

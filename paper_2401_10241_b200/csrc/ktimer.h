@@ -8,6 +8,10 @@
 #include <cstdint>
 
 namespace zb {
+
+// kernel launches of the library since the last reset (common.cuh launch())
+int64_t launch_count(bool reset);
+
 namespace ktimer {
 
 enum Class : int { GEMM = 0, ATTN_FWD = 1, ATTN_BWD = 2, GEMM_F = 3, GEMM_B = 4, GEMM_W = 5, N_CLASSES = 6 };

@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_fwd(const T* __restrict__ x, 
                                                       const float* __restrict__ b, T* __restrict__ y,
                                                       float* __restrict__ mean, float* __restrict__ rstd, int h,
                                                       float eps) {
+  pdl_wait();
   constexpr int NW = LN_THREADS / 32;
   __shared__ float red[2 * NW];
   const int64_t row = blockIdx.x;
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(128) k_ln_fwd_warp(const T* __restrict__ x, co
                                                     const float* __restrict__ b, T* __restrict__ y,
                                                     float* __restrict__ mean, float* __restrict__ rstd, int rows, int h,
                                                     float eps) {
+  pdl_wait();
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_bwd_dx(const float* __restric
                                                          const float* __restrict__ mean, const float* __restrict__ rstd,
                                                          const float* __restrict__ g, const float* resid, float* dx32,
                                                          T* dx, int h) {
+  pdl_wait();
   constexpr int NW = LN_THREADS / 32;
   __shared__ float red[2 * NW];
   const int64_t r = blockIdx.x;
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(kColThreads) k_ln_param_grads(const float* __r
                                                                 const float* __restrict__ mean,
                                                                 const float* __restrict__ rstd, float* __restrict__ gg,
                                                                 float* __restrict__ gb, int rows, int h, int beta) {
+  pdl_wait();
   constexpr int RL = kColThreads / VPC;
   extern __shared__ float colsm[];
   const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
@@ -294,6 +298,7 @@ __global__ void __launch_bounds__(kColThreads) k_ln_param_grads(const float* __r
 template <typename T, int VPC>
 __global__ void __launch_bounds__(kColThreads) k_colsum(const T* __restrict__ y, int64_t ldy, float* __restrict__ out,
                                                         int rows, int n, int beta) {
+  pdl_wait();
   constexpr int RL = kColThreads / VPC;
   extern __shared__ float colsm[];
   const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
@@ -336,6 +341,7 @@ __global__ void __launch_bounds__(kColThreads) k_colsum(const T* __restrict__ y,
 template <typename T>
 __global__ void k_embed_fwd(const int32_t* __restrict__ tok, const float* __restrict__ wte,
                             const float* __restrict__ wpe, T* __restrict__ x0, int s, int h) {
+  pdl_wait();
   const int64_t row = blockIdx.x;
   const int64_t t = tok[row];
   const int pos = static_cast<int>(row % s);
@@ -352,6 +358,7 @@ __global__ void k_embed_fwd(const int32_t* __restrict__ tok, const float* __rest
 // One-block bitonic sort of keys = tok * rows + pos (<= 8192 keys, padded with UINT32_MAX).
 __global__ void __launch_bounds__(1024) k_sort_tokens(const int32_t* __restrict__ tok, uint32_t* __restrict__ keys,
                                                      int rows) {
+  pdl_wait();
   constexpr int N = 8192;
   __shared__ uint32_t sk[N];
   for (int i = threadIdx.x; i < N; i += blockDim.x)
@@ -381,6 +388,7 @@ __global__ void __launch_bounds__(1024) k_sort_tokens(const int32_t* __restrict_
 template <typename T>
 __global__ void k_embed_bwd_wte(const uint32_t* __restrict__ keys, const T* __restrict__ dx0, float* __restrict__ dwte,
                                 int rows, int h) {
+  pdl_wait();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= rows) return;
   const uint32_t R = static_cast<uint32_t>(rows);
@@ -404,6 +412,7 @@ __global__ void k_embed_bwd_wte(const uint32_t* __restrict__ keys, const T* __re
 
 template <typename T>
 __global__ void k_embed_bwd_wpe(const T* __restrict__ dx0, float* __restrict__ dwpe, int rows, int s, int h) {
+  pdl_wait();
   const int t = blockIdx.x;
   for (int vi = threadIdx.x; vi < h / 8; vi += blockDim.x) {
     float acc[8];
@@ -423,6 +432,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024) k_ce(const float* __restrict__ logits, const int32_t* __restrict__ labels,
                                             T* __restrict__ dlogits, float* __restrict__ loss_rows, int V,
                                             float inv_scale) {
+  pdl_wait();
   __shared__ float red[32];
   __shared__ float bc;
   const int64_t row = blockIdx.x;
@@ -480,6 +490,7 @@ __global__ void __launch_bounds__(1024) k_ce(const float* __restrict__ logits, c
 
 __global__ void k_loss_reduce(const float* __restrict__ loss_rows, double* __restrict__ acc, int rows,
                               float inv_scale) {
+  pdl_wait();
   __shared__ double red[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < rows; i += blockDim.x) s += static_cast<double>(loss_rows[i]);
@@ -497,6 +508,7 @@ __global__ void k_loss_reduce(const float* __restrict__ loss_rows, double* __res
 
 template <typename T>
 __global__ void k_convert(const float* __restrict__ src, T* __restrict__ dst, int64_t n) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     dst[i] = from_f<T>(src[i]);
@@ -504,6 +516,7 @@ __global__ void k_convert(const float* __restrict__ src, T* __restrict__ dst, in
 
 // ---------------------------------------------------------------- optimizer
 __global__ void k_sumsq(const float* __restrict__ g, int64_t n, double* __restrict__ part, int32_t* __restrict__ nfp) {
+  pdl_wait();
   __shared__ double red[32];
   __shared__ int nfr[32];
   double s = 0.0;
@@ -546,6 +559,7 @@ __global__ void k_sumsq(const float* __restrict__ g, int64_t n, double* __restri
 }
 
 __global__ void k_sumsq_final(const double* __restrict__ part, const int32_t* __restrict__ nfp, int nb, PvState* st) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   double t = 0.0;
   int f = 0;
@@ -558,6 +572,7 @@ __global__ void k_sumsq_final(const double* __restrict__ part, const int32_t* __
 }
 
 __global__ void k_pv_combine(PvState* st) {
+  pdl_wait();
   st->partial_sumsq = st->partial_in_sumsq + st->local_sumsq;
   st->partial_nf = st->partial_in_nf | st->local_nf;
 }
@@ -568,6 +583,7 @@ __device__ __forceinline__ double clip_coef(double sumsq, float clip) { return c
 // partial norm already needs clipping, else an unclipped step.  In sync mode
 // the partial IS the full state and a clipped step is taken directly.
 __global__ void k_pv_decide_first(PvState* st, float clip, int sync_mode) {
+  pdl_wait();
   st->coef_rollback = 0.f;
   if (st->partial_nf) {
     st->first_action = ZB_ACT_SKIP;
@@ -597,6 +613,7 @@ __global__ void k_pv_decide_first(PvState* st, float clip, int sync_mode) {
 
 // Validation with the fully reduced state: roll back, redo, or take the deferred step.
 __global__ void k_pv_decide_final(PvState* st, float clip) {
+  pdl_wait();
   const int a = st->first_action;
   st->adam_mode = 0;
   st->final_action = ZB_ACT_NONE;
@@ -624,6 +641,7 @@ __global__ void k_pv_decide_final(PvState* st, float clip) {
 }
 
 __global__ void k_pv_finish(PvState* st) {
+  pdl_wait();
   const int mode = st->adam_mode;
   if (mode == 1) st->t += 1;
   if (mode == 2) st->t -= 1;
@@ -635,6 +653,7 @@ __global__ void k_adamw(float* __restrict__ theta, float* __restrict__ m, float*
                         const float* __restrict__ g, bf16* __restrict__ shadow, int64_t n, int64_t n_wd,
                         int64_t n_shadow, float lr, float b1, float b2, float eps, float wd,
                         const PvState* __restrict__ st) {
+  pdl_wait();
   const int mode = st->adam_mode;
   if (mode == 0) return;
   const int t0 = st->t;
@@ -689,10 +708,10 @@ static void ln_fwd_warp(DType dt, const void* x, const float* g, const float* b,
                         int rows, int h, float eps, cudaStream_t st) {
   const int blocks = (rows + 3) / 4;
   if (dt == DT_BF16)
-    k_ln_fwd_warp<bf16, VPL><<<blocks, 128, 0, st>>>(static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean,
+    launch(PDL_OPS, k_ln_fwd_warp<bf16, VPL>, blocks, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean,
                                                      rstd, rows, h, eps);
   else
-    k_ln_fwd_warp<float, VPL><<<blocks, 128, 0, st>>>(static_cast<const float*>(x), g, b, static_cast<float*>(y),
+    launch(PDL_OPS, k_ln_fwd_warp<float, VPL>, blocks, 128, 0, st, static_cast<const float*>(x), g, b, static_cast<float*>(y),
                                                       mean, rstd, rows, h, eps);
 }
 
@@ -713,10 +732,10 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
     ln_dispatch<0>(h, [&](auto V) {
       constexpr int VPT = decltype(V)::value;
       if (dt == DT_BF16)
-        k_ln_fwd<bf16, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y),
+        launch(PDL_OPS, k_ln_fwd<bf16, VPT>, rows, LN_THREADS, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y),
                                                          mean, rstd, h, eps);
       else
-        k_ln_fwd<float, VPT><<<rows, LN_THREADS, 0, st>>>(static_cast<const float*>(x), g, b, static_cast<float*>(y),
+        launch(PDL_OPS, k_ln_fwd<float, VPT>, rows, LN_THREADS, 0, st, static_cast<const float*>(x), g, b, static_cast<float*>(y),
                                                           mean, rstd, h, eps);
     });
   }
@@ -763,11 +782,11 @@ void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, 
     const size_t sm = colred_smem<VPC>(2);
     if (dt == DT_BF16) {
       allow_smem(k_ln_param_grads<bf16, VPC>, sm);
-      k_ln_param_grads<bf16, VPC><<<grid, kColThreads, sm, st>>>(dy, static_cast<const bf16*>(x), mean, rstd, gg, gb,
+      launch(PDL_OPS, k_ln_param_grads<bf16, VPC>, grid, kColThreads, sm, st, dy, static_cast<const bf16*>(x), mean, rstd, gg, gb,
                                                                  rows, h, beta);
     } else {
       allow_smem(k_ln_param_grads<float, VPC>, sm);
-      k_ln_param_grads<float, VPC><<<grid, kColThreads, sm, st>>>(dy, static_cast<const float*>(x), mean, rstd, gg,
+      launch(PDL_OPS, k_ln_param_grads<float, VPC>, grid, kColThreads, sm, st, dy, static_cast<const float*>(x), mean, rstd, gg,
                                                                   gb, rows, h, beta);
     }
   });
@@ -776,10 +795,10 @@ void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, 
   ln_dispatch<0>(h, [&](auto V) {
     constexpr int VPT = decltype(V)::value;
     if (dt == DT_BF16)
-      k_ln_bwd_dx<bf16, VPT><<<rows, LN_THREADS, 0, st>>>(dy, static_cast<const bf16*>(x), mean, rstd, g, resid, dx32,
+      launch(PDL_OPS, k_ln_bwd_dx<bf16, VPT>, rows, LN_THREADS, 0, st, dy, static_cast<const bf16*>(x), mean, rstd, g, resid, dx32,
                                                           static_cast<bf16*>(dx), h);
     else
-      k_ln_bwd_dx<float, VPT><<<rows, LN_THREADS, 0, st>>>(dy, static_cast<const float*>(x), mean, rstd, g, resid,
+      launch(PDL_OPS, k_ln_bwd_dx<float, VPT>, rows, LN_THREADS, 0, st, dy, static_cast<const float*>(x), mean, rstd, g, resid,
                                                            dx32, static_cast<float*>(dx), h);
   });
   ZB_LAUNCH_CHECK();
@@ -793,10 +812,10 @@ void bias_grad(DType dt, const void* y, int64_t ldy, float* out, int rows, int n
     const size_t sm = colred_smem<VPC>(1);
     if (dt == DT_BF16) {
       allow_smem(k_colsum<bf16, VPC>, sm);
-      k_colsum<bf16, VPC><<<grid, kColThreads, sm, st>>>(static_cast<const bf16*>(y), ldy, out, rows, n, beta);
+      launch(PDL_OPS, k_colsum<bf16, VPC>, grid, kColThreads, sm, st, static_cast<const bf16*>(y), ldy, out, rows, n, beta);
     } else {
       allow_smem(k_colsum<float, VPC>, sm);
-      k_colsum<float, VPC><<<grid, kColThreads, sm, st>>>(static_cast<const float*>(y), ldy, out, rows, n, beta);
+      launch(PDL_OPS, k_colsum<float, VPC>, grid, kColThreads, sm, st, static_cast<const float*>(y), ldy, out, rows, n, beta);
     }
   });
   ZB_LAUNCH_CHECK();
@@ -807,9 +826,9 @@ void embed_fwd(DType dt, const int32_t* tok, const float* wte, const float* wpe,
   if (rows <= 0) return;
   const int thr = h / 8 < 256 ? ((h / 8 + 31) / 32) * 32 : 256;
   if (dt == DT_BF16)
-    k_embed_fwd<bf16><<<rows, thr, 0, st>>>(tok, wte, wpe, static_cast<bf16*>(x0), s, h);
+    launch(PDL_OPS, k_embed_fwd<bf16>, rows, thr, 0, st, tok, wte, wpe, static_cast<bf16*>(x0), s, h);
   else
-    k_embed_fwd<float><<<rows, thr, 0, st>>>(tok, wte, wpe, static_cast<float*>(x0), s, h);
+    launch(PDL_OPS, k_embed_fwd<float>, rows, thr, 0, st, tok, wte, wpe, static_cast<float*>(x0), s, h);
   ZB_LAUNCH_CHECK();
 }
 
@@ -817,16 +836,16 @@ void embed_bwd(DType dt, const int32_t* tok, const void* dx0, float* dwte, float
                int s, int h, cudaStream_t st) {
   if (rows <= 0) return;
   if (rows > 8192) throw CudaError("embed_bwd: at most 8192 tokens per microbatch");
-  k_sort_tokens<<<1, 1024, 0, st>>>(tok, keys, rows);
+  launch(PDL_OPS, k_sort_tokens, 1, 1024, 0, st, tok, keys, rows);
   ZB_LAUNCH_CHECK();
   const int blocks = (rows * 32 + 255) / 256;
   const int thr = h / 8 < 256 ? ((h / 8 + 31) / 32) * 32 : 256;
   if (dt == DT_BF16) {
-    k_embed_bwd_wte<bf16><<<blocks, 256, 0, st>>>(keys, static_cast<const bf16*>(dx0), dwte, rows, h);
-    k_embed_bwd_wpe<bf16><<<s < rows ? s : rows, thr, 0, st>>>(static_cast<const bf16*>(dx0), dwpe, rows, s, h);
+    launch(PDL_OPS, k_embed_bwd_wte<bf16>, blocks, 256, 0, st, keys, static_cast<const bf16*>(dx0), dwte, rows, h);
+    launch(PDL_OPS, k_embed_bwd_wpe<bf16>, s < rows ? s : rows, thr, 0, st, static_cast<const bf16*>(dx0), dwpe, rows, s, h);
   } else {
-    k_embed_bwd_wte<float><<<blocks, 256, 0, st>>>(keys, static_cast<const float*>(dx0), dwte, rows, h);
-    k_embed_bwd_wpe<float><<<s < rows ? s : rows, thr, 0, st>>>(static_cast<const float*>(dx0), dwpe, rows, s, h);
+    launch(PDL_OPS, k_embed_bwd_wte<float>, blocks, 256, 0, st, keys, static_cast<const float*>(dx0), dwte, rows, h);
+    launch(PDL_OPS, k_embed_bwd_wpe<float>, s < rows ? s : rows, thr, 0, st, static_cast<const float*>(dx0), dwpe, rows, s, h);
   }
   ZB_LAUNCH_CHECK();
 }
@@ -836,11 +855,11 @@ void cross_entropy(DType dt, const float* logits, const int32_t* labels, void* d
   if (rows <= 0) return;
   if (V % 8) throw CudaError("cross_entropy: V must be a multiple of 8");
   if (dt == DT_BF16)
-    k_ce<bf16><<<rows, 1024, 0, st>>>(logits, labels, static_cast<bf16*>(dlogits), loss_rows, V, inv_scale);
+    launch(PDL_OPS, k_ce<bf16>, rows, 1024, 0, st, logits, labels, static_cast<bf16*>(dlogits), loss_rows, V, inv_scale);
   else
-    k_ce<float><<<rows, 1024, 0, st>>>(logits, labels, static_cast<float*>(dlogits), loss_rows, V, inv_scale);
+    launch(PDL_OPS, k_ce<float>, rows, 1024, 0, st, logits, labels, static_cast<float*>(dlogits), loss_rows, V, inv_scale);
   ZB_LAUNCH_CHECK();
-  k_loss_reduce<<<1, 1024, 0, st>>>(loss_rows, loss_acc, rows, inv_scale);
+  launch(PDL_OPS, k_loss_reduce, 1, 1024, 0, st, loss_rows, loss_acc, rows, inv_scale);
   ZB_LAUNCH_CHECK();
 }
 
@@ -851,39 +870,39 @@ void convert_rows(DType dt, const float* src, void* dst, int64_t n, cudaStream_t
 void convert_f32(DType dt, const float* src, void* dst, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
-  if (dt == DT_BF16) k_convert<bf16><<<blocks, 256, 0, st>>>(src, static_cast<bf16*>(dst), n);
-  else k_convert<float><<<blocks, 256, 0, st>>>(src, static_cast<float*>(dst), n);
+  if (dt == DT_BF16) launch(PDL_OPS, k_convert<bf16>, blocks, 256, 0, st, src, static_cast<bf16*>(dst), n);
+  else launch(PDL_OPS, k_convert<float>, blocks, 256, 0, st, src, static_cast<float*>(dst), n);
   ZB_LAUNCH_CHECK();
 }
 
 void grad_norm(const float* g, int64_t n, double* part, int32_t* nf_part, PvState* pst, cudaStream_t st) {
-  k_sumsq<<<kNormBlocks, 512, 0, st>>>(g, n, part, nf_part);
+  launch(PDL_OPS, k_sumsq, kNormBlocks, 512, 0, st, g, n, part, nf_part);
   ZB_LAUNCH_CHECK();
-  k_sumsq_final<<<1, 32, 0, st>>>(part, nf_part, kNormBlocks, pst);
+  launch(PDL_OPS, k_sumsq_final, 1, 32, 0, st, part, nf_part, kNormBlocks, pst);
   ZB_LAUNCH_CHECK();
 }
 
 void pv_combine(PvState* pst, cudaStream_t st) {
-  k_pv_combine<<<1, 1, 0, st>>>(pst);
+  launch(PDL_OPS, k_pv_combine, 1, 1, 0, st, pst);
   ZB_LAUNCH_CHECK();
 }
 void pv_decide_first(PvState* pst, float clip, int sync_mode, cudaStream_t st) {
-  k_pv_decide_first<<<1, 1, 0, st>>>(pst, clip, sync_mode);
+  launch(PDL_OPS, k_pv_decide_first, 1, 1, 0, st, pst, clip, sync_mode);
   ZB_LAUNCH_CHECK();
 }
 void pv_decide_final(PvState* pst, float clip, cudaStream_t st) {
-  k_pv_decide_final<<<1, 1, 0, st>>>(pst, clip);
+  launch(PDL_OPS, k_pv_decide_final, 1, 1, 0, st, pst, clip);
   ZB_LAUNCH_CHECK();
 }
 void pv_finish_apply(PvState* pst, cudaStream_t st) {
-  k_pv_finish<<<1, 1, 0, st>>>(pst);
+  launch(PDL_OPS, k_pv_finish, 1, 1, 0, st, pst);
   ZB_LAUNCH_CHECK();
 }
 void adamw_apply(float* theta, float* m, float* v, const float* g, bf16* shadow, int64_t n, int64_t n_wd,
                  int64_t n_shadow, float lr, float b1, float b2, float eps, float wd, const PvState* pst,
                  cudaStream_t st) {
   const int blocks = static_cast<int>(std::min<int64_t>((n + 511) / 512, 148 * 8));
-  k_adamw<<<blocks, 512, 0, st>>>(theta, m, v, g, shadow, n, n_wd, n_shadow, lr, b1, b2, eps, wd, pst);
+  launch(PDL_OPS, k_adamw, blocks, 512, 0, st, theta, m, v, g, shadow, n, n_wd, n_shadow, lr, b1, b2, eps, wd, pst);
   ZB_LAUNCH_CHECK();
 }
 
