@@ -1,17 +1,15 @@
 // Causal flash-attention FORWARD on tcgen05 (bf16, s % 128 == 0).
 //
-// One CTA per (128-query block, head, sequence), heavy blocks first.
-//   warp 0      TMA: Q once; K_j (3-stage ring, one block ahead), V_j (2-stage ring) (boxes {64 cols, 128 rows}
-//               of the packed qkv [b*s, 3h], 128B swizzle)
-//   warp 1      MMA: S_j = Q K_j^T into one of two TMEM S buffers (128 cols each),
-//               O += P_j V_j into the TMEM O accumulator (D cols); S_{j+1} is issued
-//               before PV_j so the next QK^T overlaps this block's softmax
+// One CTA per (pair of 128-query tiles, head, sequence), heaviest pairs first.
+//   warp 0      TMA: Q_0, Q_1 once; K_j, V_j in 2-stage rings (boxes {64 cols, 128 rows} of the
+//               packed qkv [b*s, 3h], 128B swizzle), shared by both query tiles
+//   warp 1      MMA: S_t = Q_t K_j^T (SS) and O_t += P_t V_j (TS, P from TMEM), ping-ponging
+//               between the two tiles so one tile's softmax overlaps the other tile's products
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-11  softmax, a row per thread pair (TMEM lane = row, one key half each): tcgen05.ld S,
-//               causal mask, online max / sum in base 2, O rescale in TMEM
-//               (tcgen05.ld/st, lazy: only when a row max grows by > 8), bf16 P written
-//               into TMEM over its S buffer (tcgen05.st) and consumed by a TS MMA (A from
-//               TMEM); finally O / l -> bf16 rows and the log-sum-exp.
+//   warps 4-7   softmax of tile 0, warps 8-11 softmax of tile 1: one row per thread (TMEM lane =
+//               row), all 128 keys of a block in registers: causal mask, row max, lazy O rescale
+//               (only when the max grows by > 8 in log2 units), exp2, bf16 P written into TMEM
+//               over S; finally O / l -> bf16 rows and the log-sum-exp.
 // Operand layouts: Q, K are K-major SW128 (atoms of 64 elements x 8 rows);
 // V is the MN-major B operand of PV (d contiguous), read from the same TMA boxes.
 #include <math.h>
@@ -27,23 +25,38 @@ constexpr int BQ = 128, BKV = 128;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
-// barrier among the softmax warps only (ids 1+; 0 is __syncthreads)
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+// 2^x on the FMA pipe for x in [-126, 9): round-to-nearest split x = j + f (f in [-1/2, 1/2]) with
+// the 1.5 * 2^23 shifter, a cubic for 2^f (max relative error 8e-5, far below bf16's 2^-9), and
+// j added to the exponent field.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05516014f, f, 0.24258275f), f, 0.69326056f), f, 0.99993022f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+
+constexpr bool kPolyExp = false;  // measured slower on B200 (the softmax is not MUFU-bound here)
 
 template <int D> struct FwdCfg {
   static constexpr int ATOMS = (D + 63) / 64;           // 64-column TMA boxes per tile
   static constexpr int TILE = ATOMS * 128 * 128;        // bytes of one 128-row tile (Q, K or V)
-  static constexpr int KST = 3, VST = 2;                // K ring (freed after S_j), V ring (freed after PV_j)
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = TILE;
-  static constexpr int OFF_V = (1 + KST) * TILE;
-  static constexpr int OFF_BAR = (1 + KST + VST) * TILE;
-  static constexpr int OFF_RED = OFF_BAR + 256;          // 768 f32
-  static constexpr int SMEM = OFF_RED + 3072 + 1024;
+  static constexpr int KST = 2, VST = 2;                // K ring (freed after S0_j, S1_j), V ring (after PV0_j, PV1_j)
+  static constexpr int OFF_Q = 0;                       // Q0, Q1
+  static constexpr int OFF_K = 2 * TILE;
+  static constexpr int OFF_V = (2 + KST) * TILE;
+  static constexpr int OFF_BAR = (2 + KST + VST) * TILE;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 
+// One CTA per (pair of 128-query tiles {2t, 2t+1}, head, sequence), heaviest pairs first.
+// TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256, 256+D), O_1 [384, 384+D);
+// P_t (bf16 pairs) is written over the first 64 columns of S_t.
+// MMA issue order per key block j:  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) — the tensor core
+// runs one tile's products while the other tile's softmax warps work.  S_t(j+1) overwrites the
+// P_t(j) that PV_t(j), issued just before it, reads: tcgen05.mma of one thread execute in issue
+// order.  The commit after S_t(j+1) also covers PV_t(j), so the softmax warps may rescale O_t
+// as soon as they see S_t(j+1).
 template <int D>
 __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o,
                                                    float* __restrict__ lse, int s, int a, float scale_log2) {
@@ -52,39 +65,37 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;     // [3]
-  uint64_t* k_empty = bar + 4;    // [3]
-  uint64_t* v_full = bar + 7;     // [2]
-  uint64_t* v_empty = bar + 9;    // [2]
-  uint64_t* s_full = bar + 11;    // [2]
-  uint64_t* s_empty = bar + 13;   // [2]
-  uint64_t* p_full = bar + 15;
-  uint64_t* o_done = bar + 16;
-  uint64_t* o_final = bar + 17;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 18);
+  uint64_t* k_full = bar + 1;     // [2]
+  uint64_t* k_empty = bar + 3;    // [2]
+  uint64_t* v_full = bar + 5;     // [2]
+  uint64_t* v_empty = bar + 7;    // [2]
+  uint64_t* s_full = bar + 9;     // [2] per tile
+  uint64_t* p_full = bar + 11;    // [2] per tile
+  uint64_t* o_final = bar + 13;   // [2] per tile
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / BQ;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
+  const int npair = (nqb + 1) / 2;
+  const int pr = npair - 1 - static_cast<int>(blockIdx.x);
   const int hd = blockIdx.y, bb = blockIdx.z;
   const int h = a * D;
-  const int nkv = qb + 1;
+  const int q0 = 2 * pr;
+  const bool two = q0 + 1 < nqb;
+  const int nkv0 = q0 + 1, nkv1 = two ? q0 + 2 : 0;
+  const int nkv = two ? nkv1 : nkv0;
 
   if (threadIdx.x == 0) {
     sm100::mbar_init(q_full, 1);
-    for (int i = 0; i < C::KST; ++i) {
+    for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&k_full[i], 1);
       sm100::mbar_init(&k_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&v_full[i], 1);
       sm100::mbar_init(&v_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1);
-      sm100::mbar_init(&s_empty[i], 1);  // released by the PV that consumed the P aliased over S
+      sm100::mbar_init(&p_full[i], 128);
+      sm100::mbar_init(&o_final[i], 1);
     }
-    sm100::mbar_init(p_full, 256);
-    sm100::mbar_init(o_done, 1);
-    sm100::mbar_init(o_final, 1);
     sm100::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) sm100::tma_prefetch(&tm);
@@ -95,17 +106,18 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
   pdl_wait();
   const uint32_t tbase = *tslot;
-  const uint32_t t_s0 = tbase, t_o = tbase + 256;
   const int row0 = bb * s;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA
-      sm100::mbar_arrive_expect_tx(q_full, C::TILE);
-      for (int at = 0; at < C::ATOMS; ++at)
-        sm100::tma_load_2d(smem + C::OFF_Q + at * 16384, &tm, q_full, hd * D + 64 * at, row0 + qb * BQ);
+      sm100::mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * C::TILE);
+      for (int t = 0; t < (two ? 2 : 1); ++t)
+        for (int at = 0; at < C::ATOMS; ++at)
+          sm100::tma_load_2d(smem + C::OFF_Q + t * C::TILE + at * 16384, &tm, q_full, hd * D + 64 * at,
+                             row0 + (q0 + t) * BQ);
       auto load_k = [&](int j) {
-        const int st = j % C::KST;
-        sm100::mbar_wait(&k_empty[st], ((j / C::KST) & 1) ^ 1);
+        const int st = j & 1;
+        sm100::mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         sm100::mbar_arrive_expect_tx(&k_full[st], C::TILE);
         for (int at = 0; at < C::ATOMS; ++at)
           sm100::tma_load_2d(smem + C::OFF_K + st * C::TILE + at * 16384, &tm, &k_full[st], h + hd * D + 64 * at,
@@ -130,138 +142,151 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = sm100::idesc_bf16(128, D, false, true);
       const uint32_t sq = sm100::smem_addr(smem + C::OFF_Q);
-      auto issue_pv = [&](int j, bool last) {
-        const int st = j & 1;
-        sm100::mbar_wait(&v_full[st], (j >> 1) & 1);
-        sm100::mbar_wait(p_full, j & 1);
-        sm100::tc_fence_after();
-        const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + st * C::TILE);
-        const uint32_t tp = t_s0 + st * 128;  // P_j (bf16 pairs) aliased over S_j
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t bd = sm100::smem_desc(sv + kk * 2048, 16384, 1024, sm100::kSwizzle128B);
-          sm100::mma_bf16_ts(t_o, tp + kk * 8, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
-        }
-        sm100::mma_commit(o_done);
-        sm100::mma_commit(&s_empty[st]);
-        sm100::mma_commit(&v_empty[st]);
-        if (last) sm100::mma_commit(o_final);
-      };
-      sm100::mbar_wait(q_full, 0);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j % C::KST, sb = j & 1;
-        sm100::mbar_wait(&k_full[st], (j / C::KST) & 1);
-        sm100::mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-        sm100::tc_fence_after();
-        const uint32_t sk = sm100::smem_addr(smem + C::OFF_K + st * C::TILE);
+      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
+        const uint32_t sk = sm100::smem_addr(smem + C::OFF_K + (j & 1) * C::TILE);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          sm100::mma_bf16_ss(t_s0 + sb * 128, sm100::smem_desc(sq + off, 16, 1024, sm100::kSwizzle128B),
+          sm100::mma_bf16_ss(tbase + t * 128, sm100::smem_desc(sq + t * C::TILE + off, 16, 1024, sm100::kSwizzle128B),
                              sm100::smem_desc(sk + off, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
         }
-        sm100::mma_commit(&s_full[sb]);
-        sm100::mma_commit(&k_empty[st]);
-        if (j > 0) issue_pv(j - 1, false);
-      }
-      issue_pv(nkv - 1, true);
-    }
-  } else if (warp >= 4) {  // ---------------- softmax: two warps per row group, one key half each
-    const int qw = warp & 3, hf = (warp - 4) >> 2;
-    const int r = qw * 32 + lane;  // row within the block = TMEM lane
-    const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
-    float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [2 parity][2][128] maxima, [2][128] sums
-    float m = -INFINITY, l = 0.f;  // m: running max (log2 units) shared by both halves; l: this half's sum
-    for (int j = 0; j < nkv; ++j) {
-      const int sb = j & 1;
-      sm100::mbar_wait(&s_full[sb], (j >> 1) & 1);
-      sm100::tc_fence_after();
-      float sv[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        sm100::tmem_ld32(t_s0 + sb * 128 + hf * 64 + lane_off + c * 32, reinterpret_cast<uint32_t*>(sv + 32 * c));
-      sm100::tmem_ld_wait();
-      float mx = -INFINITY;
-      const bool diag = j == qb;
-#pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        float x = sv[k] * scale_log2;
-        if (diag && hf * 64 + k > r) x = -INFINITY;
-        sv[k] = x;
-        mx = fmaxf(mx, x);
-      }
-      float* rj = red + (j & 1) * 256;  // double-buffered by block parity: no write-after-read race
-      rj[hf * 128 + r] = mx;
-      named_sync(1, 256);
-      mx = fmaxf(mx, rj[(hf ^ 1) * 128 + r]);
-      // lazy rescaling: keep the old reference max unless it grew by more than 8 (p <= 2^8)
-      float corr = 1.f;
-      if (mx > m + 8.f) {
-        corr = sm100::ex2(m - mx);
-        m = mx;
-      }
-      float sum = 0.f;
-#pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        const float pv = sm100::ex2(sv[k] - m);
-        sv[k] = pv;
-        sum += pv;
-      }
-      l = l * corr + sum;
-      if (j > 0) {  // PV_{j-1} has finished: O may be rescaled and the P buffer is free
-        sm100::mbar_wait(o_done, (j - 1) & 1);
+        sm100::mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
+        sm100::mbar_wait(&p_full[t], j & 1);
         sm100::tc_fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {
+        const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + (j & 1) * C::TILE);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t bd = sm100::smem_desc(sv + kk * 2048, 16384, 1024, sm100::kSwizzle128B);
+          sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+        }
+      };
+      sm100::mbar_wait(q_full, 0);
+      sm100::mbar_wait(&k_full[0], 0);
+      sm100::tc_fence_after();
+      issue_s(0, 0);
+      if (two) issue_s(1, 0);
+      sm100::mma_commit(&k_empty[0]);
+      for (int j = 0; j < nkv; ++j) {
+        const bool more = j + 1 < nkv;
+        sm100::mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        if (more) sm100::mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        sm100::tc_fence_after();
+        if (j < nkv0) {
+          issue_pv(0, j);
+          if (j == nkv0 - 1) sm100::mma_commit(&o_final[0]);
+        }
+        if (j + 1 < nkv0) issue_s(0, j + 1);
+        if (j < nkv1) {
+          issue_pv(1, j);
+          if (j == nkv1 - 1) sm100::mma_commit(&o_final[1]);
+        }
+        sm100::mma_commit(&v_empty[j & 1]);
+        if (j + 1 < nkv1) issue_s(1, j + 1);
+        if (more) sm100::mma_commit(&k_empty[(j + 1) & 1]);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- softmax: 4 warps per tile, one row per thread
+    const int t = (warp - 4) >> 2;
+    const int nk = t == 0 ? nkv0 : nkv1;
+    const int r = (warp & 3) * 32 + lane;  // row within the tile = TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t t_s = tbase + t * 128 + lane_off, t_o = tbase + 256 + t * 128 + lane_off;
+    const int qt = q0 + t;
+    float m = -INFINITY, l = 0.f;  // m: reference max (log2 units), l: running sum relative to m
+    for (int j = 0; j < nk; ++j) {
+      sm100::mbar_wait(&s_full[t], j & 1);
+      sm100::tc_fence_after();
+      float sv[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sm100::tmem_ld32(t_s + c * 32, reinterpret_cast<uint32_t*>(sv + 32 * c));
+      sm100::tmem_ld_wait();
+      if (j == qt) {
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if (k > r) sv[k] = -INFINITY;
+      }
+      float mx;
+      {  // 8 independent chains, then a tree (a single 128-long chain is pure latency)
+        float m8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m8[i] = sv[i];
+#pragma unroll
+        for (int k = 8; k < 128; ++k) m8[k & 7] = fmaxf(m8[k & 7], sv[k]);
+        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      }
+      mx *= scale_log2;
+      // lazy rescaling: keep the old reference max unless it grew by more than 8 (p <= 2^8)
+      if (mx > m + 8.f) {
+        const float corr = sm100::ex2(m - mx);
+        m = mx;
+        l *= corr;
+        if (j > 0) {  // O_t holds blocks < j (PV_t(j-1) completed before S_t(j) was committed)
 #pragma unroll 1
-          for (int c = hf; c < D / 32; c += 2) {
+          for (int c = 0; c < D / 32; ++c) {
             uint32_t ov[32];
-            sm100::tmem_ld32(t_o + lane_off + c * 32, ov);
+            sm100::tmem_ld32(t_o + c * 32, ov);
             sm100::tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-            sm100::tmem_st32(t_o + lane_off + c * 32, ov);
+            sm100::tmem_st32(t_o + c * 32, ov);
           }
           sm100::tmem_st_wait();
         }
       }
-      // P row half -> TMEM over this S buffer: keys [64 hf, 64 hf + 64) -> columns [32 hf, 32 hf + 32)
-      // (both halves finished reading S before the max exchange above)
-      uint32_t pk[32];
+      const float mneg = -m;
+      const bool poly = kPolyExp && j != qt;  // masked (-inf) scores only on the diagonal block: MUFU there
+      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        __nv_bfloat162 v2 = __floats2bfloat162_rn(sv[2 * i], sv[2 * i + 1]);
-        pk[i] = *reinterpret_cast<uint32_t*>(&v2);
+      for (int hf = 0; hf < 2; ++hf) {  // keys [64 hf, 64 hf + 64) -> P columns [32 hf, 32 hf + 32)
+        uint32_t pk[32];
+#pragma unroll
+        for (int k = 0; k < 64; k += 2) {
+          const float x0 = fmaf(sv[64 * hf + k], scale_log2, mneg), x1 = fmaf(sv[64 * hf + k + 1], scale_log2, mneg);
+          float p0, p1;
+          if ((k & 6) == 6 && poly) {  // a quarter of the exponentials on the FMA pipe (MUFU is the bottleneck)
+            p0 = ex2_poly(x0);
+            p1 = ex2_poly(x1);
+          } else {
+            p0 = sm100::ex2(x0);
+            p1 = sm100::ex2(x1);
+          }
+          sum4[(k >> 1) & 3] += p0 + p1;
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+          pk[k >> 1] = *reinterpret_cast<uint32_t*>(&v2);
+        }
+        sm100::tmem_st32(t_s + 32 * hf, pk);
       }
-      sm100::tmem_st32(t_s0 + sb * 128 + hf * 32 + lane_off, pk);
+      l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
-      sm100::mbar_arrive(p_full);
+      sm100::mbar_arrive(&p_full[t]);
     }
-    red[512 + hf * 128 + r] = l;
-    named_sync(1, 256);
-    l += red[512 + (hf ^ 1) * 128 + r];
-    sm100::mbar_wait(o_final, 0);
-    sm100::tc_fence_after();
-    const int q = qb * BQ + r;
-    const float inv = 1.f / l;
-    bf16* orow = o + (static_cast<int64_t>(bb) * s + q) * h + hd * D;
+    if (nk > 0) {
+      sm100::mbar_wait(&o_final[t], 0);
+      sm100::tc_fence_after();
+      const int q = qt * BQ + r;
+      const float inv = 1.f / l;
+      bf16* orow = o + (static_cast<int64_t>(bb) * s + q) * h + hd * D;
 #pragma unroll 1
-    for (int c = hf; c < D / 32; c += 2) {
-      uint32_t ov[32];
-      sm100::tmem_ld32(t_o + lane_off + c * 32, ov);
-      sm100::tmem_ld_wait();
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t ov[32];
+        sm100::tmem_ld32(t_o + c * 32, ov);
+        sm100::tmem_ld_wait();
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        uint4 u;
-        __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
+        for (int g = 0; g < 4; ++g) {
+          uint4 u;
+          __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * g + 2 * e]) * inv,
-                                        __uint_as_float(ov[8 * g + 2 * e + 1]) * inv);
-        *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
+          for (int e = 0; e < 4; ++e)
+            hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * g + 2 * e]) * inv,
+                                          __uint_as_float(ov[8 * g + 2 * e + 1]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
+        }
       }
+      lse[(static_cast<int64_t>(bb) * a + hd) * s + q] = (m + log2f(l)) * LN2;
     }
-    if (hf == 0) lse[(static_cast<int64_t>(bb) * a + hd) * s + q] = (m + log2f(l)) * LN2;
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -286,7 +311,7 @@ static void fwd_tc_launch(const AttnShape& sh, const void* qkv, void* o, float* 
   }
   const int h = sh.a * D;
   CUtensorMap tm = make_qkv_tmap(qkv, sh.b * sh.s, 3 * h);
-  dim3 grid(sh.s / attn_tc::BQ, sh.a, sh.b);
+  dim3 grid((sh.s / attn_tc::BQ + 1) / 2, sh.a, sh.b);
   launch(PDL_ATTN, attn_tc::k_fwd_tc<D>, grid, 384, C::SMEM, st, tm, static_cast<bf16*>(o), lse, sh.s, sh.a,
                                                    attn_tc::LOG2E / sqrtf(static_cast<float>(D)));
   ZB_LAUNCH_CHECK();
