@@ -94,6 +94,32 @@ zb_status_t zb_simulate(int32_t p, int32_t m, zb_pass_t* passes, int32_t n, cons
                         const int64_t* T_B, const int64_t* T_W, int64_t T_comm, int64_t M_B, int64_t M_W,
                         int32_t fused, zb_sim_t* sim);
 
+/* Schedules whose workers hold several model chunks ("virtual stages"
+ * v in [0, chunks * p)), each chunk a contiguous block of layers:
+ *   ZB_V      (chunks must be 2; §6): V placement — v < p
+ *             on worker v, v >= p on worker 2p-1-v; the three-phase
+ *             construction of P:410-411 and the W right-shift within M_limit
+ *             (P:413), DESIGN.md R-zbv.  sim->chosen: 0 construction, 1 / 2
+ *             W right-shift rule "gap" / "fill", whichever simulates fastest.
+ *   ZB_1F1B_I (interleaved 1F1B, the Table 4 baseline): v on worker
+ *             v mod p, Megatron-LM order (R-1f1bi), fused backward
+ *             (simulated with the upstream B waiting for the downstream W);
+ *             m must be a multiple of p.  sim->chosen = -1.
+ * T_F/T_B/T_W and M_B/M_W are PER CHUNK PASS (a chunk holds 1/chunks of a
+ * stage's layers).  M_limit: per-worker activation budget for the ZB-V
+ * right-shift (<= 0: the construction's own peak, i.e. p stage-M_B).
+ * out[0 .. 3*chunks*p*m) receives worker 0's list, then worker 1's, ...
+ * each in execution order; in every pass `stage` is the VIRTUAL stage v
+ * (the pipeline position of its chunk), `slot` the stash slot of chunk v.
+ * sim: cost / work / bubble_rate per worker (work = busiest worker's busy
+ * time), peak_bytes[w] per worker, n_slots[v] per virtual stage.
+ * Errors: ZB_EINVAL (p < 1, m < 1, chunks * p > 64, chunks != 2 for ZB_V,
+ * m % p != 0 for ZB_1F1B_I, bad family), ZB_ECAP (out_cap < 3*chunks*p*m). */
+enum { ZB_V = 4, ZB_1F1B_I = 5 };
+zb_status_t zb_schedule_chunked(int32_t p, int32_t m, int32_t chunks, int64_t T_F, int64_t T_B, int64_t T_W,
+                                int64_t T_comm, int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family,
+                                zb_pass_t* out, int32_t out_cap, zb_sim_t* sim);
+
 /* ------------------------------------------------------------------------ */
 /* Stage context: one pipeline stage on one GPU                              */
 /* ------------------------------------------------------------------------ */

@@ -17,6 +17,8 @@ ZB_OK, ZB_EINVAL, ZB_ELIMIT, ZB_ECAP, ZB_ECUDA, ZB_ENCCL, ZB_ESTATE, ZB_ETIMEOUT
 ZB_F, ZB_B, ZB_W = 0, 1, 2
 ZB_1F1B, ZB_H1, ZB_H2, ZB_AUTO = 0, 1, 2, 3
 FAMILY = {"1f1b": ZB_1F1B, "zbh1": ZB_H1, "zbh2": ZB_H2, "auto": ZB_AUTO}
+ZB_V, ZB_1F1B_I = 4, 5
+CHUNKED_FAMILY = {"zbv": ZB_V, "1f1bi": ZB_1F1B_I}
 ZB_DTYPE_BF16, ZB_DTYPE_F32 = 0, 1
 ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING = 1, 2
 ZB_OPT_SYNC, ZB_OPT_PV = 0, 1
@@ -80,6 +82,8 @@ _SIGS = {
     "zb_version": ([], C.c_char_p),
     "zb_schedule": ([_I32, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, C.POINTER(zb_pass_t), _I32,
                      C.POINTER(zb_sim_t)], _I32),
+    "zb_schedule_chunked": ([_I32, _I32, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, C.POINTER(zb_pass_t),
+                             _I32, C.POINTER(zb_sim_t)], _I32),
     "zb_simulate": ([_I32, _I32, C.POINTER(zb_pass_t), _I32, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64),
                      _I64, _I64, _I64, _I32, C.POINTER(zb_sim_t)], _I32),
     "zb_dbg_gemm": ([_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _P, _P, _I64, _I32, _P],

@@ -10,7 +10,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._lib import (FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING,
+from ._lib import (CHUNKED_FAMILY, FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING,
                    ACTIONS, check, lib, zb_iter_stats_t, zb_model_cfg_t, zb_optim_cfg_t, zb_pass_t, zb_pv_report_t,
                    zb_sim_t)
 
@@ -28,6 +28,24 @@ def schedule(family: str, p: int, m: int, T_F: int, T_B: int, T_W: int, T_comm: 
     check(lib.zb_schedule(p, m, int(T_F), int(T_B), int(T_W), int(T_comm), int(M_limit), int(M_B), int(M_W),
                           FAMILY[family], out, n, C.byref(sim)))
     return out, sim
+
+
+def schedule_chunked(family: str, p: int, m: int, chunks: int, T_F: int, T_B: int, T_W: int, T_comm: int = 0,
+                     M_limit: int = 0, M_B: int = 1, M_W: int = 1):
+    """zb_schedule_chunked ("zbv" | "1f1bi") -> (passes, sim).  passes are
+    grouped by WORKER; each pass's `stage` is its virtual stage (chunk)."""
+    n = 3 * chunks * p * m
+    out = (zb_pass_t * n)()
+    sim = zb_sim_t()
+    check(lib.zb_schedule_chunked(p, m, chunks, int(T_F), int(T_B), int(T_W), int(T_comm), int(M_limit), int(M_B),
+                                  int(M_W), CHUNKED_FAMILY[family], out, n, C.byref(sim)))
+    return out, sim
+
+
+def worker_lists(passes, p: int, m: int, chunks: int) -> List[List[Tuple[str, int, int]]]:
+    """Split a zb_schedule_chunked output into per-worker (kind, v, j) lists."""
+    per = 3 * chunks * m
+    return [[(KIND_NAME[q.kind], q.stage, q.microbatch) for q in passes[w * per:(w + 1) * per]] for w in range(p)]
 
 
 def stage_lists(passes, p: int) -> List[List[Tuple[str, int]]]:

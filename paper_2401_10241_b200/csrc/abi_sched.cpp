@@ -138,6 +138,66 @@ extern "C" zb_status_t zb_simulate(int32_t p, int32_t m, zb_pass_t* passes, int3
   ZB_CATCH
 }
 
+extern "C" zb_status_t zb_schedule_chunked(int32_t p, int32_t m, int32_t chunks, int64_t T_F, int64_t T_B,
+                                           int64_t T_W, int64_t T_comm, int64_t M_limit, int64_t M_B, int64_t M_W,
+                                           int32_t family, zb_pass_t* out, int32_t out_cap, zb_sim_t* sim) {
+  ZB_TRY {
+    if (p < 1 || m < 1 || chunks < 1 || static_cast<int64_t>(chunks) * p > ZB_MAX_STAGES)
+      return set_error(ZB_EINVAL, "need p >= 1, m >= 1, 1 <= chunks * p <= 64");
+    if (T_F < 0 || T_B < 0 || T_W < 0 || T_comm < 0 || M_B < 0 || M_W < 0)
+      return set_error(ZB_EINVAL, "times and memory must be >= 0");
+    const int64_t n = 3LL * chunks * p * m;
+    if (out != nullptr && static_cast<int64_t>(out_cap) < n) return set_error(ZB_ECAP, "out_cap < 3*chunks*p*m");
+    const int nv = chunks * p;
+    sched::VLists lists;
+    std::vector<int> place(nv);
+    int chosen = -1;
+    bool fused = false;
+    if (family == ZB_V) {
+      if (chunks != 2) return set_error(ZB_EINVAL, "ZB-V needs chunks == 2");
+      lists = sched::zbv_schedule(p, m, T_F, T_B, T_W, T_comm, M_B, M_W, M_limit, &chosen);
+      for (int v = 0; v < nv; ++v) place[v] = sched::zbv_worker(p, v);
+    } else if (family == ZB_1F1B_I) {
+      if (m % p) return set_error(ZB_EINVAL, "1F1B-I needs m divisible by p");
+      lists = sched::build_1f1b_interleaved(p, m, chunks);
+      for (int v = 0; v < nv; ++v) place[v] = v % p;
+      fused = true;
+    } else {
+      return set_error(ZB_EINVAL, "zb_schedule_chunked: family must be ZB_V or ZB_1F1B_I");
+    }
+    std::vector<int64_t> tf(nv, T_F), tb(nv, T_B), tw(nv, T_W);
+    const sched::VSimResult r = sched::simulate_v(lists, nv, place, tf, tb, tw, T_comm, fused);
+    std::vector<int> counts;
+    auto slots = sched::assign_slots_v(lists, nv, &counts);
+    auto peaks = sched::memory_peaks_v(lists, M_B, M_W);
+    if (out != nullptr) {
+      size_t k = 0;
+      for (int w = 0; w < p; ++w)
+        for (size_t i = 0; i < lists[w].size(); ++i) {
+          zb_pass_t& q = out[k++];
+          q.stage = lists[w][i].v;
+          q.microbatch = lists[w][i].j;
+          q.kind = lists[w][i].kind;
+          q.slot = slots[w][i];
+          q.start = r.start[w][i];
+          q.end = r.end[w][i];
+        }
+    }
+    if (sim != nullptr) {
+      std::memset(sim, 0, sizeof(*sim));
+      sim->cost = r.cost;
+      sim->work = r.work;
+      sim->bubble_rate = r.bubble_rate;
+      for (int w = 0; w < p; ++w) sim->peak_bytes[w] = peaks[w];
+      for (int v = 0; v < nv; ++v) sim->n_slots[v] = counts[v];
+      sim->chosen = chosen;
+      sim->n_passes = static_cast<int32_t>(n);
+    }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 // ---------------------------------------------------------------- P2P plans (host only)
 #include "plan.h"
 #include "zb_debug.h"

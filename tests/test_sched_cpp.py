@@ -110,3 +110,62 @@ def test_errors():
     assert lib.zb_schedule(4, 8, 1, 1, 1, 0, 0, 1, 1, 1, out, 5, None) == ZB_ECAP
     assert lib.zb_schedule(0, 8, 1, 1, 1, 0, 0, 1, 1, 1, out, 5, None) == ZB_EINVAL
     assert lib.zb_schedule(2, 2, 1, 1, 1, 0, 0, 1, 1, 9, out, 12, None) == ZB_EINVAL
+
+
+# ---------------------------------------------------------------- chunked schedules (ZB-V, 1F1B-I)
+
+def compare_chunked(family, p, m, chunks, TF, TB, TW, Tc, MB, MW, lim):
+    from oracle import zbv
+    passes, sim = api.schedule_chunked(family, p, m, chunks, TF, TB, TW, Tc, M_limit=lim, M_B=MB, M_W=MW)
+    nv = chunks * p
+    if family == "zbv":
+        lists, chosen, osim = zbv.zbv_schedule(p, m, TF, TB, TW, Tc, MB, MW, lim if lim > 0 else None)
+        place = lambda v: zbv.worker_of(p, v)
+        assert sim.chosen == chosen
+    else:
+        lists = zbv.build_1f1b_interleaved(p, m, chunks)
+        place = lambda v: v % p
+        osim = zbv.simulate_v(lists, nv, place, TF, TB, TW, Tc, fused=True)
+    assert api.worker_lists(passes, p, m, chunks) == lists, (family, p, m)
+    maps, counts = zbv.assign_slots_v(lists, nv)
+    k = 0
+    for w in range(p):
+        for kind, v, j in lists[w]:
+            q = passes[k]
+            assert q.slot == maps[(v, j)]
+            assert q.start == osim["start"][(kind, v, j)] and q.end == osim["end"][(kind, v, j)]
+            k += 1
+    assert sim.cost == osim["cost"] and sim.work == osim["work"]
+    assert list(sim.n_slots[:nv]) == counts
+    assert list(sim.peak_bytes[:p]) == zbv.memory_peaks_v(lists, MB, MW)
+
+
+@pytest.mark.parametrize("p,m", [(1, 1), (1, 4), (2, 3), (3, 5), (4, 8), (4, 12), (8, 24), (8, 7), (6, 40)])
+def test_zbv_unit_and_table8(p, m):
+    compare_chunked("zbv", p, m, 2, 1, 1, 1, 0, 1, 1, 0)
+    compare_chunked("zbv", p, m, 2, 9261, 9043, 4669, 601, 5, 3, 0)
+
+
+def test_zbv_random_limits():
+    rnd = random.Random(3)
+    for _ in range(40):
+        p, m = rnd.randint(1, 6), rnd.randint(1, 20)
+        TF, TB, TW, Tc = rnd.randint(1, 60), rnd.randint(1, 60), rnd.randint(1, 60), rnd.randint(0, 8)
+        MB, MW = rnd.randint(1, 9), rnd.randint(1, 9)
+        lim = rnd.choice([0, 2 * p * MB, 2 * p * MB + MB, 4 * p * MB])
+        compare_chunked("zbv", p, m, 2, TF, TB, TW, Tc, MB, MW, lim)
+
+
+@pytest.mark.parametrize("p,m,chunks", [(1, 2, 1), (2, 4, 2), (4, 8, 2), (4, 12, 3), (8, 24, 3), (8, 8, 4)])
+def test_interleaved(p, m, chunks):
+    compare_chunked("1f1bi", p, m, chunks, 6174, 6029, 3112, 601, 1, 1, 0)
+
+
+def test_chunked_errors():
+    from paper_2401_10241_b200._lib import ZbError
+    with pytest.raises(ZbError):
+        api.schedule_chunked("1f1bi", 4, 6, 2, 1, 1, 1)        # m % p != 0
+    with pytest.raises(ZbError):
+        api.schedule_chunked("zbv", 4, 8, 3, 1, 1, 1)          # ZB-V needs 2 chunks
+    with pytest.raises(ZbError):
+        api.schedule_chunked("zbv", 40, 8, 2, 1, 1, 1)         # 80 virtual stages > 64
