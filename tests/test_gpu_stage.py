@@ -234,3 +234,41 @@ def test_nan_skips_step_everywhere():
         assert r["full_nonfinite"] == 1 and r["t"] == 0
         for x, y in zip(c.get_params(), b):
             assert np.array_equal(x, y, equal_nan=True)
+
+
+def gpu_run_chunked(cfg, p, chunks, family, dtype):
+    """p workers holding `chunks` model chunks each (ZB-V / 1F1B-I) run as
+    chunks*p virtual-stage contexts in one process (zb_run_iteration_local)."""
+    import torch
+    from paper_2401_10241_b200 import api
+    nv = chunks * p
+    passes, sim = api.schedule_chunked(family, p, cfg.m, chunks, 10, 11, 6, 1, M_B=10, M_W=10)
+    ctxs = []
+    for v in range(nv):
+        c = api.Context(cfg, nv, v, cfg.m, max(1, sim.n_slots[v]), dtype=dtype)
+        params = zb_synth.make_stage_params(cfg, nv, v)
+        c.set_params([params[n] for n, _, _ in zb_synth.param_specs(cfg, nv, v)])
+        ctxs.append(c)
+    tok, lab = inputs(cfg)
+    api.run_local(ctxs, passes, torch.from_numpy(tok).cuda(), torch.from_numpy(lab).cuda())
+    grads = {}
+    for v, c in enumerate(ctxs):
+        for (name, shape, _), g in zip(zb_synth.param_specs(cfg, nv, v), c.get_grads()):
+            grads[name] = g.reshape(shape)
+    return ctxs[-1].loss(), grads
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_chunked_schedules_vs_oracle_and_bitwise(dtype):
+    """ZB-V and 1F1B-I on BASELINE configs[0] (8 layers,
+    p = 4 workers x 2 chunks of one layer): within tolerance of the oracle and
+    bitwise equal to 1F1B over the same 8 chunks."""
+    cfg = zb_synth.CONFIGS["tiny"]
+    ref_loss, ref = oracle_grads(cfg, dtype)
+    base_loss, base, _ = gpu_run(cfg, 8, dtype, "1f1b")
+    for fam in ("zbv", "1f1bi"):
+        loss, grads = gpu_run_chunked(cfg, 4, 2, fam, dtype)
+        check_tolerance(loss, grads, ref_loss, ref, dtype)
+        assert loss == base_loss, fam
+        for k in base:
+            assert np.array_equal(grads[k], base[k]), (fam, k)
