@@ -331,6 +331,16 @@ def predicted_bubbles(cfg, t_pass):
             continue
         _, sim = api.schedule(fam, p, cfg.m, us["F"], us["B"], us["W"], 20)
         out[fam] = round(sim.bubble_rate, 4)
+    # chunked schedules on the same per-layer times: ZB-V (2 chunks of Lmid/2 layers) and
+    # 1F1B-I with one layer per chunk (the Table 4 baseline); per-chunk pass times
+    half = {k: per_layer[k] * Lmid / 2 * 1000 for k in "FBW"}
+    _, sim = api.schedule_chunked("zbv", p, cfg.m, 2, int(round(half["F"])), int(round(half["B"])),
+                                  int(round(half["W"])), 20)
+    out["zbv"] = round(sim.bubble_rate, 4)
+    if cfg.m % p == 0:
+        one = {k: int(round(per_layer[k] * 1000)) for k in "FBW"}
+        _, sim = api.schedule_chunked("1f1bi", p, cfg.m, Lmid, one["F"], one["B"], one["W"], 20)
+        out["1f1bi"] = round(sim.bubble_rate, 4)
     out["measured_p1"] = 0.0
     return out
 
