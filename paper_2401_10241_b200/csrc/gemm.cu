@@ -12,6 +12,7 @@
 // (tfull/tempty) overlaps a tile's epilogue with the next tile's MMAs.
 #include <cudaTypedefs.h>
 
+#include <map>
 #include <mutex>
 #include <type_traits>
 
@@ -65,6 +66,20 @@ __device__ __forceinline__ void epi8(const EpiArgs& e, int64_t row, int col, flo
   }
 }
 
+// ------------------------------------------------------------------ ordered split-K flags
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// order generic-proxy flag accesses with async-proxy (TMA) global writes
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05 kernel
 namespace tc {
 constexpr int BM = 128, BK = 64;
@@ -100,7 +115,7 @@ __device__ __forceinline__ int swz(int lane, int j) { return lane * 128 + ((j ^ 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtensorMap* tmC, const CUtensorMap* tmX,
                                                 uint32_t taddr, uint8_t* buf, uint64_t* xbar, uint32_t& xph,
-                                                int row0, int col0, int ncols, int N, int lane) {
+                                                int row0, int col0, int ncols, int N, int lane, bool reduce) {
   using TO = OutT<EPI>;
   constexpr int CC = 128 / static_cast<int>(sizeof(TO));
   constexpr bool kAuxIn = EPI == EPI_RESID || EPI == EPI_GELU_BWD;
@@ -155,7 +170,7 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
     sm100::fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-      if (EPI == EPI_F32_ACC && ep.beta)
+      if (EPI == EPI_F32_ACC && reduce)
         sm100::tma_reduce_add_2d(tmC, buf, col, row0);
       else
         sm100::tma_store_2d(tmC, buf, col, row0);
@@ -320,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tc_fence_after();
       epilogue_chunks<EPI>(ep, &tmC, &tmX,
                            tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
-                           &xbar[warp - 4], xph, mt * BM + ew * 32, nt * BN + half * (BN / 2), BN / 2, N, lane);
+                           &xbar[warp - 4], xph, mt * BM + ew * 32, nt * BN + half * (BN / 2), BN / 2, N, lane, ep.beta != 0);
       sm100::tc_fence_before();
       sm100::mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
@@ -402,16 +417,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int num_m = (M + BM2 - 1) / BM2, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n, nk = (K + BK - 1) / BK;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  // work item t = split (t / tiles) of tile (t % tiles): every split-s item precedes every
+  // split-(s+1) item, and each CTA pair walks its items in increasing t, so the ordered
+  // split-K waits below cannot deadlock (all CTAs are resident: grid <= #SMs)
+  const int splits = EPI == EPI_F32_ACC ? ep.splits : 1;
+  const int items = tiles * splits;
+  auto kb_begin = [&](int sp) { return static_cast<int>((static_cast<int64_t>(nk) * sp) / splits); };
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t ph = 0;
-      for (int t = cid; t < tiles; t += ncl) {
+      for (int t = cid; t < items; t += ncl) {
         int mt, nt;
-        tile_coords(t, num_m, num_n, mt, nt);
+        tile_coords(t % tiles, num_m, num_n, mt, nt);
+        const int sp = t / tiles;
         const int m0 = mt * BM2 + static_cast<int>(rank) * BM, n0 = nt * BN + static_cast<int>(rank) * (BN / 2);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb_begin(sp); kb < kb_begin(sp + 1); ++kb) {
           sm100::mbar_wait(&empty[stage], ph ^ 1);
           const uint32_t fbar = sm100::map_to_cta(&full[stage], 0);
           if (leader)
@@ -445,11 +467,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = sm100::idesc_bf16(BM2, BN, A_MN, B_MN);
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
-      for (int t = cid; t < tiles; t += ncl) {
+      for (int t = cid; t < items; t += ncl) {
         sm100::mbar_wait(&tempty[acc], aph ^ 1);
         sm100::tc_fence_after();
         const uint32_t d = tbase + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int kb0 = kb_begin(t / tiles);
+        for (int kb = kb0; kb < kb_begin(t / tiles + 1); ++kb) {
           sm100::mbar_wait(&full[stage], ph);
           sm100::tc_fence_after();
           const uint32_t sa = sm100::smem_addr(smem + stage * C::STAGE);
@@ -460,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                      : sm100::smem_desc(sa + kk * 32, 16, 1024, sm100::kSwizzle128B);
             const uint64_t bd = B_MN ? sm100::smem_desc(sb + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
                                      : sm100::smem_desc(sb + kk * 32, 16, 1024, sm100::kSwizzle128B);
-            sm100::mma_bf16_ss_pair(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            sm100::mma_bf16_ss_pair(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
           }
           sm100::mma_commit_pair(&empty[stage], 0x3);
           if (++stage == C::STAGES) {
@@ -482,15 +505,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t xph = 0;
     int acc = 0;
     uint32_t aph = 0;
-    for (int t = cid; t < tiles; t += ncl) {
+    for (int t = cid; t < items; t += ncl) {
       int mt, nt;
-      tile_coords(t, num_m, num_n, mt, nt);
+      const int tile = t % tiles, sp = t / tiles;
+      tile_coords(tile, num_m, num_n, mt, nt);
+      int32_t* flag = ep.flags + tile * 16 + static_cast<int>(rank) * 8 + (warp - 4);
+      if (sp > 0 && lane == 0) {  // split sp-1 of this region has landed in C
+        while (ld_acquire(flag) < ep.flag_base + sp) {
+        }
+        fence_proxy_async_global();
+      }
+      __syncwarp();
       sm100::mbar_wait(&tfull[acc], aph);
       sm100::tc_fence_after();
       epilogue_chunks<EPI>(ep, &tmC, &tmX,
                            tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
                            &xbar[warp - 4], xph, mt * BM2 + static_cast<int>(rank) * BM + ew * 32,
-                           nt * BN + half * (BN / 2), BN / 2, N, lane);
+                           nt * BN + half * (BN / 2), BN / 2, N, lane, ep.beta != 0 || sp > 0);
+      if (sp + 1 < splits && lane == 0) {  // publish: this region's reduce-adds are complete
+        sm100::bulk_wait<0>();
+        fence_proxy_async_global();
+        st_release(flag, ep.flag_base + sp + 1);
+      }
       sm100::tc_fence_before();
       sm100::mbar_arrive_cluster(acc == 0 ? te0 : te1);
       if (++acc == 2) {
@@ -641,6 +677,53 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
   ZB_LAUNCH_CHECK();
 }
 
+// Ordered split-K of the W contraction (EPI_F32_ACC, K = T tokens): W's M x N (weight
+// shape) often gives few 256 x 256 tiles for 74 CTA pairs (proj 2304 x 2304: 81 tiles =
+// 2 rounds at 55% occupancy).  Pick the split count S <= 4 (>= 16 k-blocks per split)
+// minimising ceil(S tiles / pairs) / S, smallest S on ties.  The flag counters live in a
+// per-stream device buffer (zeroed once) with a per-stream launch base, so concurrent
+// streams (loopback stages) never share counters.
+struct SplitFlags {
+  int32_t* dev = nullptr;
+  int32_t base = 0;
+};
+static constexpr int kMaxFlagTiles = 4096;
+static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs& ep) {
+  static int disabled = -1;
+  if (disabled < 0) {
+    const char* e = getenv("ZB_GEMM_NO_SPLITK");
+    disabled = (e && e[0] == '1') ? 1 : 0;
+  }
+  ep.splits = 1;
+  if (disabled || tiles > kMaxFlagTiles) return;
+  int best = 1;
+  double best_t = static_cast<double>(ceil_div(tiles, pairs));
+  for (int sk = 2; sk <= 4 && nk / sk >= 16; ++sk) {
+    const double t = static_cast<double>(ceil_div(static_cast<int64_t>(tiles) * sk, pairs)) / sk;
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = sk;
+    }
+  }
+  if (best == 1) return;
+  static std::mutex mu;
+  static std::map<cudaStream_t, SplitFlags> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  SplitFlags& f = bufs[st];
+  if (!f.dev) {
+    ZB_CUDA(cudaMalloc(&f.dev, sizeof(int32_t) * 16 * kMaxFlagTiles));
+    ZB_CUDA(cudaMemset(f.dev, 0, sizeof(int32_t) * 16 * kMaxFlagTiles));
+  }
+  if (f.base > (1 << 30)) {  // counters would overflow: reset (ordered after earlier work on st)
+    ZB_CUDA(cudaMemsetAsync(f.dev, 0, sizeof(int32_t) * 16 * kMaxFlagTiles, st));
+    f.base = 0;
+  }
+  ep.splits = best;
+  ep.flags = f.dev;
+  ep.flag_base = f.base;
+  f.base += best;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   using C = tc::Cfg2<BN>;
@@ -654,10 +737,13 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap tb = B_MN ? make_tmap(g.B, g.N, g.K, g.ldb, 64, 64) : make_tmap(g.B, g.K, g.N, g.ldb, 64, BN / 2);
   const int tiles = static_cast<int>(ceil_div(g.M, 2 * tc::BM) * ceil_div(g.N, BN));
   const int pairs = num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  EpiArgs ep = g.ep;
+  if (EPI == EPI_F32_ACC) split_k_plan(tiles, static_cast<int>(ceil_div(g.K, tc::BK)), pairs, st, ep);
+  const int items = tiles * ep.splits;
+  const int grid = 2 * (items < pairs ? items : pairs);
   CUtensorMap tcm, txm;
   epi_tmaps<EPI>(g, tcm, txm);
-  launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, g.ep, g.M, g.N, g.K);
+  launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, ep, g.M, g.N, g.K);
   ZB_LAUNCH_CHECK();
 }
 

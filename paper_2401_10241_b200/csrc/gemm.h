@@ -34,6 +34,14 @@ struct EpiArgs {
   void* aux;
   int64_t ldaux;
   int32_t beta;
+  // ordered split-K of EPI_F32_ACC (set by gemm(), not by callers): K is cut into `splits`
+  // ranges; split s of a tile reduce-adds into C only after split s-1 of the same tile
+  // (per 32-row epilogue-warp region) has completed, so the f32 sums are formed in one
+  // fixed order (bitwise reproducible).  flags[tile * 16 + region] is a monotone counter:
+  // split s waits for >= flag_base + s and then stores flag_base + s + 1.
+  int32_t splits = 1;
+  int32_t flag_base = 0;
+  int32_t* flags = nullptr;
 };
 
 struct GemmArgs {

@@ -33,6 +33,8 @@ CASES = [
     (512, 640, 256, False, True, 3),      # GeLU backward epilogue (fc2 dgrad)
     (264, 200, 1000, True, True, 4),      # W variant dW += dY^T X, ragged T
     (768, 512, 1024, True, True, 4),
+    (512, 512, 4096, True, True, 4),      # ordered split-K: 4 tiles -> 4 splits of 16 k-blocks
+    (2304, 2304, 6144, True, True, 4),    # 1.5B proj W: 81 tiles for 74 CTA pairs -> 4 splits
     (256, 512, 320, False, False, 5),     # f32 logits
 ]
 
@@ -79,3 +81,22 @@ def test_gemm_parity(case, dtype):
         if epi == 1:
             gg = aux.double().cpu().numpy()
             assert rel(gg, _gelu(ref)) < (1e-5 if dtype == "f32" else 6e-3)
+
+
+def test_split_k_w_is_deterministic():
+    """The ordered split-K of W (gemm.cu split_k_plan) sums in one fixed order:
+    repeated accumulations are bitwise identical (P:196 needs this across schedules)."""
+    import torch
+    from paper_2401_10241_b200 import api
+    M, N, K = 2304, 2304, 6144
+    g = torch.Generator(device="cpu").manual_seed(7)
+    A = torch.randn(K, M, generator=g).bfloat16().cuda()
+    B = torch.randn(K, N, generator=g).bfloat16().cuda()
+    outs = []
+    for _ in range(3):
+        C = torch.zeros(M, N, dtype=torch.float32).cuda()
+        for beta in (0, 1, 1):
+            api.dbg_gemm(A, B, C, M=M, N=N, K=K, a_mn=True, b_mn=True, epi=4, beta=beta)
+        torch.cuda.synchronize()
+        outs.append(C.cpu())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
