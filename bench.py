@@ -16,6 +16,7 @@ bounded sample of the same workload on the host cores.
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -192,7 +193,7 @@ def run_single(args, cfg):
     import torch
     from paper_2401_10241_b200 import api
     from paper_2401_10241_b200._lib import lib
-    import ctypes as C
+    import ctypes as C  # noqa: F811
 
     p = 1
     m = cfg.m
@@ -258,6 +259,7 @@ def run_single(args, cfg):
         kstats[name] = {"ms_total": a.value / args.steps, "tflops": (b.value / (a.value / 1e3) / 1e12) if a.value else 0,
                         "launches_per_step": n.value / args.steps,
                         "share_of_step": (a.value / args.steps) / ms_ev if ms_ev else 0}
+    hbm = hbm_classes(lib, args.steps, ms_ev)
     loss = ctx.loss()
     # ---- per-pass times -> predicted bubbles at p=8 (Table 8 analog on B200)
     step(args.warmup, timing=True)
@@ -298,7 +300,12 @@ def run_single(args, cfg):
             "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside a long step)",
             "timing": f"CUDA events around every launch over a second region of the same {args.steps} steps "
                       f"({ms_ev:.1f} ms/step with the events)",
-            "per_class": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in kstats.items()}}
+            "per_class": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in kstats.items()},
+            "hbm_kernels": hbm}
+    roof["traffic"], roof["traffic_source"] = gemm_traffic()
+    accounted = sum(v["ms_total"] for k, v in kstats.items() if k in ("gemm", "attn_fwd", "attn_bwd")) + \
+        sum(v["ms_total"] for v in hbm["classes"].values())
+    roof["unaccounted_ms_per_step"] = round(ms_ev - accounted, 3)
     flops_token = cfg.L * (72 * cfg.h ** 2 + 12 * cfg.s * cfg.h) + 6 * cfg.h * cfg.V
     mfu = value * flops_token / (peaks.get("bf16_tflops", 1680.3) * 1e12)
     line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
@@ -314,6 +321,40 @@ def run_single(args, cfg):
                                 "sample": f"one {cfg.name} layer F+B+W + head on {cfg.s} tokens, extrapolated",
                                 "detail": info}
     print(json.dumps(line), flush=True)
+
+
+HBM_CLASSES = ((6, "ln_fwd"), (7, "ln_bwd_dx"), (8, "ln_param_grads"), (9, "bias_grads"), (10, "cross_entropy"),
+               (11, "optimizer"), (12, "embed_convert"))
+
+
+def hbm_classes(lib, steps, ms_ev):
+    """Per-class CUDA-event totals of the HBM-bound kernels (ktimer classes 6-12:
+    algorithmic bytes / time) against the measured copy bandwidth."""
+    peaks, src = read_peaks()
+    peak = peaks.get("hbm_gbs")
+    out = {}
+    for cls, name in HBM_CLASSES:
+        a, b, n = C.c_double(), C.c_double(), C.c_int64()
+        lib.zb_dbg_kernel_timing_read(cls, C.byref(a), C.byref(b), C.byref(n))
+        if not n.value:
+            continue
+        gbs = b.value / (a.value / 1e3) / 1e9 if a.value else 0.0
+        out[name] = {"ms_total": round(a.value / steps, 4), "gbs": round(gbs, 1),
+                     "frac": round(gbs / peak, 4) if peak else None,
+                     "launches_per_step": n.value / steps, "share_of_step": round((a.value / steps) / ms_ev, 4)}
+    return {"unit": "GB/s (algorithmic bytes / event time)", "peak": peak, "peak_source": f"{src} hbm_gbs",
+            "classes": out}
+
+
+def gemm_traffic():
+    """DRAM bytes per GEMM launch from the committed ncu capture (profiles/), if any."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "gemm_dram_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["dram_bytes_per_launch"], d["source"]
+    except (OSError, KeyError, ValueError):
+        return None, None
 
 
 def predicted_bubbles(cfg, t_pass):

@@ -36,11 +36,30 @@ zb_status_t zb_dbg_attention_bwd(int32_t dtype, int32_t b, int32_t s, int32_t a,
                                  const void* o, const void* dout, const float* lse, void* dqkv, float* delta,
                                  void* stream);
 
+/* The HBM-bound row / column kernels of the stage passes (ops.h), for the
+ * parity tests (all device pointers, row-major, f32 statistics):
+ *  layernorm_fwd: y[rows,h] = g * (x - mean) * rstd + b; mean, rstd [rows] written.
+ *  layernorm_bwd: dx = resid + rstd * (gh - mean(gh) - xhat * mean(gh*xhat)),
+ *      gh = dy * g (dy f32; resid, dx32 f32 and nullable; dx in the dtype, may alias x);
+ *      gg (+)= colsum(dy * xhat), gb (+)= colsum(dy) (beta != 0: accumulate).
+ *  bias_grad: out[n] (+)= colsum(y[rows, n] with leading dimension ldy). */
+zb_status_t zb_dbg_layernorm_fwd(int32_t dtype, const void* x, const float* g, const float* b, void* y, float* mean,
+                                 float* rstd, int32_t rows, int32_t h, float eps, void* stream);
+zb_status_t zb_dbg_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float* mean, const float* rstd,
+                                 const float* g, const float* resid, float* dx32, void* dx, float* gg, float* gb,
+                                 int32_t beta, int32_t rows, int32_t h, void* stream);
+zb_status_t zb_dbg_bias_grad(int32_t dtype, const void* y, int64_t ldy, float* out, int32_t rows, int32_t n,
+                             int32_t beta, void* stream);
+
 /* Kernel-class timing used by bench.py for the live roofline numbers: when
- * enabled, every GEMM / attention launch is bracketed by CUDA events on its
- * stream and its algorithmic FLOPs are recorded.  Classes: 0 all GEMMs,
- * 1 attention forward, 2 attention backward, 3 F GEMMs (X W^T), 4 B GEMMs
- * (dY W), 5 W GEMMs (dY^T X).  read() synchronises the pending events. */
+ * enabled, every GEMM / attention / HBM-bound op launch is bracketed by CUDA
+ * events on its stream and its algorithmic work is recorded (FLOPs for
+ * classes 0-5, BYTES for 6-12).  Classes: 0 all GEMMs, 1 attention forward,
+ * 2 attention backward, 3 F GEMMs (X W^T), 4 B GEMMs (dY W), 5 W GEMMs
+ * (dY^T X), 6 LayerNorm forward, 7 LayerNorm backward dx, 8 LayerNorm
+ * gamma/beta grads, 9 bias grads (column sums), 10 cross-entropy, 11 grad
+ * norm + AdamW, 12 embedding / conversions.  read() synchronises the
+ * pending events. */
 zb_status_t zb_dbg_kernel_timing(int32_t enable, int32_t reset);
 zb_status_t zb_dbg_kernel_timing_read(int32_t cls, double* total_ms, double* total_flops, int64_t* launches);
 

@@ -88,6 +88,9 @@ _SIGS = {
                      _I64, _I64, _I64, _I32, C.POINTER(zb_sim_t)], _I32),
     "zb_dbg_gemm": ([_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _P, _P, _I64, _I32, _P],
                     _I32),
+    "zb_dbg_layernorm_fwd": ([_I32, _P, _P, _P, _P, _P, _P, _I32, _I32, C.c_float, _P], _I32),
+    "zb_dbg_layernorm_bwd": ([_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P], _I32),
+    "zb_dbg_bias_grad": ([_I32, _P, _I64, _P, _I32, _I32, _I32, _P], _I32),
     "zb_dbg_attention_fwd": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P], _I32),
     "zb_dbg_attention_bwd": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
     "zb_dbg_stage_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, _I32, _I32, _I32, C.POINTER(_I32), _I32,

@@ -298,6 +298,24 @@ def dbg_gemm(A, B, C_out, *, M, N, K, a_mn=False, b_mn=False, epi=0, bias=None, 
                           _ptr(bias), _ptr(aux), ldaux, beta, _stream(stream)))
 
 
+def dbg_layernorm_fwd(x, g, b, y, mean, rstd, *, rows, h, eps=1e-5, stream=None):
+    dtype = ZB_DTYPE_F32 if x.element_size() == 4 else ZB_DTYPE_BF16
+    check(lib.zb_dbg_layernorm_fwd(dtype, _ptr(x), _ptr(g), _ptr(b), _ptr(y), _ptr(mean), _ptr(rstd), rows, h,
+                                   float(eps), _stream(stream)))
+
+
+def dbg_layernorm_bwd(dy, x, mean, rstd, g, dx, gg, gb, *, rows, h, resid=None, dx32=None, beta=0, stream=None):
+    dtype = ZB_DTYPE_F32 if x.element_size() == 4 else ZB_DTYPE_BF16
+    check(lib.zb_dbg_layernorm_bwd(dtype, _ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(g), _ptr(resid), _ptr(dx32),
+                                   _ptr(dx), _ptr(gg), _ptr(gb), beta, rows, h, _stream(stream)))
+
+
+def dbg_bias_grad(y, out, *, rows, n, ldy=None, beta=0, stream=None):
+    dtype = ZB_DTYPE_F32 if y.element_size() == 4 else ZB_DTYPE_BF16
+    check(lib.zb_dbg_bias_grad(dtype, _ptr(y), ldy if ldy is not None else y.shape[-1], _ptr(out), rows, n, beta,
+                               _stream(stream)))
+
+
 def dbg_attention_fwd(qkv, o, lse, *, b, s, a, d, stream=None):
     dtype = ZB_DTYPE_F32 if qkv.element_size() == 4 else ZB_DTYPE_BF16
     check(lib.zb_dbg_attention_fwd(dtype, b, s, a, d, _ptr(qkv), _ptr(o), _ptr(lse), _stream(stream)))

@@ -3,6 +3,7 @@
 #include "attention.h"
 #include "gemm.h"
 #include "ktimer.h"
+#include "ops.h"
 #include "zb_debug.h"
 
 using namespace zb;
@@ -87,6 +88,45 @@ extern "C" zb_status_t zb_dbg_kernel_timing_read(int32_t cls, double* total_ms, 
     } else {
       ktimer::read(cls, total_ms, total_flops, launches);
     }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_dbg_layernorm_fwd(int32_t dtype, const void* x, const float* g, const float* b, void* y,
+                                            float* mean, float* rstd, int32_t rows, int32_t h, float eps,
+                                            void* stream) {
+  ZB_TRY {
+    if ((dtype != ZB_DTYPE_BF16 && dtype != ZB_DTYPE_F32) || !x || !g || !b || !y || !mean || !rstd || rows < 0 ||
+        h <= 0)
+      return set_error(ZB_EINVAL, "zb_dbg_layernorm_fwd: bad arguments");
+    layernorm_fwd(static_cast<DType>(dtype), x, g, b, y, mean, rstd, rows, h, eps, static_cast<cudaStream_t>(stream));
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_dbg_layernorm_bwd(int32_t dtype, const float* dy, const void* x, const float* mean,
+                                            const float* rstd, const float* g, const float* resid, float* dx32,
+                                            void* dx, float* gg, float* gb, int32_t beta, int32_t rows, int32_t h,
+                                            void* stream) {
+  ZB_TRY {
+    if ((dtype != ZB_DTYPE_BF16 && dtype != ZB_DTYPE_F32) || !dy || !x || !mean || !rstd || !g || !dx || !gg ||
+        !gb || rows < 0 || h <= 0)
+      return set_error(ZB_EINVAL, "zb_dbg_layernorm_bwd: bad arguments");
+    layernorm_bwd(static_cast<DType>(dtype), dy, x, mean, rstd, g, resid, dx32, dx, gg, gb, beta, rows, h,
+                  static_cast<cudaStream_t>(stream));
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_dbg_bias_grad(int32_t dtype, const void* y, int64_t ldy, float* out, int32_t rows,
+                                        int32_t n, int32_t beta, void* stream) {
+  ZB_TRY {
+    if ((dtype != ZB_DTYPE_BF16 && dtype != ZB_DTYPE_F32) || !y || !out || rows < 0 || n <= 0 || ldy < n)
+      return set_error(ZB_EINVAL, "zb_dbg_bias_grad: bad arguments");
+    bias_grad(static_cast<DType>(dtype), y, ldy, out, rows, n, beta, static_cast<cudaStream_t>(stream));
     return ZB_OK;
   }
   ZB_CATCH

@@ -1,5 +1,5 @@
 // Optional per-kernel-class CUDA-event timing (zb_dbg_kernel_timing): when on,
-// every GEMM / attention launch is bracketed by events on its own stream and
+// every GEMM / attention / HBM-bound op launch is bracketed by events on its own stream and
 // its algorithmic FLOPs are recorded; bench.py reads the totals after the
 // timed region to report the dominant kernel's achieved TFLOP/s live.
 #pragma once
@@ -14,7 +14,12 @@ int64_t launch_count(bool reset);
 
 namespace ktimer {
 
-enum Class : int { GEMM = 0, ATTN_FWD = 1, ATTN_BWD = 2, GEMM_F = 3, GEMM_B = 4, GEMM_W = 5, N_CLASSES = 6 };
+// GEMM / attention classes carry algorithmic FLOPs; the HBM-bound classes (LN_*,
+// BIAS_GRAD, CE, OPT, MISC) carry algorithmic BYTES in the same field.
+enum Class : int {
+  GEMM = 0, ATTN_FWD = 1, ATTN_BWD = 2, GEMM_F = 3, GEMM_B = 4, GEMM_W = 5,
+  LN_FWD = 6, LN_BWD = 7, LN_PARAM = 8, BIAS_GRAD = 9, CE = 10, OPT = 11, MISC = 12, N_CLASSES = 13
+};
 
 bool enabled();
 void set_enabled(bool on);

@@ -4,8 +4,11 @@
 #include <math.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <type_traits>
 
+#include "ktimer.h"
 #include "ops.h"
 #include "zb.h"
 
@@ -146,6 +149,83 @@ __global__ void __launch_bounds__(128) k_ln_fwd_warp(const T* __restrict__ x, co
   }
 }
 
+// bf16, persistent warp-per-row with a one-row prefetch: each warp walks rows
+// w, w + W, ... (W = all warps of the grid) and issues the loads of its next row before
+// reducing / normalising / storing the current one, so every warp keeps a row of loads
+// in flight for the whole kernel (the one-row-per-warp kernel was latency-bound:
+// load -> reduce -> store with nothing outstanding in between, 33% of HBM bandwidth).
+// Rows are held packed (16 B per 8 columns); gamma / beta come through L1.
+template <int VPL>
+__global__ void __launch_bounds__(128, 4) k_ln_fwd_rows(const bf16* __restrict__ x, const float* __restrict__ g,
+                                                    const float* __restrict__ b, bf16* __restrict__ y,
+                                                    float* __restrict__ mean, float* __restrict__ rstd, int rows, int h,
+                                                    float eps) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * 4;
+  int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  const int nv = h / 8;
+  uint4 cur[VPL], nxt[VPL];
+  auto load = [&](int64_t r, uint4* dst) {
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int vi = lane + 32 * k;
+      dst[k] = vi < nv ? __ldcs(reinterpret_cast<const uint4*>(x + r * h + vi * 8)) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  if (row < rows) load(row, cur);
+  for (; row < rows; row += stride) {
+    if (row + stride < rows) load(row + stride, nxt);
+    float sum = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&cur[k]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(hv[i]);
+        sum += f.x + f.y;
+      }
+    }
+    const float mu = warp_sum(sum) / h;
+    float sq = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      if (lane + 32 * k < nv) {
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&cur[k]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(hv[i]);
+          sq += (f.x - mu) * (f.x - mu) + (f.y - mu) * (f.y - mu);
+        }
+      }
+    }
+    const float rs = rsqrtf(warp_sum(sq) / h + eps);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int vi = lane + 32 * k;
+      if (vi < nv) {
+        float gg[8], bb[8], o[8];
+        Vec8<float>::load(g + vi * 8, gg);
+        Vec8<float>::load(b + vi * 8, bb);
+        const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&cur[k]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(hv[i]);
+          o[2 * i] = (f.x - mu) * rs * gg[2 * i] + bb[2 * i];
+          o[2 * i + 1] = (f.y - mu) * rs * gg[2 * i + 1] + bb[2 * i + 1];
+        }
+        Vec8<bf16>::store(y + row * h + vi * 8, o);
+      }
+    }
+    if (lane == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) cur[k] = nxt[k];
+  }
+}
+
 // ---------------------------------------------------------------- LayerNorm backward
 // dx only, one CTA per row (full parallelism over rows).  The residual-gradient
 // stream stays f32 (resid and dx32, may be null); dx (activation dtype, may
@@ -201,140 +281,126 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_bwd_dx(const float* __restric
   }
 }
 
-// Column reductions in one pass: a CTA owns VPC 8-column groups over ALL rows
-// (kColThreads / VPC row lanes, each summing rows lane, lane + RL, ... in order),
-// then a fixed binary tree over the row lanes in shared memory. Deterministic
-// (fixed partition and order), no partial buffers, one launch. VPC is chosen so
-// the grid covers the SMs (colred_vpc).
-constexpr int kColThreads = 512;
+// Coalesced two-phase column reductions (bias grads, LayerNorm gamma / beta grads).
+// CTA (ct, rb) owns a 256-column tile ct (lane l of every warp: columns 8l..8l+7, so a
+// warp reads 512 contiguous bytes of a bf16 row) over row block rb; its 8 warps take rows
+// w, w+8, ... with 4 rows of loads in flight.  Warp partials meet in shared memory (fixed
+// order), the CTA's partial row goes to scratch, and the LAST CTA of the column tile
+// (atomic ticket) sums the RB partial rows in row-block order and applies beta.  The
+// result is deterministic (fixed partition, fixed summation order) and needs one launch.
+// MODE 0: out0 (+)= sum_r y[r];  MODE 1: out0 (+)= sum_r dy[r] * xhat[r], out1 (+)= sum_r dy[r].
+constexpr int kCR_THREADS = 256, kCR_COLS = 256;
 
-template <int VPC, int NACC>
-__device__ __forceinline__ void colred_tree(float (&acc)[NACC][8], float* sm) {
-  constexpr int RL = kColThreads / VPC, W = VPC * 8 + 4;  // +4: spread banks
-  const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
+template <int MODE, typename T>
+__global__ void __launch_bounds__(kCR_THREADS) k_colred2(const T* __restrict__ y, int64_t ldy,
+                                                         const float* __restrict__ dy, const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, float* __restrict__ out0,
+                                                         float* __restrict__ out1, float* __restrict__ part,
+                                                         int32_t* __restrict__ tickets, int rows, int n, int rpb,
+                                                         int beta) {
+  pdl_wait();
+  constexpr int NACC = MODE == 0 ? 1 : 2;
+  constexpr int U = MODE == 0 ? 8 : 4;  // rows of loads in flight per thread (128 / 192 B)
+  __shared__ float sm[NACC][8][kCR_COLS];
+  __shared__ int s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ct = blockIdx.x, rb = blockIdx.y, RB = gridDim.y;
+  const int col = ct * kCR_COLS + lane * 8;
+  const bool valid = col < n;
+  const int r0 = rb * rpb, r1 = min(rows, r0 + rpb);
+  float acc[NACC][8];
 #pragma unroll
   for (int q = 0; q < NACC; ++q)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sm[(q * RL + rl) * W + vec * 8 + i] = acc[q][i];
+    for (int i = 0; i < 8; ++i) acc[q][i] = 0.f;
+  if (valid) {
+    for (int r = r0 + warp; r < r1; r += 8 * U) {  // U rows per batch, tail rows masked (loads stay batched)
+      float v[U][8], d[U][8], mu[U], rs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t rr = r + 8 * u;
+        if (rr < r1) {
+          Vec8<T>::load(y + rr * ldy + col, v[u]);
+          if (MODE == 1) {
+            Vec8<float>::load(dy + rr * ldy + col, d[u]);
+            mu[u] = mean[rr];
+            rs[u] = rstd[rr];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[u][i] = d[u][i] = 0.f;
+          mu[u] = rs[u] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (MODE == 0) {
+            acc[0][i] += v[u][i];
+          } else {
+            acc[0][i] += d[u][i] * ((v[u][i] - mu[u]) * rs[u]);
+            acc[1][i] += d[u][i];
+          }
+        }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NACC; ++q)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sm[q][warp][lane * 8 + i] = acc[q][i];
   __syncthreads();
+  const int c = ct * kCR_COLS + threadIdx.x;  // thread t writes column t of the CTA's partial row
+  if (c < n) {
 #pragma unroll
-  for (int stride = RL / 2; stride > 0; stride >>= 1) {
-    if (rl < stride) {
+    for (int q = 0; q < NACC; ++q) {
+      float t = 0.f;
 #pragma unroll
-      for (int q = 0; q < NACC; ++q)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          acc[q][i] += sm[(q * RL + rl + stride) * W + vec * 8 + i];
-          sm[(q * RL + rl) * W + vec * 8 + i] = acc[q][i];
-        }
+      for (int w = 0; w < 8; ++w) t += sm[q][w][threadIdx.x];
+      part[(static_cast<int64_t>(q) * RB + rb) * n + c] = t;
     }
-    __syncthreads();
   }
-}
-
-// gamma / beta: gg (+)= sum_r dy * xhat, gb (+)= sum_r dy
-template <typename T, int VPC>
-__global__ void __launch_bounds__(kColThreads) k_ln_param_grads(const float* __restrict__ dy, const T* __restrict__ x,
-                                                                const float* __restrict__ mean,
-                                                                const float* __restrict__ rstd, float* __restrict__ gg,
-                                                                float* __restrict__ gb, int rows, int h, int beta) {
-  pdl_wait();
-  constexpr int RL = kColThreads / VPC;
-  extern __shared__ float colsm[];
-  const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
-  const int col = (blockIdx.x * VPC + vec) * 8;
-  const bool valid = col < h;
-  float acc[2][8];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&tickets[ct], 1) == RB - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last CTA of the tile: warp w sums partial rows w, w+8, ... of lane's 8 columns (all its
+  // loads in flight at once), then the 8 warp sums meet in shared memory in warp order
+  float fin[NACC][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc[0][i] = acc[1][i] = 0.f;
+  for (int q = 0; q < NACC; ++q)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) fin[q][i] = 0.f;
   if (valid) {
-    int r = rl;
-    for (; r + 3 * RL < rows; r += 4 * RL) {  // four rows of loads in flight per thread
-      float d[4][8], xv[4][8], mu[4], rs[4];
+#pragma unroll 4
+    for (int bb = warp; bb < RB; bb += 8)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t rr = r + u * RL;
-        Vec8<float>::load(dy + rr * h + col, d[u]);
-        Vec8<T>::load(x + rr * h + col, xv[u]);
-        mu[u] = mean[rr];
-        rs[u] = rstd[rr];
+      for (int q = 0; q < NACC; ++q) {
+        const float* src = part + (static_cast<int64_t>(q) * RB + bb) * n + col;
+        const float4 lo = __ldcg(reinterpret_cast<const float4*>(src));
+        const float4 hi = __ldcg(reinterpret_cast<const float4*>(src + 4));
+        fin[q][0] += lo.x; fin[q][1] += lo.y; fin[q][2] += lo.z; fin[q][3] += lo.w;
+        fin[q][4] += hi.x; fin[q][5] += hi.y; fin[q][6] += hi.z; fin[q][7] += hi.w;
       }
+  }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+  for (int q = 0; q < NACC; ++q)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          acc[0][i] += d[u][i] * ((xv[u][i] - mu[u]) * rs[u]);
-          acc[1][i] += d[u][i];
-        }
-    }
-    for (; r < rows; r += RL) {
-      float d[8], xv[8];
-      Vec8<float>::load(dy + static_cast<int64_t>(r) * h + col, d);
-      Vec8<T>::load(x + static_cast<int64_t>(r) * h + col, xv);
-      const float mu = mean[r], rs = rstd[r];
+    for (int i = 0; i < 8; ++i) sm[q][warp][lane * 8 + i] = fin[q][i];
+  __syncthreads();
+  if (c < n) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        acc[0][i] += d[i] * ((xv[i] - mu) * rs);
-        acc[1][i] += d[i];
-      }
+    for (int q = 0; q < NACC; ++q) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += sm[q][w][threadIdx.x];
+      float* o = q == 0 ? out0 : out1;
+      o[c] = beta ? o[c] + t : t;
     }
   }
-  colred_tree<VPC, 2>(acc, colsm);
-  if (rl == 0 && valid) {
-    if (beta) {
-      float o[8];
-      Vec8<float>::load(gg + col, o);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[0][i] += o[i];
-      Vec8<float>::load(gb + col, o);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[1][i] += o[i];
-    }
-    Vec8<float>::store(gg + col, acc[0]);
-    Vec8<float>::store(gb + col, acc[1]);
-  }
-}
-
-template <typename T, int VPC>
-__global__ void __launch_bounds__(kColThreads) k_colsum(const T* __restrict__ y, int64_t ldy, float* __restrict__ out,
-                                                        int rows, int n, int beta) {
-  pdl_wait();
-  constexpr int RL = kColThreads / VPC;
-  extern __shared__ float colsm[];
-  const int vec = threadIdx.x % VPC, rl = threadIdx.x / VPC;
-  const int col = (blockIdx.x * VPC + vec) * 8;
-  const bool valid = col < n;
-  float acc[1][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[0][i] = 0.f;
-  if (valid) {
-    int r = rl;
-    for (; r + 7 * RL < rows; r += 8 * RL) {
-      float v[8][8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) Vec8<T>::load(y + static_cast<int64_t>(r + u * RL) * ldy + col, v[u]);
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[0][i] += v[u][i];
-    }
-    for (; r < rows; r += RL) {
-      float v[8];
-      Vec8<T>::load(y + static_cast<int64_t>(r) * ldy + col, v);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[0][i] += v[i];
-    }
-  }
-  colred_tree<VPC, 1>(acc, colsm);
-  if (rl == 0 && valid) {
-    if (beta) {
-      float o[8];
-      Vec8<float>::load(out + col, o);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[0][i] += o[i];
-    }
-    Vec8<float>::store(out + col, acc[0]);
-  }
+  if (threadIdx.x == 0) tickets[ct] = 0;  // ready for the next launch on this stream
 }
 
 // ---------------------------------------------------------------- embedding
@@ -703,9 +769,50 @@ void ln_dispatch(int h, F&& f) {
 }  // namespace
 
 // ---------------------------------------------------------------- host wrappers
+// Per-stream scratch of the two-phase column reductions (partial rows + column-tile
+// tickets, zeroed once; the last CTA of a tile re-zeroes its ticket), so concurrent
+// streams never share tickets.
+struct ColredScratch {
+  float* part = nullptr;
+  int32_t* tickets = nullptr;
+};
+static constexpr int64_t kColredPartFloats = 4 << 20;  // 16 MB
+static constexpr int kColredTickets = 4096;
+static ColredScratch colred_scratch(cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, ColredScratch> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  ColredScratch& c = bufs[st];
+  if (!c.part) {
+    ZB_CUDA(cudaMalloc(&c.part, sizeof(float) * kColredPartFloats));
+    ZB_CUDA(cudaMalloc(&c.tickets, sizeof(int32_t) * kColredTickets));
+    ZB_CUDA(cudaMemset(c.tickets, 0, sizeof(int32_t) * kColredTickets));
+  }
+  return c;
+}
+
+// grid of the two-phase reduction: ~2 CTAs per SM (warps keep 8 / 4 rows of loads in
+// flight), a multiple of 64 rows per CTA
+static void colred2_grid(int rows, int n, int nacc, int& ntiles, int& rb, int& rpb) {
+  ntiles = (n + kCR_COLS - 1) / kCR_COLS;
+  rb = std::max(1, std::min((2 * 148 + ntiles - 1) / ntiles, (rows + 63) / 64));
+  while (static_cast<int64_t>(nacc) * rb * n > kColredPartFloats && rb > 1) rb >>= 1;
+  if (static_cast<int64_t>(nacc) * rb * n > kColredPartFloats || ntiles > kColredTickets)
+    throw CudaError("column reduction: n too large for the scratch");
+  rpb = (rows + rb - 1) / rb;
+  rpb = (rpb + 63) / 64 * 64;  // whole 8-warp x 8-row batches per CTA
+  rb = (rows + rpb - 1) / rpb;
+}
+
 template <int VPL>
 static void ln_fwd_warp(DType dt, const void* x, const float* g, const float* b, void* y, float* mean, float* rstd,
                         int rows, int h, float eps, cudaStream_t st) {
+  if (dt == DT_BF16) {  // persistent: 4 CTAs of 4 warps per SM (or fewer for small inputs)
+    const int blocks = std::min((rows + 3) / 4, 4 * 148);
+    launch(PDL_OPS, k_ln_fwd_rows<VPL>, blocks, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y),
+           mean, rstd, rows, h, eps);
+    return;
+  }
   const int blocks = (rows + 3) / 4;
   if (dt == DT_BF16)
     launch(PDL_OPS, k_ln_fwd_warp<bf16, VPL>, blocks, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean,
@@ -719,6 +826,7 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
                    int rows, int h, float eps, cudaStream_t st) {
   if (rows <= 0) return;
   if (h % 8) throw CudaError("layernorm: h must be a multiple of 8");
+  const int tk__ = ktimer::start(ktimer::LN_FWD, static_cast<double>(rows) * h * 2 * (dt == DT_BF16 ? 2.0 : 4.0) + 8.0 * h + 8.0 * rows, st);
   const int vpl = (h / 8 + 31) / 32;
   if (vpl <= 2) {
     ln_fwd_warp<2>(dt, x, g, b, y, mean, rstd, rows, h, eps, st);
@@ -740,58 +848,33 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
     });
   }
   ZB_LAUNCH_CHECK();
-}
-
-// 8-column groups per CTA: the widest of 1, 2, 4, 8 that still gives >= ~1 CTA per SM
-static int colred_vpc(int n) {
-  const int groups = n / 8;
-  int vpc = 8;
-  while (vpc > 1 && groups / vpc < 140) vpc >>= 1;
-  return vpc;
-}
-
-template <int VPC>
-static size_t colred_smem(int nacc) {
-  return static_cast<size_t>(nacc) * (kColThreads / VPC) * (VPC * 8 + 4) * sizeof(float);
-}
-
-template <typename F>
-static void colred_dispatch(int vpc, F&& f) {
-  switch (vpc) {
-    case 1: return f(std::integral_constant<int, 1>{});
-    case 2: return f(std::integral_constant<int, 2>{});
-    case 4: return f(std::integral_constant<int, 4>{});
-    default: return f(std::integral_constant<int, 8>{});
-  }
-}
-
-template <typename K>
-static void allow_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) ZB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  ktimer::stop(tk__, st);
 }
 
 void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
                    const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta, int rows, int h,
                    cudaStream_t st) {
   if (rows <= 0) return;
+  const double esz = dt == DT_BF16 ? 2.0 : 4.0, elems = static_cast<double>(rows) * h;
   // 1) gamma / beta grads (reads x before step 2 may overwrite it in place)
-  const int vpc = colred_vpc(h);
-  colred_dispatch(vpc, [&](auto V) {
-    constexpr int VPC = decltype(V)::value;
-    const int grid = (h / 8 + VPC - 1) / VPC;
-    const size_t sm = colred_smem<VPC>(2);
-    if (dt == DT_BF16) {
-      allow_smem(k_ln_param_grads<bf16, VPC>, sm);
-      launch(PDL_OPS, k_ln_param_grads<bf16, VPC>, grid, kColThreads, sm, st, dy, static_cast<const bf16*>(x), mean, rstd, gg, gb,
-                                                                 rows, h, beta);
-    } else {
-      allow_smem(k_ln_param_grads<float, VPC>, sm);
-      launch(PDL_OPS, k_ln_param_grads<float, VPC>, grid, kColThreads, sm, st, dy, static_cast<const float*>(x), mean, rstd, gg,
-                                                                  gb, rows, h, beta);
-    }
-  });
+  int tk = ktimer::start(ktimer::LN_PARAM, elems * (4.0 + esz) + 8.0 * rows + 8.0 * h, st);
+  {
+    int ntiles, rb, rpb;
+    colred2_grid(rows, h, 2, ntiles, rb, rpb);
+    const ColredScratch sc = colred_scratch(st);
+    const dim3 grid(ntiles, rb);
+    if (dt == DT_BF16)
+      launch(PDL_OPS, k_colred2<1, bf16>, grid, kCR_THREADS, 0, st, static_cast<const bf16*>(x), static_cast<int64_t>(h),
+             dy, mean, rstd, gg, gb, sc.part, sc.tickets, rows, h, rpb, beta);
+    else
+      launch(PDL_OPS, k_colred2<1, float>, grid, kCR_THREADS, 0, st, static_cast<const float*>(x), static_cast<int64_t>(h),
+             dy, mean, rstd, gg, gb, sc.part, sc.tickets, rows, h, rpb, beta);
+  }
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk, st);
   // 2) dx, one CTA per row (dy arrives in f32: the dLN GEMM epilogue keeps full precision)
+  tk = ktimer::start(ktimer::LN_BWD,
+                     elems * (4.0 + 2 * esz + (resid ? 4.0 : 0.0) + (dx32 ? 4.0 : 0.0)) + 8.0 * rows + 4.0 * h, st);
   ln_dispatch<0>(h, [&](auto V) {
     constexpr int VPT = decltype(V)::value;
     if (dt == DT_BF16)
@@ -802,40 +885,44 @@ void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, 
                                                            dx32, static_cast<float*>(dx), h);
   });
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk, st);
 }
 
 void bias_grad(DType dt, const void* y, int64_t ldy, float* out, int rows, int n, int beta, cudaStream_t st) {
   if (rows <= 0 || n <= 0) return;
-  colred_dispatch(colred_vpc(n), [&](auto V) {
-    constexpr int VPC = decltype(V)::value;
-    const int grid = (n / 8 + VPC - 1) / VPC;
-    const size_t sm = colred_smem<VPC>(1);
-    if (dt == DT_BF16) {
-      allow_smem(k_colsum<bf16, VPC>, sm);
-      launch(PDL_OPS, k_colsum<bf16, VPC>, grid, kColThreads, sm, st, static_cast<const bf16*>(y), ldy, out, rows, n, beta);
-    } else {
-      allow_smem(k_colsum<float, VPC>, sm);
-      launch(PDL_OPS, k_colsum<float, VPC>, grid, kColThreads, sm, st, static_cast<const float*>(y), ldy, out, rows, n, beta);
-    }
-  });
+  const int tk__ = ktimer::start(ktimer::BIAS_GRAD, static_cast<double>(rows) * n * (dt == DT_BF16 ? 2.0 : 4.0) + 4.0 * n, st);
+  int ntiles, rb, rpb;
+  colred2_grid(rows, n, 1, ntiles, rb, rpb);
+  const ColredScratch sc = colred_scratch(st);
+  const dim3 grid(ntiles, rb);
+  if (dt == DT_BF16)
+    launch(PDL_OPS, k_colred2<0, bf16>, grid, kCR_THREADS, 0, st, static_cast<const bf16*>(y), ldy, nullptr, nullptr,
+           nullptr, out, nullptr, sc.part, sc.tickets, rows, n, rpb, beta);
+  else
+    launch(PDL_OPS, k_colred2<0, float>, grid, kCR_THREADS, 0, st, static_cast<const float*>(y), ldy, nullptr, nullptr,
+           nullptr, out, nullptr, sc.part, sc.tickets, rows, n, rpb, beta);
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk__, st);
 }
 
 void embed_fwd(DType dt, const int32_t* tok, const float* wte, const float* wpe, void* x0, int rows, int s, int h,
                cudaStream_t st) {
   if (rows <= 0) return;
+  const int tk__ = ktimer::start(ktimer::MISC, static_cast<double>(rows) * h * (8.0 + (dt == DT_BF16 ? 2.0 : 4.0)) + 4.0 * rows, st);
   const int thr = h / 8 < 256 ? ((h / 8 + 31) / 32) * 32 : 256;
   if (dt == DT_BF16)
     launch(PDL_OPS, k_embed_fwd<bf16>, rows, thr, 0, st, tok, wte, wpe, static_cast<bf16*>(x0), s, h);
   else
     launch(PDL_OPS, k_embed_fwd<float>, rows, thr, 0, st, tok, wte, wpe, static_cast<float*>(x0), s, h);
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk__, st);
 }
 
 void embed_bwd(DType dt, const int32_t* tok, const void* dx0, float* dwte, float* dwpe, uint32_t* keys, int rows,
                int s, int h, cudaStream_t st) {
   if (rows <= 0) return;
   if (rows > 8192) throw CudaError("embed_bwd: at most 8192 tokens per microbatch");
+  const int tk__ = ktimer::start(ktimer::MISC, static_cast<double>(rows) * h * (2 * (dt == DT_BF16 ? 2.0 : 4.0) + 8.0) + 8.0 * rows, st);
   launch(PDL_OPS, k_sort_tokens, 1, 1024, 0, st, tok, keys, rows);
   ZB_LAUNCH_CHECK();
   const int blocks = (rows * 32 + 255) / 256;
@@ -848,12 +935,14 @@ void embed_bwd(DType dt, const int32_t* tok, const void* dx0, float* dwte, float
     launch(PDL_OPS, k_embed_bwd_wpe<float>, s < rows ? s : rows, thr, 0, st, static_cast<const float*>(dx0), dwpe, rows, s, h);
   }
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk__, st);
 }
 
 void cross_entropy(DType dt, const float* logits, const int32_t* labels, void* dlogits, float* loss_rows,
                    double* loss_acc, int rows, int V, float inv_scale, cudaStream_t st) {
   if (rows <= 0) return;
   if (V % 8) throw CudaError("cross_entropy: V must be a multiple of 8");
+  const int tk__ = ktimer::start(ktimer::CE, static_cast<double>(rows) * V * (4.0 + (dt == DT_BF16 ? 2.0 : 4.0)), st);
   if (dt == DT_BF16)
     launch(PDL_OPS, k_ce<bf16>, rows, 1024, 0, st, logits, labels, static_cast<bf16*>(dlogits), loss_rows, V, inv_scale);
   else
@@ -861,6 +950,7 @@ void cross_entropy(DType dt, const float* logits, const int32_t* labels, void* d
   ZB_LAUNCH_CHECK();
   launch(PDL_OPS, k_loss_reduce, 1, 1024, 0, st, loss_rows, loss_acc, rows, inv_scale);
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk__, st);
 }
 
 void convert_rows(DType dt, const float* src, void* dst, int64_t n, cudaStream_t st) {
@@ -869,17 +959,21 @@ void convert_rows(DType dt, const float* src, void* dst, int64_t n, cudaStream_t
 
 void convert_f32(DType dt, const float* src, void* dst, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
+  const int tk__ = ktimer::start(ktimer::MISC, static_cast<double>(n) * (4.0 + (dt == DT_BF16 ? 2.0 : 4.0)), st);
   const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
   if (dt == DT_BF16) launch(PDL_OPS, k_convert<bf16>, blocks, 256, 0, st, src, static_cast<bf16*>(dst), n);
   else launch(PDL_OPS, k_convert<float>, blocks, 256, 0, st, src, static_cast<float*>(dst), n);
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk__, st);
 }
 
 void grad_norm(const float* g, int64_t n, double* part, int32_t* nf_part, PvState* pst, cudaStream_t st) {
+  const int tk = ktimer::start(ktimer::OPT, 4.0 * static_cast<double>(n), st);
   launch(PDL_OPS, k_sumsq, kNormBlocks, 512, 0, st, g, n, part, nf_part);
   ZB_LAUNCH_CHECK();
   launch(PDL_OPS, k_sumsq_final, 1, 32, 0, st, part, nf_part, kNormBlocks, pst);
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk, st);
 }
 
 void pv_combine(PvState* pst, cudaStream_t st) {
@@ -902,8 +996,11 @@ void adamw_apply(float* theta, float* m, float* v, const float* g, bf16* shadow,
                  int64_t n_shadow, float lr, float b1, float b2, float eps, float wd, const PvState* pst,
                  cudaStream_t st) {
   const int blocks = static_cast<int>(std::min<int64_t>((n + 511) / 512, 148 * 8));
+  // theta, m, v, g read + theta, m, v written (f32) + the bf16 shadow (algorithmic, predicated-off work included)
+  const int tk = ktimer::start(ktimer::OPT, 28.0 * static_cast<double>(n) + 2.0 * static_cast<double>(n_shadow), st);
   launch(PDL_OPS, k_adamw, blocks, 512, 0, st, theta, m, v, g, shadow, n, n_wd, n_shadow, lr, b1, b2, eps, wd, pst);
   ZB_LAUNCH_CHECK();
+  ktimer::stop(tk, st);
 }
 
 }  // namespace zb
