@@ -120,6 +120,10 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
   constexpr int CC = 128 / static_cast<int>(sizeof(TO));
   constexpr bool kAuxIn = EPI == EPI_RESID || EPI == EPI_GELU_BWD;
   constexpr bool kBias = EPI == EPI_STORE || EPI == EPI_BIAS_GELU || EPI == EPI_RESID;
+  // the epilogue's activation traffic streams through L2 once: evict it first so it does not
+  // push the A / B operand tiles (re-read by other CTAs) out of L2.  W's f32 reduce-adds keep
+  // the default policy (split-K re-touches the same gradient tile).
+  const uint64_t pol = sm100::l2_evict_first();
 #pragma unroll 1
   for (int ch = 0; ch < ncols / CC; ++ch) {
     const int col = col0 + ch * CC;
@@ -127,7 +131,7 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
       sm100::bulk_wait_read<0>();  // the previous chunk's store has read the staging buffer
       if (kAuxIn) {
         sm100::mbar_arrive_expect_tx(xbar, kStageBytes);
-        sm100::tma_load_2d(buf, tmX, xbar, col, row0);
+        sm100::tma_load_2d_hint(buf, tmX, xbar, col, row0, pol);
       }
     }
     __syncwarp();
@@ -172,8 +176,10 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
     if (lane == 0) {
       if (EPI == EPI_F32_ACC && reduce)
         sm100::tma_reduce_add_2d(tmC, buf, col, row0);
-      else
+      else if (EPI == EPI_F32_ACC)
         sm100::tma_store_2d(tmC, buf, col, row0);
+      else
+        sm100::tma_store_2d_hint(tmC, buf, col, row0, pol);
       sm100::bulk_commit();
     }
     if (EPI == EPI_BIAS_GELU) {  // second output: GeLU of the same f32 values
@@ -189,7 +195,7 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
       sm100::fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        sm100::tma_store_2d(tmX, buf, col, row0);
+        sm100::tma_store_2d_hint(tmX, buf, col, row0, pol);
         sm100::bulk_commit();
       }
     }
