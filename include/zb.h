@@ -233,6 +233,19 @@ zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, int32_t n, 
 zb_status_t zb_run_iteration_local(zb_ctx_t* const* ctxs, int32_t p, const zb_pass_t* passes, int32_t n,
                                    const int32_t* tokens, const int32_t* labels, int32_t flags);
 
+/* One iteration of a WORKER that holds k model chunks of a chunked schedule
+ * (zb_schedule_chunked: ZB-V, 1F1B-I; §6).  chunks[k]: the
+ * worker's chunk contexts, each created as virtual stage v of nv = chunks*p
+ * (cfg.stage = v, cfg.p = nv) and attached to a transport (zb_ctx_attach_loopback
+ * with rank v); passes: the full zb_schedule_chunked output (grouped by worker).
+ * The chunks' per-stage plans are merged in the worker's pass order, so the
+ * worker runs ZB-V's three phases exactly as scheduled, one host thread per
+ * worker.  Post-validation (zb_post_validate_step / _finish per chunk: steps in
+ * ascending v, finishes in descending v on each worker) must be finished
+ * before the next iteration (no speculative warm-up Fs): ZB_ESTATE otherwise. */
+zb_status_t zb_run_iteration_worker(zb_ctx_t* const* chunks, int32_t k, const zb_pass_t* passes, int32_t n,
+                                    const int32_t* tokens, const int32_t* labels, int32_t flags);
+
 /* Per-pass event times of the last ZB_RUN_TIMING run (syncs). */
 zb_status_t zb_ctx_read_stats(zb_ctx_t* ctx, zb_iter_stats_t* stats);
 

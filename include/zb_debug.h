@@ -72,6 +72,12 @@ zb_status_t zb_dbg_stage_plan(const zb_pass_t* passes, int32_t n, int32_t p, int
                               int32_t pv_pending, int32_t amend, int32_t fused, int32_t* out_ops, int32_t cap,
                               int32_t* n_out);
 /* n'_s, the number of speculative warm-up Fs of each stage (plan.h). */
+/* Merged op list of one worker of a chunked schedule (plan.h worker_plan):
+ * 5 ints per op: type, microbatch, message index, slot, chunk (virtual stage).
+ * worker_of[nv]: the worker of every virtual stage. */
+zb_status_t zb_dbg_worker_plan(const zb_pass_t* passes, int32_t n, int32_t nv, int32_t m, int32_t worker,
+                               const int32_t* worker_of, int32_t fused, int32_t* out_ops, int32_t cap,
+                               int32_t* n_out);
 zb_status_t zb_dbg_speculative_counts(const zb_pass_t* passes, int32_t n, int32_t p, int32_t* out);
 
 #ifdef __cplusplus

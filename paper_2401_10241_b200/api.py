@@ -280,6 +280,24 @@ def run_local(ctxs: Sequence[Context], passes, tokens, labels, host_inputs=False
     check(lib.zb_run_iteration_local(arr, len(ctxs), passes, len(passes), tp, lp, flags))
 
 
+def run_worker(chunks: Sequence[Context], passes, tokens=None, labels=None, fused=False, timing=False):
+    """zb_run_iteration_worker: one worker's chunk contexts (virtual stages of a
+    zb_schedule_chunked schedule), executed in the worker's pass order."""
+    arr = (C.c_void_p * len(chunks))(*[c.h.value for c in chunks])
+    flags = (ZB_RUN_TIMING if timing else 0) | (4 if fused else 0)
+    check(lib.zb_run_iteration_worker(arr, len(chunks), passes, len(passes), _ptr(tokens), _ptr(labels), flags))
+
+
+def worker_plan(passes, nv: int, m: int, worker: int, worker_of: Sequence[int], fused: bool = False):
+    """zb_dbg_worker_plan -> [(type, microbatch, msg, slot, chunk)]."""
+    cap = 16 * len(passes) + 64
+    buf = (C.c_int32 * (5 * cap))()
+    wo = (C.c_int32 * nv)(*worker_of)
+    n = C.c_int32()
+    check(lib.zb_dbg_worker_plan(passes, len(passes), nv, m, worker, wo, int(fused), buf, cap, C.byref(n)))
+    return [tuple(buf[5 * i:5 * i + 5]) for i in range(n.value)]
+
+
 def post_validate_local(ctxs: Sequence[Context], opt: zb_optim_cfg_t):
     arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
     check(lib.zb_post_validate_local(arr, len(ctxs), C.byref(opt)))

@@ -133,14 +133,15 @@ extern "C" zb_status_t zb_ctx_set_params(zb_ctx_t* ctx, const float* const* host
     Ctx* c = C_(ctx);
     if (n != static_cast<int32_t>(c->params.size())) return set_error(ZB_EINVAL, "wrong parameter count");
     ZB_CUDA(cudaStreamSynchronize(c->stream));
-    ZB_CUDA(cudaMemset(c->theta, 0, sizeof(float) * c->n_total));
+    // every initialisation is ordered on the context's own (possibly non-blocking) stream
+    ZB_CUDA(cudaMemsetAsync(c->theta, 0, sizeof(float) * c->n_total, c->stream));
     for (int i = 0; i < n; ++i)
-      ZB_CUDA(cudaMemcpy(c->theta + c->params[i].off, host[i], sizeof(float) * c->params[i].numel,
-                         cudaMemcpyHostToDevice));
-    ZB_CUDA(cudaMemset(c->m, 0, sizeof(float) * c->n_total));
-    ZB_CUDA(cudaMemset(c->v, 0, sizeof(float) * c->n_total));
-    ZB_CUDA(cudaMemset(c->grad, 0, sizeof(float) * c->n_total));
-    ZB_CUDA(cudaMemset(c->pv, 0, sizeof(PvState)));
+      ZB_CUDA(cudaMemcpyAsync(c->theta + c->params[i].off, host[i], sizeof(float) * c->params[i].numel,
+                              cudaMemcpyHostToDevice, c->stream));
+    ZB_CUDA(cudaMemsetAsync(c->m, 0, sizeof(float) * c->n_total, c->stream));
+    ZB_CUDA(cudaMemsetAsync(c->v, 0, sizeof(float) * c->n_total, c->stream));
+    ZB_CUDA(cudaMemsetAsync(c->grad, 0, sizeof(float) * c->n_total, c->stream));
+    ZB_CUDA(cudaMemsetAsync(c->pv, 0, sizeof(PvState), c->stream));
     if (c->shadow) convert_f32(DT_BF16, c->theta, c->shadow, c->n_shadow, c->stream);
     ZB_CUDA(cudaStreamSynchronize(c->stream));
     return ZB_OK;
@@ -283,6 +284,19 @@ extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, 
         c->backward_weight(q.microbatch, q.slot);
       if (flags & ZB_RUN_TIMING) c->timing_end(c->n_timed++);
     }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_run_iteration_worker(zb_ctx_t* const* chunks, int32_t k, const zb_pass_t* passes,
+                                               int32_t n, const int32_t* tokens, const int32_t* labels,
+                                               int32_t flags) {
+  ZB_TRY {
+    if (!chunks || k < 1 || !passes || n <= 0) return set_error(ZB_EINVAL, "bad arguments");
+    std::vector<Ctx*> cs(k);
+    for (int i = 0; i < k; ++i) cs[i] = C_(chunks[i]);
+    run_iteration_worker(cs, passes, n, tokens, labels, flags);
     return ZB_OK;
   }
   ZB_CATCH

@@ -231,3 +231,24 @@ extern "C" zb_status_t zb_dbg_speculative_counts(const zb_pass_t* passes, int32_
   }
   ZB_CATCH
 }
+
+extern "C" zb_status_t zb_dbg_worker_plan(const zb_pass_t* passes, int32_t n, int32_t nv, int32_t m, int32_t worker,
+                                          const int32_t* worker_of, int32_t fused, int32_t* out_ops, int32_t cap,
+                                          int32_t* n_out) {
+  ZB_TRY {
+    if (!passes || nv < 1 || m < 1 || !worker_of || !out_ops || !n_out)
+      return set_error(ZB_EINVAL, "zb_dbg_worker_plan: bad arguments");
+    auto ops = plan::worker_plan(passes, n, nv, m, worker, worker_of, fused != 0);
+    *n_out = static_cast<int32_t>(ops.size());
+    if (static_cast<int32_t>(ops.size()) > cap) return set_error(ZB_ECAP, "plan longer than cap");
+    for (size_t i = 0; i < ops.size(); ++i) {
+      out_ops[5 * i] = ops[i].op.type;
+      out_ops[5 * i + 1] = ops[i].op.mb;
+      out_ops[5 * i + 2] = ops[i].op.msg;
+      out_ops[5 * i + 3] = ops[i].op.slot;
+      out_ops[5 * i + 4] = ops[i].chunk;
+    }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}

@@ -398,40 +398,44 @@ void pv_send_full(Ctx& c) {
 }
 
 // ---------------------------------------------------------------- runner
-void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* tokens, const int32_t* labels,
-                        int flags) {
-  Comm& cm = *c.comm;
-  const int p = c.cfg.p, m = c.cfg.m, s = c.cfg.stage, T = c.T;
-  const size_t act_bytes = c.esz * static_cast<size_t>(T) * c.h;
-  const bool fused = (flags & ZB_RUN_FUSED_BW) != 0;
-  // inputs (host or device) are handled exactly as in the single-stage runner
-  const size_t nt = static_cast<size_t>(m) * T;
-  if (flags & ZB_RUN_HOST_INPUTS) {
-    if (c.first && tokens) {
-      ZB_CUDA(cudaMemcpyAsync(c.tok_stage, tokens, nt * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
-      tokens = c.tok_stage;
-    }
-    if (c.last && labels) {
-      ZB_CUDA(cudaMemcpyAsync(c.lab_stage, labels, nt * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
-      labels = c.lab_stage;
-    }
-  }
-  if (c.first && !tokens) throw Error(ZB_EINVAL, "tokens required on stage 0");
-  if (c.last && !labels) throw Error(ZB_EINVAL, "labels required on the last stage");
-  c.first_b_done = c.first_w_done = false;
-  ZB_CUDA(cudaMemsetAsync(c.loss_acc, 0, sizeof(double), c.stream));
+// Executes plan ops of ONE stage context (its send rings and input pointers).
+struct StageExec {
+  Ctx& c;
+  Comm& cm;
+  const int32_t* tokens;
+  const int32_t* labels;
+  int flags;
+  size_t act_bytes, grad_bytes;
+  int act_ring = 0, grad_ring = 0, last_act_buf = -1, last_grad_buf = -1;
 
-  const bool pending = c.pv_pending;
-  std::vector<plan::Op> ops = plan::stage_plan(passes, n, p, m, s, pending, false, fused);
-  std::vector<plan::Op> ops_amend;
-  if (pending) ops_amend = plan::stage_plan(passes, n, p, m, s, true, true, fused);
-  const size_t grad_bytes = sizeof(float) * static_cast<size_t>(T) * c.h;  // f32 gradient stream (R-grad32)
-  int act_ring = 0, grad_ring = 0;
-  int last_act_buf = -1, last_grad_buf = -1;
-  c.n_timed = 0;
-  bool switched = false;
-  for (size_t k = 0; k < ops.size(); ++k) {
-    const plan::Op op = ops[k];
+  StageExec(Ctx& c_, const int32_t* tok, const int32_t* lab, int fl)
+      : c(c_), cm(*c_.comm), tokens(tok), labels(lab), flags(fl) {
+    act_bytes = c.esz * static_cast<size_t>(c.T) * c.h;
+    grad_bytes = sizeof(float) * static_cast<size_t>(c.T) * c.h;  // f32 gradient stream (R-grad32)
+  }
+
+  // H2D of host inputs, input checks, per-iteration resets (as the single-stage runner)
+  void begin() {
+    const size_t nt = static_cast<size_t>(c.cfg.m) * c.T;
+    if (flags & ZB_RUN_HOST_INPUTS) {
+      if (c.first && tokens) {
+        ZB_CUDA(cudaMemcpyAsync(c.tok_stage, tokens, nt * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+        tokens = c.tok_stage;
+      }
+      if (c.last && labels) {
+        ZB_CUDA(cudaMemcpyAsync(c.lab_stage, labels, nt * sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+        labels = c.lab_stage;
+      }
+    }
+    if (c.first && !tokens) throw Error(ZB_EINVAL, "tokens required on stage 0");
+    if (c.last && !labels) throw Error(ZB_EINVAL, "labels required on the last stage");
+    c.first_b_done = c.first_w_done = false;
+    ZB_CUDA(cudaMemsetAsync(c.loss_acc, 0, sizeof(double), c.stream));
+    c.n_timed = 0;
+  }
+
+  void exec(const plan::Op& op) {
+    const int T = c.T;
     Slot* sl = op.slot >= 0 ? &c.slots.at(op.slot) : nullptr;
     switch (op.type) {
       case plan::OP_RECV_ACT: {
@@ -496,27 +500,78 @@ void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* t
         if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
         break;
       }
-      case plan::OP_VALIDATE: {
-        pv_recv_full(c);
-        pv_send_full(c);
-        pv_decide_final(c.pv, c.pv_clip, c.stream);
-        adamw_apply(c.theta, c.m, c.v, c.grad, c.shadow, c.n_total, c.n_wd, c.shadow ? c.n_shadow : 0, c.pv_opt[0],
-                    c.pv_opt[1], c.pv_opt[2], c.pv_opt[3], c.pv_opt[4], c.pv, c.stream);
-        pv_finish_apply(c.pv, c.stream);
-        c.pv_pending = false;
-        // the host needs the outcome to know whether the speculative Fs must be replayed
-        PvState hst;
-        ZB_CUDA(cudaMemcpyAsync(&hst, c.pv, sizeof(PvState), cudaMemcpyDeviceToHost, c.stream));
-        ZB_CUDA(cudaStreamSynchronize(c.stream));
-        const double coef = c.pv_clip / (std::sqrt(hst.full_sumsq) + 1e-6);
-        const bool amend = hst.full_nf != 0 || coef < 1.0;  // identical on every stage
-        if (amend && !switched) {
-          ops = ops_amend;  // same prefix up to and including this VALIDATE
-          switched = true;
-        }
-        break;
-      }
+      default:
+        throw Error(ZB_EINVAL, "StageExec: unexpected op");
     }
+  }
+};
+
+void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* tokens, const int32_t* labels,
+                        int flags) {
+  const int p = c.cfg.p, m = c.cfg.m, s = c.cfg.stage;
+  const bool fused = (flags & ZB_RUN_FUSED_BW) != 0;
+  StageExec ex(c, tokens, labels, flags);
+  ex.begin();
+  const bool pending = c.pv_pending;
+  std::vector<plan::Op> ops = plan::stage_plan(passes, n, p, m, s, pending, false, fused);
+  std::vector<plan::Op> ops_amend;
+  if (pending) ops_amend = plan::stage_plan(passes, n, p, m, s, true, true, fused);
+  bool switched = false;
+  for (size_t k = 0; k < ops.size(); ++k) {
+    const plan::Op op = ops[k];
+    if (op.type != plan::OP_VALIDATE) {
+      ex.exec(op);
+      continue;
+    }
+    pv_recv_full(c);
+    pv_send_full(c);
+    pv_decide_final(c.pv, c.pv_clip, c.stream);
+    adamw_apply(c.theta, c.m, c.v, c.grad, c.shadow, c.n_total, c.n_wd, c.shadow ? c.n_shadow : 0, c.pv_opt[0],
+                c.pv_opt[1], c.pv_opt[2], c.pv_opt[3], c.pv_opt[4], c.pv, c.stream);
+    pv_finish_apply(c.pv, c.stream);
+    c.pv_pending = false;
+    // the host needs the outcome to know whether the speculative Fs must be replayed
+    PvState hst;
+    ZB_CUDA(cudaMemcpyAsync(&hst, c.pv, sizeof(PvState), cudaMemcpyDeviceToHost, c.stream));
+    ZB_CUDA(cudaStreamSynchronize(c.stream));
+    const double coef = c.pv_clip / (std::sqrt(hst.full_sumsq) + 1e-6);
+    const bool amend = hst.full_nf != 0 || coef < 1.0;  // identical on every stage
+    if (amend && !switched) {
+      ops = ops_amend;  // same prefix up to and including this VALIDATE
+      switched = true;
+    }
+  }
+}
+
+void run_iteration_worker(const std::vector<Ctx*>& chunks, const zb_pass_t* passes, int n, const int32_t* tokens,
+                          const int32_t* labels, int flags) {
+  if (chunks.empty()) throw Error(ZB_EINVAL, "no chunk contexts");
+  const int nv = chunks[0]->cfg.p, m = chunks[0]->cfg.m;
+  std::vector<int> worker_of(nv, -1);
+  std::vector<StageExec*> ex(nv, nullptr);
+  std::vector<std::unique_ptr<StageExec>> own;
+  // passes come grouped by worker (zb_schedule_chunked), chunks x 3m passes per worker
+  const int per_worker = 3 * m * static_cast<int>(chunks.size());
+  if (per_worker <= 0 || n % per_worker) throw Error(ZB_EINVAL, "pass count is not workers x chunks x 3m");
+  for (int i = 0; i < n; ++i) {
+    const int v = passes[i].stage, w = i / per_worker;
+    if (worker_of[v] >= 0 && worker_of[v] != w) throw Error(ZB_EINVAL, "a virtual stage spans two workers");
+    worker_of[v] = w;
+  }
+  int me = -1;
+  for (Ctx* c : chunks) {
+    if (c->cfg.p != nv || c->cfg.m != m || !c->comm) throw Error(ZB_EINVAL, "chunk contexts must share p, m and a transport");
+    const int v = c->cfg.stage;
+    if (me >= 0 && worker_of[v] != me) throw Error(ZB_EINVAL, "chunk contexts belong to different workers");
+    me = worker_of[v];
+    if (c->pv_pending) throw Error(ZB_ESTATE, "chunked schedules: call zb_post_validate_finish before the next iteration");
+    own.emplace_back(new StageExec(*c, c->first ? tokens : nullptr, c->last ? labels : nullptr, flags));
+    ex[v] = own.back().get();
+    ex[v]->begin();
+  }
+  for (const plan::WOp& w : plan::worker_plan(passes, n, nv, m, me, worker_of.data(), (flags & ZB_RUN_FUSED_BW) != 0)) {
+    if (!ex[w.chunk]) throw Error(ZB_EINVAL, "worker plan references a chunk without a context");
+    ex[w.chunk]->exec(w.op);
   }
 }
 

@@ -73,6 +73,12 @@ void attach_nccl(Ctx& c, const void* ids, int rank, int world);
 // One iteration of this stage's passes with NCCL send / recv.
 void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* tokens, const int32_t* labels,
                         int flags);
+// One iteration of a WORKER holding several chunk contexts (virtual stages of a chunked
+// schedule, zb_schedule_chunked): the chunks' plans merged in the worker's pass order
+// (plan::worker_plan).  Every chunk context must be attached to a transport as virtual
+// stage cfg.stage of cfg.p; post-validation must be finished before the next iteration.
+void run_iteration_worker(const std::vector<Ctx*>& chunks, const zb_pass_t* passes, int n, const int32_t* tokens,
+                          const int32_t* labels, int flags);
 // Post-validation chain messages over the attached communicators.
 void pv_recv_partial(Ctx& c);
 void pv_send_partial(Ctx& c);

@@ -718,7 +718,7 @@ static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs&
   SplitFlags& f = bufs[st];
   if (!f.dev) {
     ZB_CUDA(cudaMalloc(&f.dev, sizeof(int32_t) * 16 * kMaxFlagTiles));
-    ZB_CUDA(cudaMemset(f.dev, 0, sizeof(int32_t) * 16 * kMaxFlagTiles));
+    ZB_CUDA(cudaMemsetAsync(f.dev, 0, sizeof(int32_t) * 16 * kMaxFlagTiles, st));  // ordered on st
   }
   if (f.base > (1 << 30)) {  // counters would overflow: reset (ordered after earlier work on st)
     ZB_CUDA(cudaMemsetAsync(f.dev, 0, sizeof(int32_t) * 16 * kMaxFlagTiles, st));

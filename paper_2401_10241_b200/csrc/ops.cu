@@ -786,7 +786,9 @@ static ColredScratch colred_scratch(cudaStream_t st) {
   if (!c.part) {
     ZB_CUDA(cudaMalloc(&c.part, sizeof(float) * kColredPartFloats));
     ZB_CUDA(cudaMalloc(&c.tickets, sizeof(int32_t) * kColredTickets));
-    ZB_CUDA(cudaMemset(c.tickets, 0, sizeof(int32_t) * kColredTickets));
+    // on the stream itself: a legacy-stream cudaMemset is not ordered before work on a
+    // non-blocking stream (the first launch could read uninitialised tickets)
+    ZB_CUDA(cudaMemsetAsync(c.tickets, 0, sizeof(int32_t) * kColredTickets, st));
   }
   return c;
 }

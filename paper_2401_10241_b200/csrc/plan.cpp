@@ -80,5 +80,45 @@ std::vector<Op> stage_plan(const zb_pass_t* passes, int n, int p, int m, int sta
   return ops;
 }
 
+std::vector<WOp> worker_plan(const zb_pass_t* passes, int n, int nv, int m, int worker, const int* worker_of,
+                             bool fused) {
+  std::vector<std::vector<std::vector<Op>>> groups(nv);  // per virtual stage of this worker: per pass
+  for (int v = 0; v < nv; ++v) {
+    if (worker_of[v] != worker) continue;
+    for (const Op& op : stage_plan(passes, n, nv, m, v, false, false, fused)) {
+      const bool compute = op.type == OP_F || op.type == OP_B || op.type == OP_W;
+      const bool recv = op.type == OP_RECV_ACT || op.type == OP_RECV_GRAD;
+      // a new group starts at a receive or at a compute op unless the group is still waiting for its pass
+      bool fresh = groups[v].empty();
+      if (!fresh) {
+        bool has_compute = false;
+        for (const Op& q : groups[v].back())
+          if (q.type == OP_F || q.type == OP_B || q.type == OP_W) has_compute = true;
+        fresh = has_compute && (recv || compute);
+      }
+      if (fresh) groups[v].emplace_back();
+      groups[v].back().push_back(op);
+    }
+  }
+  std::vector<size_t> next(nv, 0);
+  std::vector<WOp> out;
+  for (int i = 0; i < n; ++i) {
+    const zb_pass_t& q = passes[i];
+    if (q.stage < 0 || q.stage >= nv) throw std::invalid_argument("pass stage out of range");
+    if (worker_of[q.stage] != worker) continue;
+    auto& g = groups[q.stage];
+    if (next[q.stage] >= g.size()) throw std::invalid_argument("worker plan: more passes than plan groups");
+    bool match = false;
+    for (const Op& op : g[next[q.stage]]) {
+      if ((op.type == OP_F || op.type == OP_B || op.type == OP_W) && op.type == q.kind && op.mb == q.microbatch)
+        match = true;
+      out.push_back({q.stage, op});
+    }
+    if (!match) throw std::logic_error("worker plan: pass order and plan groups disagree");
+    ++next[q.stage];
+  }
+  return out;
+}
+
 }  // namespace plan
 }  // namespace zb

@@ -46,5 +46,18 @@ std::vector<int> speculative_counts(const zb_pass_t* passes, int n, int p);
 std::vector<Op> stage_plan(const zb_pass_t* passes, int n, int p, int m, int stage, bool pv_pending, bool amend,
                            bool fused);
 
+// ---- workers holding several model chunks (zb_schedule_chunked: ZB-V, 1F1B-I) ----------
+// Every chunk is a virtual stage v of an nv-stage chain (its own context and channels to
+// v-1 / v+1); a worker executes the ops of its chunks in ITS pass order: the plan of each
+// chunk (stage_plan over nv virtual stages, no post-validation speculation) is cut into one
+// group per pass ([RECV] pass [SEND]) and the groups are merged in the order in which the
+// worker's passes appear in `passes`.  worker_of[v] gives the worker of every virtual stage.
+struct WOp {
+  int32_t chunk;  // virtual stage the op belongs to
+  Op op;
+};
+std::vector<WOp> worker_plan(const zb_pass_t* passes, int n, int nv, int m, int worker, const int* worker_of,
+                             bool fused);
+
 }  // namespace plan
 }  // namespace zb

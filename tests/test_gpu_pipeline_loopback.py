@@ -166,3 +166,65 @@ def test_loopback_post_validation_with_speculation(case):
         assert all(r["final"] in ("skip", "none") and r["t"] == 0 for r in reps), reps
         assert np.isnan(got[0])
     _assert_same(got, want, case)
+
+
+# ---------------------------------------------------------------- chunked schedules (ZB-V, 1F1B-I)
+CFG_V = zb_synth.ModelConfig("lbv", h=64, a=1, L=8, s=256, b=2, V=512, p=4, m=8, family="zbh1")
+
+
+def _chunk_contexts(cfg, p, family, dtype, own_streams):
+    import torch
+    from paper_2401_10241_b200 import api
+    nv = 2 * p
+    passes, sim = api.schedule_chunked(family, p, cfg.m, 2, 10, 11, 6, 1, M_B=10, M_W=10)
+    ctxs = []
+    for v in range(nv):
+        st = torch.cuda.Stream() if own_streams else None
+        c = api.Context(cfg, nv, v, cfg.m, max(1, sim.n_slots[v]), dtype=dtype, stream=st)
+        params = zb_synth.make_stage_params(cfg, nv, v)
+        c.set_params([params[n] for n, _, _ in zb_synth.param_specs(cfg, nv, v)])
+        ctxs.append(c)
+    per = 3 * 2 * cfg.m
+    workers = [sorted({passes[i].stage for i in range(w * per, (w + 1) * per)}) for w in range(p)]
+    return ctxs, passes, workers
+
+
+@pytest.mark.parametrize("family", ["zbv", "1f1bi"])
+def test_loopback_chunked_workers_equal_virtual_stages(family):
+    """p = 4 workers x 2 chunks (P:404 V placement / cyclic 1F1B-I), each worker
+    one host thread running zb_run_iteration_worker in its own pass order over
+    the loopback transport; two iterations with the post-validated step between
+    (steps in ascending v, finishes in descending v per worker).  Reference: the
+    same 8 chunk contexts under zb_run_iteration_local / zb_post_validate_local."""
+    import torch
+    from paper_2401_10241_b200 import api
+    p, dtype = CFG_V.p, "bf16"
+    nv = 2 * p
+    tok1, lab1 = _inputs(CFG_V, 0)
+    tok2, lab2 = _inputs(CFG_V, 1)
+    opt = api.optim_cfg(mode="pv", lr=1e-3, clip=1e6)
+    ref, passes, workers = _chunk_contexts(CFG_V, p, family, dtype, own_streams=False)
+    api.run_local(ref, passes, tok1, lab1)
+    api.post_validate_local(ref, opt)
+    api.run_local(ref, passes, tok2, lab2)
+    want = _state(ref)
+
+    ctxs, passes, workers = _chunk_contexts(CFG_V, p, family, dtype, own_streams=True)
+    group = api.Loopback(nv)
+    for c in ctxs:
+        c.attach_loopback(group)
+    torch.cuda.synchronize()
+    fused = family == "1f1bi"
+
+    def worker(w, _):
+        mine = [ctxs[v] for v in workers[w]]
+        for it, (tok, lab) in enumerate(((tok1, lab1), (tok2, lab2))):
+            api.run_worker(mine, passes, tok if 0 in workers[w] else None, lab if nv - 1 in workers[w] else None,
+                           fused=fused)
+            if it == 0:
+                for c in sorted(mine, key=lambda c: c.stage):
+                    c.post_validate_step(opt)
+                for c in sorted(mine, key=lambda c: -c.stage):
+                    c.post_validate_finish(opt)
+    _threads(list(range(p)), worker)
+    _assert_same(_state(ctxs), want, family)
