@@ -114,7 +114,8 @@ zb_status_t zb_simulate(int32_t p, int32_t m, zb_pass_t* passes, int32_t n, cons
  * sim: cost / work / bubble_rate per worker (work = busiest worker's busy
  * time), peak_bytes[w] per worker, n_slots[v] per virtual stage.
  * Errors: ZB_EINVAL (p < 1, m < 1, chunks * p > 64, chunks != 2 for ZB_V,
- * m % p != 0 for ZB_1F1B_I, bad family), ZB_ECAP (out_cap < 3*chunks*p*m). */
+ * m % p != 0 for ZB_1F1B_I, bad family), ZB_ECAP (out_cap < 3*chunks*p*m),
+ * ZB_ELIMIT (ZB_V with 0 < M_limit < the construction's per-worker peak). */
 enum { ZB_V = 4, ZB_1F1B_I = 5 };
 zb_status_t zb_schedule_chunked(int32_t p, int32_t m, int32_t chunks, int64_t T_F, int64_t T_B, int64_t T_W,
                                 int64_t T_comm, int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family,

@@ -400,6 +400,8 @@ def zbv_schedule(p: int, m: int, TF: int, TB: int, TW: int, Tcomm: int = 0, MB: 
     base = build_zbv(p, m)
     place = lambda v: worker_of(p, v)
     lim = Mlimit if Mlimit is not None else max(memory_peaks_v(base, MB, MW))
+    if max(memory_peaks_v(base, MB, MW)) > lim:
+        raise ValueError("M_limit below the ZB-V construction's peak (p M_B of a stage)")
     cands = [(0, base)]
     for idx, rule in ((1, "gap"), (2, "fill")):
         try:

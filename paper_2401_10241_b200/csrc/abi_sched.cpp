@@ -157,6 +157,11 @@ extern "C" zb_status_t zb_schedule_chunked(int32_t p, int32_t m, int32_t chunks,
       if (chunks != 2) return set_error(ZB_EINVAL, "ZB-V needs chunks == 2");
       lists = sched::zbv_schedule(p, m, T_F, T_B, T_W, T_comm, M_B, M_W, M_limit, &chosen);
       for (int v = 0; v < nv; ++v) place[v] = sched::zbv_worker(p, v);
+      if (M_limit > 0) {
+        auto pk = sched::memory_peaks_v(lists, M_B, M_W);
+        if (*std::max_element(pk.begin(), pk.end()) > M_limit)
+          return set_error(ZB_ELIMIT, "ZB-V needs at least its construction's peak (p stage M_B) per worker");
+      }
     } else if (family == ZB_1F1B_I) {
       if (m % p) return set_error(ZB_EINVAL, "1F1B-I needs m divisible by p");
       lists = sched::build_1f1b_interleaved(p, m, chunks);

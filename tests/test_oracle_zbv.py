@@ -172,3 +172,8 @@ def test_table4_interleaved_column(row):
 def test_table6_interleaved_28p3B(row):
     p, m = int(row["p"]), int(row["m"])
     assert abs(_interleaved_rate("28.3B", p, m, _t8("28.3B", m)) - float(row["1F1B-I"])) < 0.005
+
+
+def test_zbv_limit_below_its_peak_rejected():
+    with pytest.raises(ValueError):
+        zbv.zbv_schedule(4, 8, 1, 1, 1, 0, 1, 1, Mlimit=7)

@@ -152,7 +152,9 @@ def test_zbv_random_limits():
         p, m = rnd.randint(1, 6), rnd.randint(1, 20)
         TF, TB, TW, Tc = rnd.randint(1, 60), rnd.randint(1, 60), rnd.randint(1, 60), rnd.randint(0, 8)
         MB, MW = rnd.randint(1, 9), rnd.randint(1, 9)
-        lim = rnd.choice([0, 2 * p * MB, 2 * p * MB + MB, 4 * p * MB])
+        from oracle import zbv
+        pk = max(zbv.memory_peaks_v(zbv.build_zbv(p, m), MB, MW))
+        lim = rnd.choice([0, pk, pk + MB, 2 * pk])
         compare_chunked("zbv", p, m, 2, TF, TB, TW, Tc, MB, MW, lim)
 
 
