@@ -686,7 +686,7 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
 // Ordered split-K of the W contraction (EPI_F32_ACC, K = T tokens): W's M x N (weight
 // shape) often gives few 256 x 256 tiles for 74 CTA pairs (proj 2304 x 2304: 81 tiles =
 // 2 rounds at 55% occupancy).  Pick the split count S <= 4 (>= 16 k-blocks per split)
-// minimising ceil(S tiles / pairs) / S, smallest S on ties.  The flag counters live in a
+// minimising ceil(S tiles / pairs) / S x (1 + 0.15 (S - 1)), smallest S on ties.  The flag counters live in a
 // per-stream device buffer (zeroed once) with a per-stream launch base, so concurrent
 // streams (loopback stages) never share counters.
 struct SplitFlags {
@@ -705,12 +705,20 @@ static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs&
   int best = 1;
   double best_t = static_cast<double>(ceil_div(tiles, pairs));
   for (int sk = 2; sk <= 4 && nk / sk >= 16; ++sk) {
-    const double t = static_cast<double>(ceil_div(static_cast<int64_t>(tiles) * sk, pairs)) / sk;
+    // each extra split costs ~15% (measured on the 1.5B W shapes: 81 tiles -> S = 2 is
+    // 1.52x S = 1 but S = 4 only 1.30x; 243 / 324 tiles: S = 1 within 2% of the best)
+    const double t = static_cast<double>(ceil_div(static_cast<int64_t>(tiles) * sk, pairs)) / sk * (1.0 + 0.15 * (sk - 1));
     if (t < best_t - 1e-9) {
       best_t = t;
       best = sk;
     }
   }
+  static int force = -1;  // ZB_GEMM_SPLITK=<S>: fixed split count (measurement only)
+  if (force < 0) {
+    const char* e = getenv("ZB_GEMM_SPLITK");
+    force = e ? std::max(1, std::min(4, atoi(e))) : 0;
+  }
+  if (force) best = force;
   if (best == 1) return;
   static std::mutex mu;
   static std::map<cudaStream_t, SplitFlags> bufs;
