@@ -217,11 +217,16 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       }
       mx *= scale_log2;
-      // lazy rescaling: keep the old reference max unless it grew by more than 8 (p <= 2^8)
-      if (mx > m + 8.f) {
-        const float corr = sm100::ex2(m - mx);
-        m = mx;
-        l *= corr;
+      // lazy rescaling: keep the old reference max unless it grew by more than 8 (p <= 2^8).
+      // The decision is per row, but tcgen05.ld / st are warp-collective (.sync.aligned):
+      // the whole warp enters the rescale when any of its rows needs it (corr = 1 elsewhere).
+      const bool grow = mx > m + 8.f;
+      if (__any_sync(0xffffffffu, grow)) {
+        const float corr = grow ? sm100::ex2(m - mx) : 1.f;
+        if (grow) {
+          m = mx;
+          l *= corr;
+        }
         if (j > 0) {  // O_t holds blocks < j (PV_t(j-1) completed before S_t(j) was committed)
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {

@@ -58,3 +58,29 @@ def test_attention_parity(shape, dtype):
     for i, name in enumerate("QKV"):
         blk = slice(i * h, (i + 1) * h)
         assert rel(got[:, blk], dqkv_ref[:, blk]) < btol, name
+
+
+@pytest.mark.parametrize("d", [96, 128])
+def test_attention_fwd_divergent_lazy_rescale(d):
+    """Rows of one warp whose running max jumps at different key blocks (the lazy
+    O-rescale is taken by some rows only): the warp-collective TMEM traffic of the
+    rescale must not depend on the row (a divergent tcgen05.ld hung the 6.2B step)."""
+    import torch
+    from oracle import model as om
+    from paper_2401_10241_b200 import api
+    b, s, a = 1, 512, 2
+    h = a * d
+    g = torch.Generator().manual_seed(d)
+    qkv = torch.randn(b * s, 3 * h, generator=g) * 0.3
+    u = torch.randn(d, generator=g)
+    u = u / u.norm()
+    for hd in range(a):
+        qkv[200, h + hd * d: h + (hd + 1) * d] = 40.0 * u          # one strong key in block 1
+        qkv[300:, hd * d:(hd + 1) * d][::2] += 6.0 * u             # even query rows >= 300 align with it
+    qkv = qkv.bfloat16().cuda()
+    o = torch.empty(b * s, h, dtype=torch.bfloat16).cuda()
+    lse = torch.empty(b, a, s, dtype=torch.float32).cuda()
+    api.dbg_attention_fwd(qkv, o, lse, b=b, s=s, a=a, d=d)
+    torch.cuda.synchronize()
+    O_ref, _ = om.causal_attention_fwd(qkv.double().cpu().numpy(), b, s, a)
+    assert rel(o.double().cpu().numpy(), O_ref) < 1e-2
