@@ -184,7 +184,11 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
+        if args.family in ("zbv", "1f1bi"):
+            return run_pipeline_chunked(args, cfg, rank, world, local)
         return run_pipeline(args, cfg, rank, world, local)
+    if args.family in ("zbv", "1f1bi"):
+        raise SystemExit("--family zbv / 1f1bi needs --gpus >= 2 (two model chunks per GPU)")
     return run_single(args, cfg)
 
 
@@ -512,6 +516,79 @@ def run_pipeline(args, cfg, rank, world, local):
                 "vs_1f1b": {"tokens_per_s_1f1b": tokens_per_step / (ms_1f1b / 1000.0) if ms_1f1b else None,
                             "speedup": ms_1f1b / ms if ms_1f1b else None},
                 "model_flops_utilization": round(value * flops_token / (p * peaks.get("bf16_tflops", 1680.3) * 1e12), 4)}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def run_pipeline_chunked(args, cfg, rank, world, local):
+    """ZB-V / 1F1B-I over N GPUs (section 6): two model chunks per GPU (virtual
+    stages v of 2N, V placement for ZB-V, cyclic for 1F1B-I), NCCL links between GPUs
+    and an in-process link for ZB-V's turn (zb_ctx_attach_nccl_chunks), each GPU running
+    its merged pass list (zb_run_iteration_worker); max-over-ranks CUDA-event timing."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2401_10241_b200 import api
+
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p, m, chunks = world, cfg.m, 2
+    nv = chunks * p
+    fused = args.family == "1f1bi"
+    slot_b = api.slot_bytes(api.model_cfg(cfg, nv, 1, m, 1, "bf16"))
+    passes, sim = api.schedule_chunked(args.family, p, m, chunks, 10, 10, 10, 0, M_B=slot_b, M_W=slot_b)
+    per = 3 * chunks * m
+    worker_of = [0] * nv
+    for i in range(len(passes)):
+        worker_of[passes[i].stage] = i // per
+    mine = [v for v in range(nv) if worker_of[v] == rank]
+    ids = [api.nccl_unique_ids(2 * (nv - 1)) if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    stream = torch.cuda.Stream()
+    ctxs = []
+    for v in mine:
+        c = api.Context(cfg, nv, v, m, max(1, sim.n_slots[v]), dtype="bf16", stream=stream)
+        params = zb_synth.make_stage_params(cfg, nv, v)
+        c.set_params([params[n] for n, _, _ in zb_synth.param_specs(cfg, nv, v)])
+        del params
+        ctxs.append(c)
+    api.attach_nccl_chunks(ctxs, ids[0], nv, worker_of, rank)
+    n_steps = args.warmup + args.steps
+    toks = [zb_synth.make_tokens(cfg, i) for i in range(n_steps)]
+    tok_d = [torch.from_numpy(np.ascontiguousarray(t[..., :cfg.s])).cuda() for t in toks]
+    lab_d = [torch.from_numpy(np.ascontiguousarray(t[..., 1:])).cuda() for t in toks]
+    opt = api.optim_cfg(lr=1e-4, mode="pv", clip=1.0)
+
+    def run(steps, first):
+        for i in range(first, first + steps):
+            api.run_worker(ctxs, passes, tok_d[i % n_steps] if 0 in mine else None,
+                           lab_d[i % n_steps] if nv - 1 in mine else None, fused=fused)
+            for c in sorted(ctxs, key=lambda c: c.stage):      # partial chain: ascending v
+                c.post_validate_step(opt)
+            for c in sorted(ctxs, key=lambda c: -c.stage):     # full chain: descending v
+                c.post_validate_finish(opt)
+
+    run(args.warmup, 0)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run(args.steps, args.warmup)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t)
+    value = cfg.T * m / (ms / 1000.0)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": p, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (zb_synth seeded weights and tokens)",
+                "config": dict(workload_config(cfg, p, args.family), chunks_per_gpu=chunks),
+                "clocks": clk.summary(), "e2e": None, "roofline": None,
+                "bubble": {"predicted": sim.bubble_rate}}
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -306,6 +306,17 @@ zb_status_t zb_nccl_unique_id(void* id128);
  * or in zb_post_validate_finish when no iteration follows. */
 zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* ids, int32_t rank, int32_t world);
 
+/* Attach the k chunk contexts of worker `worker` of a chunked schedule (ZB-V,
+ * 1F1B-I; contexts created as virtual stages v of nv): links to chunks on
+ * other workers become 2-rank NCCL communicators, ids as for
+ * zb_ctx_attach_nccl with world = nv (ids[k] activations of link (k, k+1),
+ * ids[nv-1+k] its gradients; identical on every rank), links between two
+ * chunks of this worker (ZB-V's v = p-1 -> p turn) an in-process loopback
+ * channel.  worker_of[nv]: the worker of every virtual stage.  Then drive the
+ * worker with zb_run_iteration_worker.  ZB_ENCCL if libnccl is unavailable. */
+zb_status_t zb_ctx_attach_nccl_chunks(zb_ctx_t* const* chunks, int32_t k, const void* ids, int32_t nv,
+                                      const int32_t* worker_of, int32_t worker);
+
 /* In-process loopback group (test transport for one GPU): world stage
  * contexts of ONE process attach to the same group and are then driven
  * exactly like NCCL-attached contexts, each by its own host thread

@@ -97,6 +97,7 @@ _SIGS = {
                            C.POINTER(_I32)], _I32),
     "zb_dbg_worker_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, C.POINTER(_I32), _I32, C.POINTER(_I32),
                             _I32, C.POINTER(_I32)], _I32),
+    "zb_ctx_attach_nccl_chunks": ([C.POINTER(_P), _I32, _P, _I32, C.POINTER(_I32), _I32], _I32),
     "zb_run_iteration_worker": ([C.POINTER(_P), _I32, C.POINTER(zb_pass_t), _I32, _P, _P, _I32], _I32),
     "zb_dbg_speculative_counts": ([C.POINTER(zb_pass_t), _I32, _I32, C.POINTER(_I32)], _I32),
     "zb_dbg_kernel_timing": ([_I32, _I32], _I32),

@@ -288,6 +288,14 @@ def run_worker(chunks: Sequence[Context], passes, tokens=None, labels=None, fuse
     check(lib.zb_run_iteration_worker(arr, len(chunks), passes, len(passes), _ptr(tokens), _ptr(labels), flags))
 
 
+def attach_nccl_chunks(chunks: Sequence[Context], ids: bytes, nv: int, worker_of: Sequence[int], worker: int):
+    """zb_ctx_attach_nccl_chunks: NCCL links to other workers, loopback inside this worker."""
+    arr = (C.c_void_p * len(chunks))(*[c.h.value for c in chunks])
+    buf = C.create_string_buffer(ids, len(ids))
+    wo = (C.c_int32 * nv)(*worker_of)
+    check(lib.zb_ctx_attach_nccl_chunks(arr, len(chunks), buf, nv, wo, worker))
+
+
 def worker_plan(passes, nv: int, m: int, worker: int, worker_of: Sequence[int], fused: bool = False):
     """zb_dbg_worker_plan -> [(type, microbatch, msg, slot, chunk)]."""
     cap = 16 * len(passes) + 64

@@ -289,6 +289,18 @@ extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, 
   ZB_CATCH
 }
 
+extern "C" zb_status_t zb_ctx_attach_nccl_chunks(zb_ctx_t* const* chunks, int32_t k, const void* ids, int32_t nv,
+                                                 const int32_t* worker_of, int32_t worker) {
+  ZB_TRY {
+    if (!chunks || k < 1 || !ids || nv < 2 || !worker_of) return set_error(ZB_EINVAL, "bad arguments");
+    std::vector<Ctx*> cs(k);
+    for (int i = 0; i < k; ++i) cs[i] = C_(chunks[i]);
+    attach_nccl_chunks(cs, ids, nv, std::vector<int>(worker_of, worker_of + nv), worker);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 extern "C" zb_status_t zb_run_iteration_worker(zb_ctx_t* const* chunks, int32_t k, const zb_pass_t* passes,
                                                int32_t n, const int32_t* tokens, const int32_t* labels,
                                                int32_t flags) {

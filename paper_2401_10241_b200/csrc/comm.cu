@@ -344,6 +344,79 @@ void attach_loopback(Ctx& c, const std::shared_ptr<LoopbackGroup>& g, int rank) 
   c.comm = std::move(cm);
 }
 
+// ---------------------------------------------------------------- chunk contexts of one worker
+namespace {
+// per-channel composition: links to chunks on other workers ride NCCL, links between two
+// chunks of this worker (ZB-V's V turn v = p-1 -> p) ride an in-process loopback channel
+struct HybridTransport : Transport {
+  std::unique_ptr<NcclTransport> nccl;
+  std::unique_ptr<LoopbackTransport> local;
+  Transport* sub[4] = {nullptr, nullptr, nullptr, nullptr};
+  void send(int which, const void* buf, size_t bytes, cudaStream_t st) override {
+    if (!sub[which]) throw Error(ZB_EINVAL, "hybrid transport: channel not attached");
+    sub[which]->send(which, buf, bytes, st);
+  }
+  void recv(int which, void* buf, size_t bytes, cudaStream_t st) override {
+    if (!sub[which]) throw Error(ZB_EINVAL, "hybrid transport: channel not attached");
+    sub[which]->recv(which, buf, bytes, st);
+  }
+};
+}  // namespace
+
+void attach_nccl_chunks(const std::vector<Ctx*>& chunks, const void* ids, int nv, const std::vector<int>& worker_of,
+                        int me) {
+  if (static_cast<int>(worker_of.size()) != nv) throw Error(ZB_EINVAL, "worker_of must have nv entries");
+  std::vector<Ctx*> byv(nv, nullptr);
+  for (Ctx* c : chunks) {
+    if (c->cfg.p != nv || worker_of.at(c->cfg.stage) != me) throw Error(ZB_EINVAL, "chunk context / worker mismatch");
+    byv[c->cfg.stage] = c;
+  }
+  auto group = loopback_create(nv);
+  std::vector<std::unique_ptr<HybridTransport>> tx(nv);
+  for (Ctx* c : chunks) {
+    const int v = c->cfg.stage;
+    tx[v] = std::make_unique<HybridTransport>();
+    tx[v]->nccl = std::make_unique<NcclTransport>();
+    tx[v]->local = std::make_unique<LoopbackTransport>();
+    tx[v]->local->g = group;
+    tx[v]->local->rank = v;
+  }
+  const char* id = static_cast<const char*>(ids);
+  auto nccl_init = [&](int v, int which, int link, bool grad, int r) {
+    ncclUniqueId_t u;
+    std::memcpy(&u, id + 128 * (grad ? (nv - 1 + link) : link), 128);
+    nck(nccl().init(&tx[v]->nccl->comm[which], 2, u, r), "ncclCommInitRank");
+    tx[v]->sub[which] = tx[v]->nccl.get();
+  };
+  // every process walks the links in increasing order and joins the remote ones it is on:
+  // the lowest pending link always has both participants waiting on it -> no init deadlock
+  for (int k = 0; k + 1 < nv; ++k) {
+    const int a = k, b = k + 1;
+    const bool ha = worker_of[a] == me, hb = worker_of[b] == me;
+    if (ha && hb) {
+      tx[a]->sub[C_ACT_TO] = tx[a]->local.get();
+      tx[a]->sub[C_GRAD_FROM] = tx[a]->local.get();
+      tx[b]->sub[C_ACT_FROM] = tx[b]->local.get();
+      tx[b]->sub[C_GRAD_TO] = tx[b]->local.get();
+    } else if (ha) {
+      nccl_init(a, C_ACT_TO, k, false, 0);
+      nccl_init(a, C_GRAD_FROM, k, true, 0);
+    } else if (hb) {
+      nccl_init(b, C_ACT_FROM, k, false, 1);
+      nccl_init(b, C_GRAD_TO, k, true, 1);
+    }
+  }
+  for (Ctx* c : chunks) {
+    const int v = c->cfg.stage;
+    auto cm = std::make_unique<Comm>();
+    cm->rank = v;
+    cm->world = nv;
+    cm->tx = std::move(tx[v]);
+    setup_comm(*c, *cm);
+    c->comm = std::move(cm);
+  }
+}
+
 // ---------------------------------------------------------------- post-validation messages
 // message layout: double sumsq, int32 nonfinite, pad (16 bytes)
 void pv_recv_partial(Ctx& c) {

@@ -70,6 +70,12 @@ void nccl_unique_id(void* id128);
 // ids: 2*(world-1) unique ids, [k] for the activation comm of pair (k, k+1),
 // [world-1+k] for the gradient comm of the same pair.
 void attach_nccl(Ctx& c, const void* ids, int rank, int world);
+// Chunk contexts (virtual stages v of nv) of worker `me` of a chunked schedule: links to
+// chunks on other workers get 2-rank NCCL communicators (ids as attach_nccl with world =
+// nv: [k] activations of link (k, k+1), [nv-1+k] its gradients), links between two chunks
+// of this worker an in-process loopback channel.
+void attach_nccl_chunks(const std::vector<Ctx*>& chunks, const void* ids, int nv, const std::vector<int>& worker_of,
+                        int me);
 // One iteration of this stage's passes with NCCL send / recv.
 void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* tokens, const int32_t* labels,
                         int flags);

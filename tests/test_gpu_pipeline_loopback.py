@@ -228,3 +228,21 @@ def test_loopback_chunked_workers_equal_virtual_stages(family):
                     c.post_validate_finish(opt)
     _threads(list(range(p)), worker)
     _assert_same(_state(ctxs), want, family)
+
+
+def test_hybrid_attach_single_worker_zbv():
+    """zb_ctx_attach_nccl_chunks on a worker whose every link is local (ZB-V with
+    p = 1: chunks v = 0, 1 on worker 0, the V turn is the in-process channel):
+    the hybrid transport path without NCCL, bitwise equal to virtual stages."""
+    import torch
+    from paper_2401_10241_b200 import api
+    cfg = CFG_V.with_(L=4, m=3)
+    tok, lab = _inputs(cfg, 0)
+    ref, passes, workers = _chunk_contexts(cfg, 1, "zbv", "bf16", own_streams=False)
+    api.run_local(ref, passes, tok, lab)
+    want = _state(ref)
+    ctxs, passes, workers = _chunk_contexts(cfg, 1, "zbv", "bf16", own_streams=True)
+    api.attach_nccl_chunks(ctxs, b"\0" * 128 * 2, 2, [0, 0], 0)
+    torch.cuda.synchronize()
+    api.run_worker(ctxs, passes, tok, lab)
+    _assert_same(_state(ctxs), want, "hybrid")
