@@ -23,6 +23,24 @@ namespace attn_bwd_tc {
 
 constexpr float LOG2E = 1.4426950408889634f;
 
+#ifdef ZB_ATTN_TRACE
+// timeline of one CTA (blockIdx (TR_BX, 0, 0)) of k_dkdv_tc, globaltimer ns (measurement build only)
+__device__ unsigned long long g_trace[8][64];
+#ifndef TR_BX
+#define TR_BX 0
+#endif
+__device__ __forceinline__ void tr(int row, int n) {
+  if (blockIdx.x == TR_BX && blockIdx.y == 0 && blockIdx.z == 0 && n < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[row][n] = t;
+  }
+}
+#define TR(row, n) tr(row, n)
+#else
+#define TR(row, n)
+#endif
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -33,6 +51,9 @@ template <int D> struct DkdvCfg {
   static constexpr int ATOMS = (D + 63) / 64;
   static constexpr int KV_TILE = ATOMS * 16384;  // 128 rows
   static constexpr int Q_TILE = ATOMS * 8192;    // 64 rows
+  // Q_i / dO_i ring depth.  The globaltimer trace (scripts/attn_trace.py) shows ~1.1 us per
+  // 64-query step with Q_i / dO_i arriving ~1.1 us after issue; ST = 4 moved the issue 2.3 us
+  // ahead without shortening the step (arrivals stay ~1.1 us apart), so 3 stages suffice
   static constexpr int ST = 3;
   static constexpr int STAGE = 2 * Q_TILE + 1024;  // Q_i, dO_i, L_i[64], D_i[64] (1024-aligned)
   static constexpr int OFF_K = 0, OFF_V = KV_TILE, OFF_ST = 2 * KV_TILE;
@@ -50,13 +71,14 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bar + 0;
-  uint64_t* st_full = bar + 1;   // [3]
-  uint64_t* st_empty = bar + 4;  // [3]
-  uint64_t* sp_full = bar + 7;   // [2]
-  uint64_t* sp_empty = bar + 9;  // [2]
-  uint64_t* ds_full = bar + 11;  // [2]
-  uint64_t* o_final = bar + 13;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* st_full = bar + 1;                 // [ST]
+  uint64_t* st_empty = st_full + C::ST;        // [ST]
+  uint64_t* sp_full = st_empty + C::ST;        // [2]
+  uint64_t* sp_empty = sp_full + 2;            // [2]
+  uint64_t* ds_full = sp_empty + 2;            // [2]
+  uint64_t* o_final = ds_full + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_final + 1);
+  static_assert((1 + 2 * C::ST + 7) * 8 + 4 <= 256, "barrier area");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x, hd = blockIdx.y, bb = blockIdx.z;
@@ -65,6 +87,7 @@ __global__ void __launch_bounds__(384, 1)
   const int row0 = bb * s;
   const int64_t stat0 = (static_cast<int64_t>(bb) * a + hd) * s;
 
+  if (threadIdx.x == 0) TR(6, 0);
   if (threadIdx.x == 0) {
     sm100::mbar_init(kv_full, 1);
     for (int i = 0; i < C::ST; ++i) {
@@ -103,6 +126,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int n = 0; n < nq; ++n) {
         const int i = i0 + n, st = n % C::ST;
         sm100::mbar_wait(&st_empty[st], ((n / C::ST) & 1) ^ 1);
+        TR(0, n);
         uint8_t* sg = smem + C::OFF_ST + st * C::STAGE;
         sm100::mbar_arrive_expect_tx(&st_full[st], 2 * C::Q_TILE + 512);
         for (int at = 0; at < C::ATOMS; ++at) {
@@ -121,6 +145,7 @@ __global__ void __launch_bounds__(384, 1)
       auto issue_grad = [&](int n) {
         const int b = n & 1, st = n % C::ST;
         sm100::mbar_wait(&ds_full[b], (n >> 1) & 1);
+        TR(3, n);
         sm100::tc_fence_after();
         const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t sdo = sq + C::Q_TILE;
@@ -141,7 +166,9 @@ __global__ void __launch_bounds__(384, 1)
       for (int n = 0; n < nq; ++n) {
         const int b = n & 1, st = n % C::ST;
         sm100::mbar_wait(&st_full[st], (n / C::ST) & 1);
+        TR(1, n);
         sm100::mbar_wait(&sp_empty[b], ((n >> 1) & 1) ^ 1);
+        TR(2, n);
         sm100::tc_fence_after();
         const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t sdo = sq + C::Q_TILE;
@@ -169,6 +196,7 @@ __global__ void __launch_bounds__(384, 1)
       const float* Ls = reinterpret_cast<const float*>(smem + C::OFF_ST + st * C::STAGE + 2 * C::Q_TILE);
       const float* Ds = Ls + 64;
       sm100::mbar_wait(&sp_full[b], (n >> 1) & 1);
+      if (warp == 4 && lane == 0) TR(4, n);
       sm100::tc_fence_after();
       uint32_t sr[32], dr[32];
       const uint32_t tp = tbase + b * 128 + lane_off;
@@ -194,9 +222,11 @@ __global__ void __launch_bounds__(384, 1)
       sm100::tmem_st16(tp + 64 + 32 * hf, dk);  // dS^T over this half's dP^T columns
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
+      if (warp == 4 && lane == 0) TR(5, n);
       sm100::mbar_arrive(&ds_full[b]);
     }
     sm100::mbar_wait(o_final, 0);
+    if (warp == 4 && lane == 0) TR(6, 1);
     sm100::tc_fence_after();
     bf16* row = dqkv + (static_cast<int64_t>(row0) + key) * (3 * h) + hd * D;
 #pragma unroll 1
@@ -237,7 +267,7 @@ template <int D> struct DqCfg {
   static constexpr int ATOMS = (D + 63) / 64;
   static constexpr int Q_TILE = ATOMS * 16384;   // 128 rows
   static constexpr int KV_TILE = ATOMS * 8192;   // 64 rows
-  static constexpr int ST = 3;
+  static constexpr int ST = 3;  // K_j / V_j ring depth (see DkdvCfg)
   static constexpr int STAGE = 2 * KV_TILE;      // K_j, V_j
   static constexpr int OFF_Q = 0, OFF_DO = Q_TILE, OFF_ST = 2 * Q_TILE;
   static constexpr int OFF_BAR = OFF_ST + ST * STAGE;
@@ -254,13 +284,14 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* st_full = bar + 1;   // [3]
-  uint64_t* st_empty = bar + 4;  // [3]
-  uint64_t* sp_full = bar + 7;   // [2]
-  uint64_t* sp_empty = bar + 9;  // [2]
-  uint64_t* ds_full = bar + 11;  // [2]
-  uint64_t* o_final = bar + 13;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* st_full = bar + 1;                 // [ST]
+  uint64_t* st_empty = st_full + C::ST;        // [ST]
+  uint64_t* sp_full = st_empty + C::ST;        // [2]
+  uint64_t* sp_empty = sp_full + 2;            // [2]
+  uint64_t* ds_full = sp_empty + 2;            // [2]
+  uint64_t* o_final = ds_full + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_final + 1);
+  static_assert((1 + 2 * C::ST + 7) * 8 + 4 <= 256, "barrier area");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / 128;
@@ -458,3 +489,9 @@ bool attention_bwd_tc(const AttnShape& sh, const void* qkv, const void* dout, co
 }
 
 }  // namespace zb
+
+#ifdef ZB_ATTN_TRACE
+extern "C" int zb_dbg_attn_trace(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_bwd_tc::g_trace, sizeof(unsigned long long) * 8 * 64));
+}
+#endif
