@@ -161,6 +161,14 @@ __global__ void __launch_bounds__(128, 4) k_ln_fwd_rows(const bf16* __restrict__
                                                     float* __restrict__ mean, float* __restrict__ rstd, int rows, int h,
                                                     float eps) {
   pdl_wait();
+  // gamma / beta staged once per (persistent) CTA: read from shared memory per row instead of
+  // L2 (the dependent global loads of the output loop were the long-scoreboard stalls)
+  extern __shared__ float gb_sm[];  // [2][h]
+  for (int i = threadIdx.x; i < h / 4; i += blockDim.x) {
+    reinterpret_cast<float4*>(gb_sm)[i] = reinterpret_cast<const float4*>(g)[i];
+    reinterpret_cast<float4*>(gb_sm + h)[i] = reinterpret_cast<const float4*>(b)[i];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * 4;
   int64_t row = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
@@ -205,8 +213,8 @@ __global__ void __launch_bounds__(128, 4) k_ln_fwd_rows(const bf16* __restrict__
       const int vi = lane + 32 * k;
       if (vi < nv) {
         float gg[8], bb[8], o[8];
-        Vec8<float>::load(g + vi * 8, gg);
-        Vec8<float>::load(b + vi * 8, bb);
+        Vec8<float>::load(gb_sm + vi * 8, gg);
+        Vec8<float>::load(gb_sm + h + vi * 8, bb);
         const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&cur[k]);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -811,7 +819,13 @@ static void ln_fwd_warp(DType dt, const void* x, const float* g, const float* b,
                         int rows, int h, float eps, cudaStream_t st) {
   if (dt == DT_BF16) {  // persistent: 4 CTAs of 4 warps per SM (or fewer for small inputs)
     const int blocks = std::min((rows + 3) / 4, 4 * 148);
-    launch(PDL_OPS, k_ln_fwd_rows<VPL>, blocks, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y),
+    const size_t sm = 2 * sizeof(float) * static_cast<size_t>(h);
+    static bool attr = false;
+    if (!attr) {  // h <= 3072 here: at most 24 KB
+      ZB_CUDA(cudaFuncSetAttribute(k_ln_fwd_rows<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024));
+      attr = true;
+    }
+    launch(PDL_OPS, k_ln_fwd_rows<VPL>, blocks, 128, sm, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y),
            mean, rstd, rows, h, eps);
     return;
   }
