@@ -115,7 +115,8 @@ __device__ __forceinline__ int swz(int lane, int j) { return lane * 128 + ((j ^ 
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtensorMap* tmC, const CUtensorMap* tmX,
                                                 uint32_t taddr, uint8_t* buf, uint64_t* xbar, uint32_t& xph,
-                                                int row0, int col0, int ncols, int N, int lane, bool reduce) {
+                                                int row0, int col0, int ncols, int N, int lane, bool reduce,
+                                                bool pre = false) {
   using TO = OutT<EPI>;
   constexpr int CC = 128 / static_cast<int>(sizeof(TO));
   constexpr bool kAuxIn = EPI == EPI_RESID || EPI == EPI_GELU_BWD;
@@ -127,7 +128,7 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
 #pragma unroll 1
   for (int ch = 0; ch < ncols / CC; ++ch) {
     const int col = col0 + ch * CC;
-    if (lane == 0) {
+    if (lane == 0 && !(pre && ch == 0)) {  // pre: chunk 0's aux tile was requested by the caller
       sm100::bulk_wait_read<0>();  // the previous chunk's store has read the staging buffer
       if (kAuxIn) {
         sm100::mbar_arrive_expect_tx(xbar, kStageBytes);
@@ -522,12 +523,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_proxy_async_global();
       }
       __syncwarp();
+      const int erow = mt * BM2 + static_cast<int>(rank) * BM + ew * 32, ecol = nt * BN + half * (BN / 2);
+      constexpr bool kAuxIn = EPI == EPI_RESID || EPI == EPI_GELU_BWD;
+      if (kAuxIn && lane == 0) {  // request chunk 0's aux tile while this tile's MMAs still run
+        sm100::bulk_wait_read<0>();
+        sm100::mbar_arrive_expect_tx(&xbar[warp - 4], kStageBytes);
+        sm100::tma_load_2d_hint(buf, &tmX, &xbar[warp - 4], ecol, erow, sm100::l2_evict_first());
+      }
       sm100::mbar_wait(&tfull[acc], aph);
       sm100::tc_fence_after();
       epilogue_chunks<EPI>(ep, &tmC, &tmX,
                            tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
-                           &xbar[warp - 4], xph, mt * BM2 + static_cast<int>(rank) * BM + ew * 32,
-                           nt * BN + half * (BN / 2), BN / 2, N, lane, ep.beta != 0 || sp > 0);
+                           &xbar[warp - 4], xph, erow, ecol, BN / 2, N, lane, ep.beta != 0 || sp > 0, kAuxIn);
       if (sp + 1 < splits && lane == 0) {  // publish: this region's reduce-adds are complete
         sm100::bulk_wait<0>();
         fence_proxy_async_global();
