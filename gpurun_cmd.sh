@@ -1,2 +1,2 @@
-timeout 300 python -m pytest tests/test_gpu_attention.py -x -q -m gpu 2>&1 | tail -15
-echo "=== tc"; timeout 200 python scripts/attn_perf.py 2>&1 | tail -4
+timeout 120 python -m pytest tests/test_gpu_attention.py -x -q 2>&1 | tail -2
+timeout 60 python scripts/attn_perf.py 2>&1 | tail -3

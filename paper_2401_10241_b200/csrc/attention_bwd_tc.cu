@@ -150,13 +150,13 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t sdo = sq + C::Q_TILE;
         const uint32_t tp = tbase + b * 128;
+        const uint64_t dod = sm100::smem_desc(sdo, 8192, 1024, sm100::kSwizzle128B);
+        const uint64_t qd = sm100::smem_desc(sq, 8192, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries: halves live at columns [0,16) and [32,48)
           const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
-          sm100::mma_bf16_ts(t_dv, tp + acol, sm100::smem_desc(sdo + kk * 2048, 8192, 1024, sm100::kSwizzle128B),
-                             idesc_g, (n | kk) != 0 ? 1u : 0u);
-          sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::smem_desc(sq + kk * 2048, 8192, 1024, sm100::kSwizzle128B),
-                             idesc_g, (n | kk) != 0 ? 1u : 0u);
+          sm100::mma_bf16_ts(t_dv, tp + acol, sm100::desc_adv(dod, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+          sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::desc_adv(qd, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
         }
         sm100::mma_commit(&sp_empty[b]);
         sm100::mma_commit(&st_empty[st]);
@@ -173,13 +173,15 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t sdo = sq + C::Q_TILE;
         const uint32_t tp = tbase + b * 128;
+        const uint64_t kd = sm100::smem_desc(sk, 16, 1024, sm100::kSwizzle128B);
+        const uint64_t vd = sm100::smem_desc(sv, 16, 1024, sm100::kSwizzle128B);
+        const uint64_t qd = sm100::smem_desc(sq, 16, 1024, sm100::kSwizzle128B);
+        const uint64_t dod = sm100::smem_desc(sdo, 16, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-          sm100::mma_bf16_ss(tp, sm100::smem_desc(sk + oa, 16, 1024, sm100::kSwizzle128B),
-                             sm100::smem_desc(sq + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
-          sm100::mma_bf16_ss(tp + 64, sm100::smem_desc(sv + oa, 16, 1024, sm100::kSwizzle128B),
-                             sm100::smem_desc(sdo + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
+          sm100::mma_bf16_ss(tp, sm100::desc_adv(kd, oa), sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
+          sm100::mma_bf16_ss(tp + 64, sm100::desc_adv(vd, oa), sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
         }
         sm100::mma_commit(&sp_full[b]);
         if (n > 0) issue_grad(n - 1);
@@ -359,11 +361,11 @@ __global__ void __launch_bounds__(384, 1)
         sm100::tc_fence_after();
         const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t tp = tbase + b * 128;
+        const uint64_t kjd = sm100::smem_desc(skj, 8192, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
-          sm100::mma_bf16_ts(t_dq, tp + acol, sm100::smem_desc(skj + kk * 2048, 8192, 1024, sm100::kSwizzle128B),
-                             idesc_g, (j | kk) != 0 ? 1u : 0u);
+          sm100::mma_bf16_ts(t_dq, tp + acol, sm100::desc_adv(kjd, kk * 2048), idesc_g, (j | kk) != 0 ? 1u : 0u);
         }
         sm100::mma_commit(&sp_empty[b]);
         sm100::mma_commit(&st_empty[st]);
@@ -378,13 +380,15 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t svj = skj + C::KV_TILE;
         const uint32_t tp = tbase + b * 128;
+        const uint64_t qd = sm100::smem_desc(sq, 16, 1024, sm100::kSwizzle128B);
+        const uint64_t dod = sm100::smem_desc(sdo, 16, 1024, sm100::kSwizzle128B);
+        const uint64_t kjd = sm100::smem_desc(skj, 16, 1024, sm100::kSwizzle128B);
+        const uint64_t vjd = sm100::smem_desc(svj, 16, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-          sm100::mma_bf16_ss(tp, sm100::smem_desc(sq + oa, 16, 1024, sm100::kSwizzle128B),
-                             sm100::smem_desc(skj + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
-          sm100::mma_bf16_ss(tp + 64, sm100::smem_desc(sdo + oa, 16, 1024, sm100::kSwizzle128B),
-                             sm100::smem_desc(svj + ob, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
+          sm100::mma_bf16_ss(tp, sm100::desc_adv(qd, oa), sm100::desc_adv(kjd, ob), idesc_s, kk != 0 ? 1u : 0u);
+          sm100::mma_bf16_ss(tp + 64, sm100::desc_adv(dod, oa), sm100::desc_adv(vjd, ob), idesc_s, kk != 0 ? 1u : 0u);
         }
         sm100::mma_commit(&sp_full[b]);
         if (j > 0) issue_dq(j - 1);

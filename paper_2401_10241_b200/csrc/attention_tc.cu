@@ -144,11 +144,13 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       const uint32_t sq = sm100::smem_addr(smem + C::OFF_Q);
       auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
         const uint32_t sk = sm100::smem_addr(smem + C::OFF_K + (j & 1) * C::TILE);
+        const uint64_t qd = sm100::smem_desc(sq + t * C::TILE, 16, 1024, sm100::kSwizzle128B);
+        const uint64_t kd = sm100::smem_desc(sk, 16, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          sm100::mma_bf16_ss(tbase + t * 128, sm100::smem_desc(sq + t * C::TILE + off, 16, 1024, sm100::kSwizzle128B),
-                             sm100::smem_desc(sk + off, 16, 1024, sm100::kSwizzle128B), idesc_s, kk != 0 ? 1u : 0u);
+          sm100::mma_bf16_ss(tbase + t * 128, sm100::desc_adv(qd, off), sm100::desc_adv(kd, off), idesc_s,
+                             kk != 0 ? 1u : 0u);
         }
         sm100::mma_commit(&s_full[t]);
       };
@@ -156,9 +158,10 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         sm100::mbar_wait(&p_full[t], j & 1);
         sm100::tc_fence_after();
         const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + (j & 1) * C::TILE);
+        const uint64_t vd = sm100::smem_desc(sv, 16384, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t bd = sm100::smem_desc(sv + kk * 2048, 16384, 1024, sm100::kSwizzle128B);
+          const uint64_t bd = sm100::desc_adv(vd, kk * 2048);
           sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
         }
       };

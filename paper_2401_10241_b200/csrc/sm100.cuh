@@ -267,6 +267,10 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 constexpr uint32_t kSwizzle128B = 2;
+// a descriptor advanced by `bytes` (16-byte units in the start-address field; the field
+// cannot carry out for shared-memory addresses < 256 KB): lets an unrolled MMA loop build
+// its descriptors with one add each instead of re-packing every field
+__device__ __forceinline__ uint64_t desc_adv(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
 
 // Instruction descriptor, kind::f16: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16
 // [10,13)=1, A major [15], B major [16] (1 = MN-major), N>>3 [17,23), M>>4 [24,29).
