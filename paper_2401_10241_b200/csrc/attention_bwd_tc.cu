@@ -2,7 +2,8 @@
 // one kernel owns dK / dV of a 128-key block, another owns dQ of a 128-query block.
 //
 // dK/dV kernel (per key block kb, loop over 64-query blocks i >= 2 kb):
-//   MMA   S^T = K Q_i^T, dP^T = V dO_i^T             (SS, M = 128 keys, N = 64 queries)
+//   MMA   S^T = K Q_i^T, dP^T = V dO_i^T             (M = 128 keys, N = 64 queries; K (and V
+//         when the TMEM columns allow, d <= 64) copied once into TMEM: TS, else SS)
 //   warps 4-11 (key row per thread pair, one query half each):
 //         P^T = exp2(S^T c - lse_q log2 e) (causal), dS^T = P^T (dP^T - D_q),
 //         both written back as bf16 into TMEM over their own S^T / dP^T columns
@@ -10,7 +11,8 @@
 //   S^T / dP^T are double-buffered (2 x 128 columns) so block i+1's products overlap
 //   block i's elementwise work; dK, dV accumulate in TMEM (2 x D columns).
 // dQ kernel (per query block, loop over 64-key blocks j <= 2 qb + 1):
-//   MMA   S = Q K_j^T, dP = dO V_j^T;  dS = P (dP - D) -> TMEM;  dQ += dS K_j (TS).
+//   MMA   S = Q K_j^T, dP = dO V_j^T (TS: Q, dO copied once into TMEM);
+//         dS = P (dP - D) -> TMEM;  dQ += dS K_j (TS).
 // Q, dO, L, D of a query block arrive by TMA / bulk copy in a 3-stage ring.
 #include <math.h>
 
@@ -25,7 +27,7 @@ constexpr float LOG2E = 1.4426950408889634f;
 
 #ifdef ZB_ATTN_TRACE
 // timeline of one CTA (blockIdx (TR_BX, 0, 0)) of k_dkdv_tc, globaltimer ns (measurement build only)
-__device__ unsigned long long g_trace[8][64];
+__device__ unsigned long long g_trace[12][64];
 #ifndef TR_BX
 #define TR_BX 0
 #endif
@@ -46,8 +48,38 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Row r (0..127) of a 128-row SWIZZLE_128B bf16 tile (D columns in 64-column atoms 16 KB apart,
+// 16-byte chunk c of row r stored at chunk c ^ (r & 7)) into TMEM lane r, columns
+// [taddr, taddr + D/2) as packed bf16 pairs (low half = even column): the A-operand layout of a
+// TS tcgen05.mma, so a CTA-constant A tile is read from TMEM by every product instead of from
+// shared memory (an SS product streams A AND B through the shared-memory port; the A read is
+// what bounds the small-N products of these kernels).  Warp-collective: the calling warp
+// (warp % 4 == r / 32) owns TMEM lanes 32 (warp % 4) ..; taddr carries that lane offset.
+template <int D>
+__device__ __forceinline__ void tile_row_to_tmem(const uint8_t* tile, int r, uint32_t taddr) {
+  static_assert(D % 32 == 0, "head dim");
+#pragma unroll
+  for (int g = 0; g < D / 32; ++g) {
+    uint32_t w[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int gc = g * 4 + c;
+      const uint4 u = *reinterpret_cast<const uint4*>(tile + (gc >> 3) * 16384 + r * 128 + (((gc & 7) ^ (r & 7)) << 4));
+      w[4 * c] = u.x;
+      w[4 * c + 1] = u.y;
+      w[4 * c + 2] = u.z;
+      w[4 * c + 3] = u.w;
+    }
+    sm100::tmem_st16(taddr + g * 16, w);
+  }
+}
+
 // ================================================================== dK / dV
 template <int D> struct DkdvCfg {
+  // TMEM: S^T / dP^T x 2 buffers (256 columns), dK, dV (D each), then the CTA-constant A
+  // operands K (and V) as packed bf16 (D/2 each) where the 512 columns allow it
+  static constexpr bool KT = 256 + 2 * D + D / 2 <= 512;
+  static constexpr bool VT = 256 + 2 * D + D <= 512;
   static constexpr int ATOMS = (D + 63) / 64;
   static constexpr int KV_TILE = ATOMS * 16384;  // 128 rows
   static constexpr int Q_TILE = ATOMS * 8192;    // 64 rows
@@ -77,8 +109,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* sp_empty = sp_full + 2;            // [2]
   uint64_t* ds_full = sp_empty + 2;            // [2]
   uint64_t* o_final = ds_full + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_final + 1);
-  static_assert((1 + 2 * C::ST + 7) * 8 + 4 <= 256, "barrier area");
+  uint64_t* at_full = o_final + 1;  // K (V) resident in TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(at_full + 1);
+  static_assert((1 + 2 * C::ST + 8) * 8 + 4 <= 256, "barrier area");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x, hd = blockIdx.y, bb = blockIdx.z;
@@ -100,6 +133,10 @@ __global__ void __launch_bounds__(384, 1)
       sm100::mbar_init(&ds_full[i], 256);
     }
     sm100::mbar_init(o_final, 1);
+    sm100::mbar_init(at_full, 256);
+#ifdef ZB_ATTN_TRACE
+    sm100::mbar_init(bar + 20, 1);
+#endif
     sm100::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -115,6 +152,7 @@ __global__ void __launch_bounds__(384, 1)
   pdl_wait();
   const uint32_t tbase = *tslot;
   const uint32_t t_dk = tbase + 256, t_dv = tbase + 256 + D;
+  const uint32_t t_kt = tbase + 256 + 2 * D, t_vt = t_kt + D / 2;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA / bulk copies
@@ -138,13 +176,13 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA
+    {  // ---------------- MMA
       constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 64, false, false);
       constexpr uint32_t idesc_g = sm100::idesc_bf16(128, D, false, true);
       const uint32_t sk = sm100::smem_addr(smem + C::OFF_K), sv = sm100::smem_addr(smem + C::OFF_V);
       auto issue_grad = [&](int n) {
         const int b = n & 1, st = n % C::ST;
-        sm100::mbar_wait(&ds_full[b], (n >> 1) & 1);
+        sm100::mbar_wait_warp(&ds_full[b], (n >> 1) & 1);
         TR(3, n);
         sm100::tc_fence_after();
         const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
@@ -155,19 +193,29 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries: halves live at columns [0,16) and [32,48)
           const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
-          sm100::mma_bf16_ts(t_dv, tp + acol, sm100::desc_adv(dod, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
-          sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::desc_adv(qd, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+          if (sm100::elect_one()) {
+            sm100::mma_bf16_ts(t_dv, tp + acol, sm100::desc_adv(dod, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+            sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::desc_adv(qd, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+          }
         }
-        sm100::mma_commit(&sp_empty[b]);
-        sm100::mma_commit(&st_empty[st]);
-        if (n == nq - 1) sm100::mma_commit(o_final);
+        TR(10, n);
+        if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
+        if (sm100::elect_one()) sm100::mma_commit(&st_empty[st]);
+#ifdef ZB_ATTN_TRACE
+        if (sm100::elect_one()) sm100::mma_commit(bar + 20);
+#endif
+        if (n == nq - 1) { if (sm100::elect_one()) sm100::mma_commit(o_final); }
       };
-      sm100::mbar_wait(kv_full, 0);
+      sm100::mbar_wait_warp(kv_full, 0);
+      if constexpr (C::KT) {
+        sm100::mbar_wait_warp(at_full, 0);
+        sm100::tc_fence_after();
+      }
       for (int n = 0; n < nq; ++n) {
         const int b = n & 1, st = n % C::ST;
-        sm100::mbar_wait(&st_full[st], (n / C::ST) & 1);
+        sm100::mbar_wait_warp(&st_full[st], (n / C::ST) & 1);
         TR(1, n);
-        sm100::mbar_wait(&sp_empty[b], ((n >> 1) & 1) ^ 1);
+        sm100::mbar_wait_warp(&sp_empty[b], ((n >> 1) & 1) ^ 1);
         TR(2, n);
         sm100::tc_fence_after();
         const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
@@ -180,23 +228,46 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-          sm100::mma_bf16_ss(tp, sm100::desc_adv(kd, oa), sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
-          sm100::mma_bf16_ss(tp + 64, sm100::desc_adv(vd, oa), sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
+          if (sm100::elect_one()) {
+            if constexpr (C::KT)
+              sm100::mma_bf16_ts(tp, t_kt + kk * 8, sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
+            else
+              sm100::mma_bf16_ss(tp, sm100::desc_adv(kd, oa), sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
+            if constexpr (C::VT)
+              sm100::mma_bf16_ts(tp + 64, t_vt + kk * 8, sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
+            else
+              sm100::mma_bf16_ss(tp + 64, sm100::desc_adv(vd, oa), sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
+          }
         }
-        sm100::mma_commit(&sp_full[b]);
+        TR(11, n);
+        if (sm100::elect_one()) sm100::mma_commit(&sp_full[b]);
         if (n > 0) issue_grad(n - 1);
       }
       issue_grad(nq - 1);
     }
+#ifdef ZB_ATTN_TRACE
+  } else if (warp == 3) {  // trace observer: completion of each step's dV / dK products
+    if (lane == 0)
+      for (int n = 0; n < nq; ++n) {
+        sm100::mbar_wait(bar + 20, n & 1);
+        TR(9, n);
+      }
+#endif
   } else if (warp >= 4) {  // ---------------- elementwise: P^T, dS^T
     const int qw = warp & 3, hf = (warp - 4) >> 2;
     const int r = qw * 32 + lane;
     const int key = kb * 128 + r;
     const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    if constexpr (C::KT) {
+      sm100::mbar_wait(kv_full, 0);
+      if (hf == 0) tile_row_to_tmem<D>(smem + C::OFF_K, r, t_kt + lane_off);
+      if (C::VT && hf == 1) tile_row_to_tmem<D>(smem + C::OFF_V, r, t_vt + lane_off);
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(at_full);
+    }
     for (int n = 0; n < nq; ++n) {
       const int i = i0 + n, b = n & 1, st = n % C::ST;
-      const float* Ls = reinterpret_cast<const float*>(smem + C::OFF_ST + st * C::STAGE + 2 * C::Q_TILE);
-      const float* Ds = Ls + 64;
       sm100::mbar_wait(&sp_full[b], (n >> 1) & 1);
       if (warp == 4 && lane == 0) TR(4, n);
       sm100::tc_fence_after();
@@ -205,21 +276,41 @@ __global__ void __launch_bounds__(384, 1)
       sm100::tmem_ld32(tp + 32 * hf, sr);
       sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
       sm100::tmem_ld_wait();
+      // this half's 32 L_q and D_q (warp-uniform: broadcast loads), L in log2 units
+      float nl[32], dd[32];
+      {
+        const uint32_t sl = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE + 2 * C::Q_TILE) + 128 * hf;
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const float4 l4 = sm100::lds128(sl + 4 * c), d4 = sm100::lds128(sl + 256 + 4 * c);
+          nl[c] = -l4.x * LOG2E, nl[c + 1] = -l4.y * LOG2E, nl[c + 2] = -l4.z * LOG2E, nl[c + 3] = -l4.w * LOG2E;
+          dd[c] = d4.x, dd[c + 1] = d4.y, dd[c + 2] = d4.z, dd[c + 3] = d4.w;
+        }
+      }
+      if (warp == 4 && lane == 0) TR(7, n);
+      // queries of this half: i*64 + 32 hf + c; the causal mask (q >= key) only bites on blocks
+      // that reach below the diagonal of this key block
+      const int qlo = i * 64 + 32 * hf;
+      const bool diag = qlo < kb * 128 + 128;
       uint32_t pk[16], dk[16];
 #pragma unroll
       for (int c = 0; c < 32; c += 2) {
         float pv[2], dv[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int qc = 32 * hf + c + e;
-          const int q = i * 64 + qc;
-          const float p = q >= key ? sm100::ex2(__uint_as_float(sr[c + e]) * scale_log2 - Ls[qc] * LOG2E) : 0.f;
+#ifdef ZB_TRACE_NOEXP
+          float p = fmaf(__uint_as_float(sr[c + e]), scale_log2, nl[c + e]);
+#else
+          float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, nl[c + e]));
+#endif
+          if (diag && qlo + c + e < key) p = 0.f;
           pv[e] = p;
-          dv[e] = p * (__uint_as_float(dr[c + e]) - Ds[qc]);
+          dv[e] = p * (__uint_as_float(dr[c + e]) - dd[c + e]);
         }
         pk[c >> 1] = pack_bf16(pv[0], pv[1]);
         dk[c >> 1] = pack_bf16(dv[0], dv[1]);
       }
+      if (warp == 4 && lane == 0) TR(8, n);
       sm100::tmem_st16(tp + 32 * hf, pk);       // P^T over this half's S^T columns
       sm100::tmem_st16(tp + 64 + 32 * hf, dk);  // dS^T over this half's dP^T columns
       sm100::tmem_st_wait();
@@ -292,8 +383,10 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* sp_empty = sp_full + 2;            // [2]
   uint64_t* ds_full = sp_empty + 2;            // [2]
   uint64_t* o_final = ds_full + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_final + 1);
-  static_assert((1 + 2 * C::ST + 7) * 8 + 4 <= 256, "barrier area");
+  uint64_t* at_full = o_final + 1;  // Q, dO resident in TMEM
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(at_full + 1);
+  static_assert((1 + 2 * C::ST + 8) * 8 + 4 <= 256, "barrier area");
+  static_assert(256 + 2 * D <= 512, "TMEM: S/dP x 2, dQ, Q and dO as packed bf16");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / 128;
@@ -315,6 +408,7 @@ __global__ void __launch_bounds__(384, 1)
       sm100::mbar_init(&ds_full[i], 256);
     }
     sm100::mbar_init(o_final, 1);
+    sm100::mbar_init(at_full, 256);
     sm100::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -330,6 +424,7 @@ __global__ void __launch_bounds__(384, 1)
   pdl_wait();
   const uint32_t tbase = *tslot;
   const uint32_t t_dq = tbase + 256;
+  const uint32_t t_qt = tbase + 256 + D, t_dot = t_qt + D / 2;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA
@@ -351,13 +446,12 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA
+    {  // ---------------- MMA
       constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 64, false, false);
       constexpr uint32_t idesc_g = sm100::idesc_bf16(128, D, false, true);
-      const uint32_t sq = sm100::smem_addr(smem + C::OFF_Q), sdo = sm100::smem_addr(smem + C::OFF_DO);
       auto issue_dq = [&](int j) {
         const int b = j & 1, st = j % C::ST;
-        sm100::mbar_wait(&ds_full[b], (j >> 1) & 1);
+        sm100::mbar_wait_warp(&ds_full[b], (j >> 1) & 1);
         sm100::tc_fence_after();
         const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t tp = tbase + b * 128;
@@ -365,32 +459,33 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
-          sm100::mma_bf16_ts(t_dq, tp + acol, sm100::desc_adv(kjd, kk * 2048), idesc_g, (j | kk) != 0 ? 1u : 0u);
+          if (sm100::elect_one()) sm100::mma_bf16_ts(t_dq, tp + acol, sm100::desc_adv(kjd, kk * 2048), idesc_g, (j | kk) != 0 ? 1u : 0u);
         }
-        sm100::mma_commit(&sp_empty[b]);
-        sm100::mma_commit(&st_empty[st]);
-        if (j == nkv - 1) sm100::mma_commit(o_final);
+        if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
+        if (sm100::elect_one()) sm100::mma_commit(&st_empty[st]);
+        if (j == nkv - 1) { if (sm100::elect_one()) sm100::mma_commit(o_final); }
       };
-      sm100::mbar_wait(q_full, 0);
+      sm100::mbar_wait_warp(at_full, 0);
+      sm100::tc_fence_after();
       for (int j = 0; j < nkv; ++j) {
         const int b = j & 1, st = j % C::ST;
-        sm100::mbar_wait(&st_full[st], (j / C::ST) & 1);
-        sm100::mbar_wait(&sp_empty[b], ((j >> 1) & 1) ^ 1);
+        sm100::mbar_wait_warp(&st_full[st], (j / C::ST) & 1);
+        sm100::mbar_wait_warp(&sp_empty[b], ((j >> 1) & 1) ^ 1);
         sm100::tc_fence_after();
         const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t svj = skj + C::KV_TILE;
         const uint32_t tp = tbase + b * 128;
-        const uint64_t qd = sm100::smem_desc(sq, 16, 1024, sm100::kSwizzle128B);
-        const uint64_t dod = sm100::smem_desc(sdo, 16, 1024, sm100::kSwizzle128B);
         const uint64_t kjd = sm100::smem_desc(skj, 16, 1024, sm100::kSwizzle128B);
         const uint64_t vjd = sm100::smem_desc(svj, 16, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-          sm100::mma_bf16_ss(tp, sm100::desc_adv(qd, oa), sm100::desc_adv(kjd, ob), idesc_s, kk != 0 ? 1u : 0u);
-          sm100::mma_bf16_ss(tp + 64, sm100::desc_adv(dod, oa), sm100::desc_adv(vjd, ob), idesc_s, kk != 0 ? 1u : 0u);
+          const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+          if (sm100::elect_one()) {
+            sm100::mma_bf16_ts(tp, t_qt + kk * 8, sm100::desc_adv(kjd, ob), idesc_s, kk != 0 ? 1u : 0u);
+            sm100::mma_bf16_ts(tp + 64, t_dot + kk * 8, sm100::desc_adv(vjd, ob), idesc_s, kk != 0 ? 1u : 0u);
+          }
         }
-        sm100::mma_commit(&sp_full[b]);
+        if (sm100::elect_one()) sm100::mma_commit(&sp_full[b]);
         if (j > 0) issue_dq(j - 1);
       }
       issue_dq(nkv - 1);
@@ -402,6 +497,11 @@ __global__ void __launch_bounds__(384, 1)
     const int64_t si = (static_cast<int64_t>(bb) * a + hd) * s + q;
     const float L2 = lse[si] * LOG2E, Dq = delta[si];
     const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    sm100::mbar_wait(q_full, 0);
+    tile_row_to_tmem<D>(smem + (hf == 0 ? C::OFF_Q : C::OFF_DO), r, (hf == 0 ? t_qt : t_dot) + lane_off);
+    sm100::tmem_st_wait();
+    sm100::tc_fence_before();
+    sm100::mbar_arrive(at_full);
     for (int j = 0; j < nkv; ++j) {
       const int b = j & 1;
       sm100::mbar_wait(&sp_full[b], (j >> 1) & 1);
@@ -496,6 +596,6 @@ bool attention_bwd_tc(const AttnShape& sh, const void* qkv, const void* dout, co
 
 #ifdef ZB_ATTN_TRACE
 extern "C" int zb_dbg_attn_trace(unsigned long long* host) {
-  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_bwd_tc::g_trace, sizeof(unsigned long long) * 8 * 64));
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_bwd_tc::g_trace, sizeof(unsigned long long) * 12 * 64));
 }
 #endif

@@ -21,6 +21,21 @@
 namespace zb {
 namespace attn_tc {
 
+#ifdef ZB_ATTN_TRACE
+// timeline of CTA (0, 0, 0) (the heaviest query-tile pair), globaltimer ns (measurement build only)
+__device__ unsigned long long g_trace_fwd[8][64];
+__device__ __forceinline__ void trf(int row, int n) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && n < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace_fwd[row][n] = t;
+  }
+}
+#define TRF(row, n) trf(row, n)
+#else
+#define TRF(row, n)
+#endif
+
 constexpr int BQ = 128, BKV = 128;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
@@ -138,7 +153,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA
+    {  // ---------------- MMA
       constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = sm100::idesc_bf16(128, D, false, true);
       const uint32_t sq = sm100::smem_addr(smem + C::OFF_Q);
@@ -149,45 +164,46 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          sm100::mma_bf16_ss(tbase + t * 128, sm100::desc_adv(qd, off), sm100::desc_adv(kd, off), idesc_s,
+          if (sm100::elect_one()) sm100::mma_bf16_ss(tbase + t * 128, sm100::desc_adv(qd, off), sm100::desc_adv(kd, off), idesc_s,
                              kk != 0 ? 1u : 0u);
         }
-        sm100::mma_commit(&s_full[t]);
+        if (sm100::elect_one()) sm100::mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
-        sm100::mbar_wait(&p_full[t], j & 1);
+        sm100::mbar_wait_warp(&p_full[t], j & 1);
+        TRF(t, j);
         sm100::tc_fence_after();
         const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + (j & 1) * C::TILE);
         const uint64_t vd = sm100::smem_desc(sv, 16384, 1024, sm100::kSwizzle128B);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
           const uint64_t bd = sm100::desc_adv(vd, kk * 2048);
-          sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+          if (sm100::elect_one()) sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
         }
       };
-      sm100::mbar_wait(q_full, 0);
-      sm100::mbar_wait(&k_full[0], 0);
+      sm100::mbar_wait_warp(q_full, 0);
+      sm100::mbar_wait_warp(&k_full[0], 0);
       sm100::tc_fence_after();
       issue_s(0, 0);
       if (two) issue_s(1, 0);
-      sm100::mma_commit(&k_empty[0]);
+      if (sm100::elect_one()) sm100::mma_commit(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
         const bool more = j + 1 < nkv;
-        sm100::mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-        if (more) sm100::mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        sm100::mbar_wait_warp(&v_full[j & 1], (j >> 1) & 1);
+        if (more) sm100::mbar_wait_warp(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
         sm100::tc_fence_after();
         if (j < nkv0) {
           issue_pv(0, j);
-          if (j == nkv0 - 1) sm100::mma_commit(&o_final[0]);
+          if (j == nkv0 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[0]); }
         }
         if (j + 1 < nkv0) issue_s(0, j + 1);
         if (j < nkv1) {
           issue_pv(1, j);
-          if (j == nkv1 - 1) sm100::mma_commit(&o_final[1]);
+          if (j == nkv1 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[1]); }
         }
-        sm100::mma_commit(&v_empty[j & 1]);
+        if (sm100::elect_one()) sm100::mma_commit(&v_empty[j & 1]);
         if (j + 1 < nkv1) issue_s(1, j + 1);
-        if (more) sm100::mma_commit(&k_empty[(j + 1) & 1]);
+        if (more) { if (sm100::elect_one()) sm100::mma_commit(&k_empty[(j + 1) & 1]); }
       }
     }
   } else if (warp >= 4) {  // ---------------- softmax: 4 warps per tile, one row per thread
@@ -200,11 +216,13 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
     float m = -INFINITY, l = 0.f;  // m: reference max (log2 units), l: running sum relative to m
     for (int j = 0; j < nk; ++j) {
       sm100::mbar_wait(&s_full[t], j & 1);
+      if ((warp & 3) == 0 && lane == 0) TRF(2 + 3 * t, j);
       sm100::tc_fence_after();
       float sv[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) sm100::tmem_ld32(t_s + c * 32, reinterpret_cast<uint32_t*>(sv + 32 * c));
       sm100::tmem_ld_wait();
+      if ((warp & 3) == 0 && lane == 0) TRF(3 + 3 * t, j);
       if (j == qt) {
 #pragma unroll
         for (int k = 0; k < 128; ++k)
@@ -269,6 +287,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
+      if ((warp & 3) == 0 && lane == 0) TRF(4 + 3 * t, j);
       sm100::mbar_arrive(&p_full[t]);
     }
     if (nk > 0) {
@@ -336,3 +355,9 @@ bool attention_fwd_tc(const AttnShape& sh, const void* qkv, void* o, float* lse,
 }
 
 }  // namespace zb
+
+#ifdef ZB_ATTN_TRACE
+extern "C" int zb_dbg_attn_fwd_trace(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_trace_fwd, sizeof(unsigned long long) * 8 * 64));
+}
+#endif
