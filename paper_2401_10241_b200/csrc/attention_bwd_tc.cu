@@ -16,6 +16,8 @@
 // Q, dO, L, D of a query block arrive by TMA / bulk copy in a 3-stage ring.
 #include <math.h>
 
+#include <type_traits>
+
 #include "attention.h"
 #include "gemm.h"
 #include "sm100.cuh"
@@ -293,23 +295,28 @@ __global__ void __launch_bounds__(384, 1)
       const int qlo = i * 64 + 32 * hf;
       const bool diag = qlo < kb * 128 + 128;
       uint32_t pk[16], dk[16];
+      // the mask test only on the (warp-uniform) diagonal steps: off the diagonal the
+      // compare / select / index arithmetic was a third of the loop's instructions
+      auto elementwise = [&](auto masked) {
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        float pv[2], dv[2];
+        for (int c = 0; c < 32; c += 2) {
+          float pv[2], dv[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-#ifdef ZB_TRACE_NOEXP
-          float p = fmaf(__uint_as_float(sr[c + e]), scale_log2, nl[c + e]);
-#else
-          float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, nl[c + e]));
-#endif
-          if (diag && qlo + c + e < key) p = 0.f;
-          pv[e] = p;
-          dv[e] = p * (__uint_as_float(dr[c + e]) - dd[c + e]);
+          for (int e = 0; e < 2; ++e) {
+            float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, nl[c + e]));
+            if constexpr (decltype(masked)::value)
+              if (qlo + c + e < key) p = 0.f;
+            pv[e] = p;
+            dv[e] = p * (__uint_as_float(dr[c + e]) - dd[c + e]);
+          }
+          pk[c >> 1] = pack_bf16(pv[0], pv[1]);
+          dk[c >> 1] = pack_bf16(dv[0], dv[1]);
         }
-        pk[c >> 1] = pack_bf16(pv[0], pv[1]);
-        dk[c >> 1] = pack_bf16(dv[0], dv[1]);
-      }
+      };
+      if (diag)
+        elementwise(std::true_type{});
+      else
+        elementwise(std::false_type{});
       if (warp == 4 && lane == 0) TR(8, n);
       sm100::tmem_st16(tp + 32 * hf, pk);       // P^T over this half's S^T columns
       sm100::tmem_st16(tp + 64 + 32 * hf, dk);  // dS^T over this half's dP^T columns
@@ -512,17 +519,26 @@ __global__ void __launch_bounds__(384, 1)
       sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
       sm100::tmem_ld_wait();
       uint32_t dk[16];
+      const int klo = j * 64 + 32 * hf;
+      auto elementwise = [&](auto masked) {
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        float dv[2];
+        for (int c = 0; c < 32; c += 2) {
+          float dv[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int key = j * 64 + 32 * hf + c + e;
-          const float p = key <= q ? sm100::ex2(__uint_as_float(sr[c + e]) * scale_log2 - L2) : 0.f;
-          dv[e] = p * (__uint_as_float(dr[c + e]) - Dq);
+          for (int e = 0; e < 2; ++e) {
+            float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, -L2));
+            if constexpr (decltype(masked)::value)
+              if (klo + c + e > q) p = 0.f;
+            dv[e] = p * (__uint_as_float(dr[c + e]) - Dq);
+          }
+          dk[c >> 1] = pack_bf16(dv[0], dv[1]);
         }
-        dk[c >> 1] = pack_bf16(dv[0], dv[1]);
-      }
+      };
+      // keys of this half reach above the warp's first query only near the diagonal
+      if (klo + 31 > qb * 128 + qw * 32)
+        elementwise(std::true_type{});
+      else
+        elementwise(std::false_type{});
       sm100::tmem_st16(tp + 32 * hf, dk);  // dS over this half's S columns
       sm100::tmem_st_wait();
       sm100::tc_fence_before();

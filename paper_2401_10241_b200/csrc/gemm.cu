@@ -293,34 +293,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (whole warp, one elected lane issues)
       constexpr uint32_t idesc = sm100::idesc_bf16(BM, BN, A_MN, B_MN);
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        sm100::mbar_wait(&tempty[acc], aph ^ 1);
+        sm100::mbar_wait_warp(&tempty[acc], aph ^ 1);
         sm100::tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         for (int kb = 0; kb < nk; ++kb) {
-          sm100::mbar_wait(&full[stage], ph);
+          sm100::mbar_wait_warp(&full[stage], ph);
           sm100::tc_fence_after();
           const uint32_t sa = sm100::smem_addr(smem + stage * C::STAGE);
           const uint32_t sb = sa + A_BYTES;
+          const uint64_t ad0 = A_MN ? sm100::smem_desc(sa, 8192, 1024, sm100::kSwizzle128B)
+                                    : sm100::smem_desc(sa, 16, 1024, sm100::kSwizzle128B);
+          const uint64_t bd0 = B_MN ? sm100::smem_desc(sb, 8192, 1024, sm100::kSwizzle128B)
+                                    : sm100::smem_desc(sb, 16, 1024, sm100::kSwizzle128B);
+          if (sm100::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = A_MN ? sm100::smem_desc(sa + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
-                                     : sm100::smem_desc(sa + kk * 32, 16, 1024, sm100::kSwizzle128B);
-            const uint64_t bd = B_MN ? sm100::smem_desc(sb + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
-                                     : sm100::smem_desc(sb + kk * 32, 16, 1024, sm100::kSwizzle128B);
-            sm100::mma_bf16_ss(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk)
+              sm100::mma_bf16_ss(d, sm100::desc_adv(ad0, A_MN ? kk * 2048 : kk * 32),
+                                 sm100::desc_adv(bd0, B_MN ? kk * 2048 : kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
+            sm100::mma_commit(&empty[stage]);
           }
-          sm100::mma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == C::STAGES) {
             stage = 0;
             ph ^= 1;
           }
         }
-        sm100::mma_commit(&tfull[acc]);
+        if (sm100::elect_one()) sm100::mma_commit(&tfull[acc]);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
@@ -470,35 +474,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
+    if (leader) {  // ---------------- MMA issuer (leader only; whole warp, one elected lane issues)
       constexpr uint32_t idesc = sm100::idesc_bf16(BM2, BN, A_MN, B_MN);
       int stage = 0, acc = 0;
       uint32_t ph = 0, aph = 0;
       for (int t = cid; t < items; t += ncl) {
-        sm100::mbar_wait(&tempty[acc], aph ^ 1);
+        sm100::mbar_wait_warp(&tempty[acc], aph ^ 1);
         sm100::tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         const int kb0 = kb_begin(t / tiles);
         for (int kb = kb0; kb < kb_begin(t / tiles + 1); ++kb) {
-          sm100::mbar_wait(&full[stage], ph);
+          sm100::mbar_wait_warp(&full[stage], ph);
           sm100::tc_fence_after();
           const uint32_t sa = sm100::smem_addr(smem + stage * C::STAGE);
           const uint32_t sb = sa + A_BYTES;
+          const uint64_t ad0 = A_MN ? sm100::smem_desc(sa, 8192, 1024, sm100::kSwizzle128B)
+                                    : sm100::smem_desc(sa, 16, 1024, sm100::kSwizzle128B);
+          const uint64_t bd0 = B_MN ? sm100::smem_desc(sb, 8192, 1024, sm100::kSwizzle128B)
+                                    : sm100::smem_desc(sb, 16, 1024, sm100::kSwizzle128B);
+          if (sm100::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = A_MN ? sm100::smem_desc(sa + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
-                                     : sm100::smem_desc(sa + kk * 32, 16, 1024, sm100::kSwizzle128B);
-            const uint64_t bd = B_MN ? sm100::smem_desc(sb + kk * 2048, 8192, 1024, sm100::kSwizzle128B)
-                                     : sm100::smem_desc(sb + kk * 32, 16, 1024, sm100::kSwizzle128B);
-            sm100::mma_bf16_ss_pair(d, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk)
+              sm100::mma_bf16_ss_pair(d, sm100::desc_adv(ad0, A_MN ? kk * 2048 : kk * 32),
+                                      sm100::desc_adv(bd0, B_MN ? kk * 2048 : kk * 32), idesc,
+                                      (kb != kb0 || kk != 0) ? 1u : 0u);
+            sm100::mma_commit_pair(&empty[stage], 0x3);
           }
-          sm100::mma_commit_pair(&empty[stage], 0x3);
+          __syncwarp();
           if (++stage == C::STAGES) {
             stage = 0;
             ph ^= 1;
           }
         }
-        sm100::mma_commit_pair(&tfull[acc], 0x3);
+        if (sm100::elect_one()) sm100::mma_commit_pair(&tfull[acc], 0x3);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
