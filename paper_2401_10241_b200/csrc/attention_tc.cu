@@ -23,7 +23,7 @@ namespace attn_tc {
 
 #ifdef ZB_ATTN_TRACE
 // timeline of CTA (0, 0, 0) (the heaviest query-tile pair), globaltimer ns (measurement build only)
-__device__ unsigned long long g_trace_fwd[8][64];
+__device__ unsigned long long g_trace_fwd[12][64];
 __device__ __forceinline__ void trf(int row, int n) {
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && n < 64) {
     unsigned long long t;
@@ -51,7 +51,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-constexpr bool kPolyExp = false;  // measured slower on B200 (the softmax is not MUFU-bound here)
+constexpr bool kAlternate = false;
+constexpr bool kPolyExp = false;  // measured slower on B200 twice (75.6 -> 89 us; with the elect-style MMA issue 77.6 -> 91.6 us)
 
 template <int D> struct FwdCfg {
   static constexpr int ATOMS = (D + 63) / 64;           // 64-column TMA boxes per tile
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   uint64_t* p_full = bar + 11;    // [2] per tile
   uint64_t* o_final = bar + 13;   // [2] per tile
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 15);
+  uint64_t* tok = bar + 16;       // [2] per tile: the other tile's exponential phase is done
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / BQ;
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&p_full[i], 128);
       sm100::mbar_init(&o_final[i], 1);
+      sm100::mbar_init(&tok[i], 128);
     }
     sm100::fence_mbar_init();
   }
@@ -261,6 +264,13 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
           sm100::tmem_st_wait();
         }
       }
+      // kAlternate: the two tiles' exponential phases strictly alternate (token passing), so
+      // each runs alone on the MUFU while the other tile's PV and next S use the tensor core.
+      // Measured: no faster than free-running (the per-tile chain exp -> PV, S -> exp, not
+      // the MUFU, sets the period: scripts/attn_fwd_trace.py), so it is off.
+      const bool alt = kAlternate && two && j < nkv0;
+      if (alt) sm100::mbar_wait(&tok[t], t == 0 ? ((j & 1) ^ 1) : (j & 1));
+      if ((warp & 3) == 0 && lane == 0) TRF(8 + t, j);
       const float mneg = -m;
       const bool poly = kPolyExp && j != qt;  // masked (-inf) scores only on the diagonal block: MUFU there
       float sum4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -285,6 +295,8 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         sm100::tmem_st32(t_s + 32 * hf, pk);
       }
       l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+      if ((warp & 3) == 0 && lane == 0) TRF(10 + t, j);
+      if (alt) sm100::mbar_arrive(&tok[t ^ 1]);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       if ((warp & 3) == 0 && lane == 0) TRF(4 + 3 * t, j);
@@ -358,6 +370,6 @@ bool attention_fwd_tc(const AttnShape& sh, const void* qkv, void* o, float* lse,
 
 #ifdef ZB_ATTN_TRACE
 extern "C" int zb_dbg_attn_fwd_trace(unsigned long long* host) {
-  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_trace_fwd, sizeof(unsigned long long) * 8 * 64));
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_trace_fwd, sizeof(unsigned long long) * 12 * 64));
 }
 #endif

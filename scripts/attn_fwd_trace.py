@@ -16,13 +16,13 @@ lse = torch.zeros(b, a, s, device="cuda")
 for _ in range(3):
     api.dbg_attention_fwd(qkv, o, lse, b=b, s=s, a=a, d=d)
 torch.cuda.synchronize()
-buf = (C.c_ulonglong * (8 * 64))()
+buf = (C.c_ulonglong * (12 * 64))()
 lib.zb_dbg_attn_fwd_trace(buf)
 n = s // 128
-t0 = min(buf[r * 64 + j] for r in range(8) for j in range(n) if buf[r * 64 + j])
+t0 = min(buf[r * 64 + j] for r in range(12) for j in range(n) if buf[r * 64 + j])
 names = ["pv0_issue", "pv1_issue", "t0_s_ready", "t0_s_loaded", "t0_p_stored", "t1_s_ready", "t1_s_loaded",
-         "t1_p_stored"]
-print("blk " + " ".join(f"{x:>12s}" for x in names))
+         "t1_p_stored", "t0_exp_go", "t1_exp_go", "t0_exp_end", "t1_exp_end"]
+print("blk " + " ".join(f"{x:>11s}" for x in names))
 for j in range(n):
-    print(f"{j:3d} " + " ".join(f"{(buf[r * 64 + j] - t0) / 1e3 if buf[r * 64 + j] else float('nan'):12.2f}"
-                             for r in range(8)))
+    print(f"{j:3d} " + " ".join(f"{(buf[r * 64 + j] - t0) / 1e3 if buf[r * 64 + j] else float('nan'):11.2f}"
+                             for r in range(12)))
