@@ -1,2 +1,4 @@
-timeout 60 python scripts/attn_perf.py 2>&1 | tail -3 > gpurun_out/attn_perf_r2.jsonl; cat gpurun_out/attn_perf_r2.jsonl
-timeout 60 ./scripts/micro/mma_rate > gpurun_out/mma_rate.txt 2>&1; timeout 60 ./scripts/micro/mma_issue > gpurun_out/mma_issue.txt 2>&1; timeout 60 ./scripts/micro/ex2_rate > gpurun_out/ex2_rate.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/tests_final.log 2>&1; tail -3 gpurun_out/tests_final.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -2 gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_22l.csv python scripts/profile_step.py --layers 22 --m 1 > gpurun_out/launches.log 2>&1; echo ncu rc=$?
