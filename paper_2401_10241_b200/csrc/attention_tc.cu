@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   uint64_t* o_final = bar + 13;   // [2] per tile
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 15);
   uint64_t* tok = bar + 16;       // [2] per tile: the other tile's exponential phase is done
+  uint64_t* p_half = bar + 18;    // [2] per tile: P of keys [0, 64) stored (PV's first half may start)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / BQ;
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       sm100::mbar_init(&p_full[i], 128);
       sm100::mbar_init(&o_final[i], 1);
       sm100::mbar_init(&tok[i], 128);
+      sm100::mbar_init(&p_half[i], 128);
     }
     sm100::fence_mbar_init();
   }
@@ -172,16 +174,21 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         }
         if (sm100::elect_one()) sm100::mma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
-        sm100::mbar_wait_warp(&p_full[t], j & 1);
-        TRF(t, j);
-        sm100::tc_fence_after();
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j, the first 64 keys as soon as their P is stored
         const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + (j & 1) * C::TILE);
         const uint64_t vd = sm100::smem_desc(sv, 16384, 1024, sm100::kSwizzle128B);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint64_t bd = sm100::desc_adv(vd, kk * 2048);
-          if (sm100::elect_one()) sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, bd, idesc_o, (j | kk) != 0 ? 1u : 0u);
+        for (int hf = 0; hf < 2; ++hf) {
+          sm100::mbar_wait_warp(hf == 0 ? &p_half[t] : &p_full[t], j & 1);
+          if (hf == 1) TRF(t, j);
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) {
+#pragma unroll
+            for (int kk = 4 * hf; kk < 4 * hf + 4; ++kk)
+              sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, sm100::desc_adv(vd, kk * 2048),
+                                 idesc_o, (j | kk) != 0 ? 1u : 0u);
+          }
+          __syncwarp();
         }
       };
       sm100::mbar_wait_warp(q_full, 0);
@@ -293,6 +300,11 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
           pk[k >> 1] = *reinterpret_cast<uint32_t*>(&v2);
         }
         sm100::tmem_st32(t_s + 32 * hf, pk);
+        if (hf == 0) {  // publish P of keys [0, 64): PV's first half overlaps the second half here
+          sm100::tmem_st_wait();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&p_half[t]);
+        }
       }
       l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       if ((warp & 3) == 0 && lane == 0) TRF(10 + t, j);
