@@ -52,6 +52,12 @@ __device__ __forceinline__ float ex2_poly(float x) {
 }
 
 constexpr bool kAlternate = false;
+// P of a key block is published to the MMA warp in PQ parts (2: halves of 64 keys, 4: quarters
+// of 32) so the PV products of the first parts overlap the exponentials of the later ones
+#ifndef ZB_ATTN_PQ
+#define ZB_ATTN_PQ 2  // 4 measured equal (73.9 vs 74.1 us)
+#endif
+constexpr int PQ = ZB_ATTN_PQ;
 constexpr bool kPolyExp = false;  // measured slower on B200 twice (75.6 -> 89 us; with the elect-style MMA issue 77.6 -> 91.6 us)
 
 template <int D> struct FwdCfg {
@@ -90,7 +96,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   uint64_t* o_final = bar + 13;   // [2] per tile
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 15);
   uint64_t* tok = bar + 16;       // [2] per tile: the other tile's exponential phase is done
-  uint64_t* p_half = bar + 18;    // [2] per tile: P of keys [0, 64) stored (PV's first half may start)
+  uint64_t* p_part = bar + 18;    // [2][PQ - 1] per tile: P of keys [0, 32 (q + 1)) stored (PV may start)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / BQ;
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       sm100::mbar_init(&p_full[i], 128);
       sm100::mbar_init(&o_final[i], 1);
       sm100::mbar_init(&tok[i], 128);
-      sm100::mbar_init(&p_half[i], 128);
+      for (int q = 0; q < PQ - 1; ++q) sm100::mbar_init(&p_part[i * (PQ - 1) + q], 128);
     }
     sm100::fence_mbar_init();
   }
@@ -178,13 +184,14 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + (j & 1) * C::TILE);
         const uint64_t vd = sm100::smem_desc(sv, 16384, 1024, sm100::kSwizzle128B);
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          sm100::mbar_wait_warp(hf == 0 ? &p_half[t] : &p_full[t], j & 1);
-          if (hf == 1) TRF(t, j);
+        for (int q = 0; q < PQ; ++q) {
+          constexpr int KQ = BKV / 16 / PQ;  // K-steps per published part of P
+          sm100::mbar_wait_warp(q + 1 < PQ ? &p_part[t * (PQ - 1) + q] : &p_full[t], j & 1);
+          if (q + 1 == PQ) TRF(t, j);
           sm100::tc_fence_after();
           if (sm100::elect_one()) {
 #pragma unroll
-            for (int kk = 4 * hf; kk < 4 * hf + 4; ++kk)
+            for (int kk = KQ * q; kk < KQ * q + KQ; ++kk)
               sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, sm100::desc_adv(vd, kk * 2048),
                                  idesc_o, (j | kk) != 0 ? 1u : 0u);
           }
@@ -282,11 +289,12 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       const bool poly = kPolyExp && j != qt;  // masked (-inf) scores only on the diagonal block: MUFU there
       float sum4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // keys [64 hf, 64 hf + 64) -> P columns [32 hf, 32 hf + 32)
-        uint32_t pk[32];
+      for (int q = 0; q < PQ; ++q) {  // keys [KP q, KP q + KP) -> P columns [KP q / 2, KP (q + 1) / 2)
+        constexpr int KP = BKV / PQ;
+        uint32_t pk[KP / 2];
 #pragma unroll
-        for (int k = 0; k < 64; k += 2) {
-          const float x0 = fmaf(sv[64 * hf + k], scale_log2, mneg), x1 = fmaf(sv[64 * hf + k + 1], scale_log2, mneg);
+        for (int k = 0; k < KP; k += 2) {
+          const float x0 = fmaf(sv[KP * q + k], scale_log2, mneg), x1 = fmaf(sv[KP * q + k + 1], scale_log2, mneg);
           float p0, p1;
           if ((k & 6) == 6 && poly) {  // a quarter of the exponentials on the FMA pipe (MUFU is the bottleneck)
             p0 = ex2_poly(x0);
@@ -299,11 +307,14 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
           __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
           pk[k >> 1] = *reinterpret_cast<uint32_t*>(&v2);
         }
-        sm100::tmem_st32(t_s + 32 * hf, pk);
-        if (hf == 0) {  // publish P of keys [0, 64): PV's first half overlaps the second half here
+        if constexpr (KP == 64)
+          sm100::tmem_st32(t_s + KP / 2 * q, pk);
+        else
+          sm100::tmem_st16(t_s + KP / 2 * q, pk);
+        if (q + 1 < PQ) {  // publish this part of P: its PV products overlap the next part here
           sm100::tmem_st_wait();
           sm100::tc_fence_before();
-          sm100::mbar_arrive(&p_half[t]);
+          sm100::mbar_arrive(&p_part[t * (PQ - 1) + q]);
         }
       }
       l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
