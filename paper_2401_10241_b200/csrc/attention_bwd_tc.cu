@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* o_final = ds_full + 2;
   uint64_t* at_full = o_final + 1;  // K (V) resident in TMEM
   uint32_t* tslot = reinterpret_cast<uint32_t*>(at_full + 1);
+  uint64_t* ds_part = bar + 16;  // [2]: the first 16 queries / keys of each half are in TMEM
   static_assert((1 + 2 * C::ST + 8) * 8 + 4 <= 256, "barrier area");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(384, 1)
       sm100::mbar_init(&sp_full[i], 1);
       sm100::mbar_init(&sp_empty[i], 1);
       sm100::mbar_init(&ds_full[i], 256);
+      sm100::mbar_init(&ds_part[i], 256);
     }
     sm100::mbar_init(o_final, 1);
     sm100::mbar_init(at_full, 256);
@@ -184,21 +186,28 @@ __global__ void __launch_bounds__(384, 1)
       const uint32_t sk = sm100::smem_addr(smem + C::OFF_K), sv = sm100::smem_addr(smem + C::OFF_V);
       auto issue_grad = [&](int n) {
         const int b = n & 1, st = n % C::ST;
-        sm100::mbar_wait_warp(&ds_full[b], (n >> 1) & 1);
-        TR(3, n);
-        sm100::tc_fence_after();
         const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t sdo = sq + C::Q_TILE;
         const uint32_t tp = tbase + b * 128;
         const uint64_t dod = sm100::smem_desc(sdo, 8192, 1024, sm100::kSwizzle128B);
         const uint64_t qd = sm100::smem_desc(sq, 8192, 1024, sm100::kSwizzle128B);
+        // K = 64 queries: halves live at columns [0,16) and [32,48); each half's first 16 queries
+        // (K-steps 0 and 2) are published before its last 16 (K-steps 1 and 3)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries: halves live at columns [0,16) and [32,48)
-          const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
+        for (int part = 0; part < 2; ++part) {
+          sm100::mbar_wait_warp(part == 0 ? &ds_part[b] : &ds_full[b], (n >> 1) & 1);
+          if (part == 1) TR(3, n);
+          sm100::tc_fence_after();
           if (sm100::elect_one()) {
-            sm100::mma_bf16_ts(t_dv, tp + acol, sm100::desc_adv(dod, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
-            sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::desc_adv(qd, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
+              const int kk = 2 * kh + part;
+              const uint32_t acol = kh * 32 + part * 8;
+              sm100::mma_bf16_ts(t_dv, tp + acol, sm100::desc_adv(dod, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+              sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::desc_adv(qd, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+            }
           }
+          __syncwarp();
         }
         TR(10, n);
         if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
@@ -297,9 +306,9 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t pk[16], dk[16];
       // the mask test only on the (warp-uniform) diagonal steps: off the diagonal the
       // compare / select / index arithmetic was a third of the loop's instructions
-      auto elementwise = [&](auto masked) {
+      auto elementwise = [&](auto masked, int c0) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
+        for (int c = c0; c < c0 + 16; c += 2) {
           float pv[2], dv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
@@ -313,13 +322,22 @@ __global__ void __launch_bounds__(384, 1)
           dk[c >> 1] = pack_bf16(dv[0], dv[1]);
         }
       };
-      if (diag)
-        elementwise(std::true_type{});
-      else
-        elementwise(std::false_type{});
+      // two parts of 16 queries: the grad products of the first overlap the second's exponentials
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        if (diag)
+          elementwise(std::true_type{}, 16 * part);
+        else
+          elementwise(std::false_type{}, 16 * part);
+        sm100::tmem_st8(tp + 32 * hf + 8 * part, pk + 8 * part);       // P^T over this half's S^T columns
+        sm100::tmem_st8(tp + 64 + 32 * hf + 8 * part, dk + 8 * part);  // dS^T over this half's dP^T columns
+        if (part == 0) {
+          sm100::tmem_st_wait();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&ds_part[b]);
+        }
+      }
       if (warp == 4 && lane == 0) TR(8, n);
-      sm100::tmem_st16(tp + 32 * hf, pk);       // P^T over this half's S^T columns
-      sm100::tmem_st16(tp + 64 + 32 * hf, dk);  // dS^T over this half's dP^T columns
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       if (warp == 4 && lane == 0) TR(5, n);
@@ -392,6 +410,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* o_final = ds_full + 2;
   uint64_t* at_full = o_final + 1;  // Q, dO resident in TMEM
   uint32_t* tslot = reinterpret_cast<uint32_t*>(at_full + 1);
+  uint64_t* ds_part = bar + 16;  // [2]: the first 16 queries / keys of each half are in TMEM
   static_assert((1 + 2 * C::ST + 8) * 8 + 4 <= 256, "barrier area");
   static_assert(256 + 2 * D <= 512, "TMEM: S/dP x 2, dQ, Q and dO as packed bf16");
 
@@ -413,6 +432,7 @@ __global__ void __launch_bounds__(384, 1)
       sm100::mbar_init(&sp_full[i], 1);
       sm100::mbar_init(&sp_empty[i], 1);
       sm100::mbar_init(&ds_full[i], 256);
+      sm100::mbar_init(&ds_part[i], 256);
     }
     sm100::mbar_init(o_final, 1);
     sm100::mbar_init(at_full, 256);
@@ -458,15 +478,22 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idesc_g = sm100::idesc_bf16(128, D, false, true);
       auto issue_dq = [&](int j) {
         const int b = j & 1, st = j % C::ST;
-        sm100::mbar_wait_warp(&ds_full[b], (j >> 1) & 1);
-        sm100::tc_fence_after();
         const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
         const uint32_t tp = tbase + b * 128;
         const uint64_t kjd = sm100::smem_desc(skj, 8192, 1024, sm100::kSwizzle128B);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
-          if (sm100::elect_one()) sm100::mma_bf16_ts(t_dq, tp + acol, sm100::desc_adv(kjd, kk * 2048), idesc_g, (j | kk) != 0 ? 1u : 0u);
+        for (int part = 0; part < 2; ++part) {  // see the dK / dV kernel
+          sm100::mbar_wait_warp(part == 0 ? &ds_part[b] : &ds_full[b], (j >> 1) & 1);
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) {
+#pragma unroll
+            for (int kh = 0; kh < 2; ++kh) {
+              const int kk = 2 * kh + part;
+              sm100::mma_bf16_ts(t_dq, tp + kh * 32 + part * 8, sm100::desc_adv(kjd, kk * 2048), idesc_g,
+                                 (j | kk) != 0 ? 1u : 0u);
+            }
+          }
+          __syncwarp();
         }
         if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
         if (sm100::elect_one()) sm100::mma_commit(&st_empty[st]);
@@ -520,9 +547,9 @@ __global__ void __launch_bounds__(384, 1)
       sm100::tmem_ld_wait();
       uint32_t dk[16];
       const int klo = j * 64 + 32 * hf;
-      auto elementwise = [&](auto masked) {
+      auto elementwise = [&](auto masked, int c0) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
+        for (int c = c0; c < c0 + 16; c += 2) {
           float dv[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
@@ -535,11 +562,19 @@ __global__ void __launch_bounds__(384, 1)
         }
       };
       // keys of this half reach above the warp's first query only near the diagonal
-      if (klo + 31 > qb * 128 + qw * 32)
-        elementwise(std::true_type{});
-      else
-        elementwise(std::false_type{});
-      sm100::tmem_st16(tp + 32 * hf, dk);  // dS over this half's S columns
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        if (klo + 31 > qb * 128 + qw * 32)
+          elementwise(std::true_type{}, 16 * part);
+        else
+          elementwise(std::false_type{}, 16 * part);
+        sm100::tmem_st8(tp + 32 * hf + 8 * part, dk + 8 * part);  // dS over this half's S columns
+        if (part == 0) {
+          sm100::tmem_st_wait();
+          sm100::tc_fence_before();
+          sm100::mbar_arrive(&ds_part[b]);
+        }
+      }
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&ds_full[b]);
