@@ -1,4 +1,5 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/tests_final.log 2>&1; tail -2 gpurun_out/tests_final.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/smoke.log
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
-timeout 60 python scripts/attn_perf.py 2>&1 | tail -3 > gpurun_out/attn_perf_r3.jsonl
+timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -2
+for i in 1 2; do
+echo NEW; timeout 120 python scripts/gemm_perf.py 2>&1 | grep -E "F proj|F fc1|F fc2|B fc2" | cut -c1-90
+echo OLD; ZB_LIB=libzb_old.so timeout 120 python scripts/gemm_perf.py 2>&1 | grep -E "F proj|F fc1|F fc2|B fc2" | cut -c1-90
+done
