@@ -84,8 +84,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 namespace tc {
 constexpr int BM = 128, BK = 64;
 constexpr int kThreads = 384;     // warps 0-3: TMA, MMA, TMEM alloc, idle; warps 4-11: epilogue
-constexpr int kEpiThreads = 256;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 8;     // 256 epilogue threads
 constexpr int kStageBytes = 4096;  // epilogue staging per warp: a 32-row x 128-byte TMA box
 constexpr int A_BYTES = BM * BK * 2;
 template <int BN> struct Cfg {
@@ -237,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], kEpiThreads);
+      sm100::mbar_init(&tempty[i], kEpiWarps);  // one arrival per epilogue warp
     }
     for (int i = 0; i < kEpiWarps; ++i) sm100::mbar_init(&xbar[i], 1);
     sm100::fence_mbar_init();
@@ -348,7 +347,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                            tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
                            &xbar[warp - 4], xph, mt * BM + ew * 32, nt * BN + half * (BN / 2), BN / 2, N, lane, ep.beta != 0);
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;
         aph ^= 1;
@@ -406,7 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], 2 * kEpiThreads);  // both CTAs' epilogue threads
+      sm100::mbar_init(&tempty[i], 2 * kEpiWarps);  // one arrival per epilogue warp of both CTAs
     }
     for (int i = 0; i < kEpiWarps; ++i) sm100::mbar_init(&xbar[i], 1);
     sm100::fence_mbar_init();
@@ -550,7 +550,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         st_release(flag, ep.flag_base + sp + 1);
       }
       sm100::tc_fence_before();
-      sm100::mbar_arrive_cluster(acc == 0 ? te0 : te1);
+      __syncwarp();  // the warp's TMEM reads are complete (tmem_ld_wait + fence above): one remote arrival
+      if (lane == 0) sm100::mbar_arrive_cluster(acc == 0 ? te0 : te1);
       if (++acc == 2) {
         acc = 0;
         aph ^= 1;
