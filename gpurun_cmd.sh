@@ -1,3 +1,2 @@
-timeout 300 python -m pytest tests/test_gpu_gemm.py -x -q 2>&1 | tail -2
-echo NEW; timeout 200 python scripts/gemm_epi_sweep.py 2>&1 | tail -10
-echo OLD; ZB_LIB=libzb_old.so timeout 200 python scripts/gemm_epi_sweep.py 2>&1 | tail -10
+timeout 60 python -m pytest tests/test_gpu_attention.py -x -q 2>&1 | tail -2
+for i in 1 2; do timeout 60 python scripts/attn_perf.py 2>&1 | tail -3 | cut -c1-60; done

@@ -133,11 +133,11 @@ __global__ void __launch_bounds__(384, 1)
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&sp_full[i], 1);
       sm100::mbar_init(&sp_empty[i], 1);
-      sm100::mbar_init(&ds_full[i], 256);
-      sm100::mbar_init(&ds_part[i], 256);
+      sm100::mbar_init(&ds_full[i], 8);  // one arrival per elementwise warp
+      sm100::mbar_init(&ds_part[i], 8);
     }
     sm100::mbar_init(o_final, 1);
-    sm100::mbar_init(at_full, 256);
+    sm100::mbar_init(at_full, 8);
 #ifdef ZB_ATTN_TRACE
     sm100::mbar_init(bar + 20, 1);
 #endif
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(384, 1)
       if (C::VT && hf == 1) tile_row_to_tmem<D>(smem + C::OFF_V, r, t_vt + lane_off);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
-      sm100::mbar_arrive(at_full);
+      sm100::mbar_arrive_warp(at_full);
     }
     for (int n = 0; n < nq; ++n) {
       const int i = i0 + n, b = n & 1, st = n % C::ST;
@@ -334,14 +334,14 @@ __global__ void __launch_bounds__(384, 1)
         if (part == 0) {
           sm100::tmem_st_wait();
           sm100::tc_fence_before();
-          sm100::mbar_arrive(&ds_part[b]);
+          sm100::mbar_arrive_warp(&ds_part[b]);
         }
       }
       if (warp == 4 && lane == 0) TR(8, n);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       if (warp == 4 && lane == 0) TR(5, n);
-      sm100::mbar_arrive(&ds_full[b]);
+      sm100::mbar_arrive_warp(&ds_full[b]);
     }
     sm100::mbar_wait(o_final, 0);
     if (warp == 4 && lane == 0) TR(6, 1);
@@ -431,11 +431,11 @@ __global__ void __launch_bounds__(384, 1)
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&sp_full[i], 1);
       sm100::mbar_init(&sp_empty[i], 1);
-      sm100::mbar_init(&ds_full[i], 256);
-      sm100::mbar_init(&ds_part[i], 256);
+      sm100::mbar_init(&ds_full[i], 8);  // one arrival per elementwise warp
+      sm100::mbar_init(&ds_part[i], 8);
     }
     sm100::mbar_init(o_final, 1);
-    sm100::mbar_init(at_full, 256);
+    sm100::mbar_init(at_full, 8);
     sm100::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(384, 1)
     tile_row_to_tmem<D>(smem + (hf == 0 ? C::OFF_Q : C::OFF_DO), r, (hf == 0 ? t_qt : t_dot) + lane_off);
     sm100::tmem_st_wait();
     sm100::tc_fence_before();
-    sm100::mbar_arrive(at_full);
+    sm100::mbar_arrive_warp(at_full);
     for (int j = 0; j < nkv; ++j) {
       const int b = j & 1;
       sm100::mbar_wait(&sp_full[b], (j >> 1) & 1);
@@ -572,12 +572,12 @@ __global__ void __launch_bounds__(384, 1)
         if (part == 0) {
           sm100::tmem_st_wait();
           sm100::tc_fence_before();
-          sm100::mbar_arrive(&ds_part[b]);
+          sm100::mbar_arrive_warp(&ds_part[b]);
         }
       }
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&ds_full[b]);
+      sm100::mbar_arrive_warp(&ds_full[b]);
     }
     sm100::mbar_wait(o_final, 0);
     sm100::tc_fence_after();

@@ -117,10 +117,10 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       sm100::mbar_init(&v_full[i], 1);
       sm100::mbar_init(&v_empty[i], 1);
       sm100::mbar_init(&s_full[i], 1);
-      sm100::mbar_init(&p_full[i], 128);
+      sm100::mbar_init(&p_full[i], 4);  // one arrival per softmax warp
       sm100::mbar_init(&o_final[i], 1);
-      sm100::mbar_init(&tok[i], 128);
-      for (int q = 0; q < PQ - 1; ++q) sm100::mbar_init(&p_part[i * (PQ - 1) + q], 128);
+      sm100::mbar_init(&tok[i], 4);
+      for (int q = 0; q < PQ - 1; ++q) sm100::mbar_init(&p_part[i * (PQ - 1) + q], 4);
     }
     sm100::fence_mbar_init();
   }
@@ -314,16 +314,16 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         if (q + 1 < PQ) {  // publish this part of P: its PV products overlap the next part here
           sm100::tmem_st_wait();
           sm100::tc_fence_before();
-          sm100::mbar_arrive(&p_part[t * (PQ - 1) + q]);
+          sm100::mbar_arrive_warp(&p_part[t * (PQ - 1) + q]);
         }
       }
       l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
       if ((warp & 3) == 0 && lane == 0) TRF(10 + t, j);
-      if (alt) sm100::mbar_arrive(&tok[t ^ 1]);
+      if (alt) sm100::mbar_arrive_warp(&tok[t ^ 1]);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       if ((warp & 3) == 0 && lane == 0) TRF(4 + 3 * t, j);
-      sm100::mbar_arrive(&p_full[t]);
+      sm100::mbar_arrive_warp(&p_full[t]);
     }
     if (nk > 0) {
       sm100::mbar_wait(&o_final[t], 0);

@@ -43,6 +43,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// One arrival per warp (barrier count = number of warps): the warp's threads have finished
+// their prior work (tcgen05.wait + fence::before_thread_sync where TMEM is involved); a
+// per-thread arrival would serialise 32x more atomics on the barrier word.
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 // mbar_wait by a whole warp that then needs to be converged (elect_one() follows)
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   mbar_wait(bar, parity);
