@@ -95,11 +95,12 @@ template <int D> struct DkdvCfg {
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 
+// (the tensor maps are references to the launching kernel's __grid_constant__ parameters)
 template <int D>
-__global__ void __launch_bounds__(384, 1)
-    k_dkdv_tc(const __grid_constant__ CUtensorMap tmKV, const __grid_constant__ CUtensorMap tmQ,
-              const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse,
-              const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2) {
+__device__ __forceinline__ void dkdv_body(const CUtensorMap& tmKV, const CUtensorMap& tmQ, const CUtensorMap& tmDO,
+                                          const float* __restrict__ lse, const float* __restrict__ delta,
+                                          bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2,
+                                          int kb_, int hd_, int bb_) {
   using C = DkdvCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(384, 1)
   static_assert((1 + 2 * C::ST + 8) * 8 + 4 <= 256, "barrier area");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = blockIdx.x, hd = blockIdx.y, bb = blockIdx.z;
+  const int kb = kb_, hd = hd_, bb = bb_;
   const int h = a * D;
   const int i0 = 2 * kb, nq = s / 64 - i0;
   const int row0 = bb * s;
@@ -393,10 +394,10 @@ template <int D> struct DqCfg {
 };
 
 template <int D>
-__global__ void __launch_bounds__(384, 1)
-    k_dq_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
-            const __grid_constant__ CUtensorMap tmDO, const float* __restrict__ lse, const float* __restrict__ delta,
-            bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2) {
+__device__ __forceinline__ void dq_body(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const CUtensorMap& tmDO,
+                                        const float* __restrict__ lse, const float* __restrict__ delta,
+                                        bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2, int level,
+                                        int hd_, int bb_) {
   using C = DqCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -416,8 +417,8 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / 128;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
-  const int hd = blockIdx.y, bb = blockIdx.z;
+  const int qb = nqb - 1 - level;
+  const int hd = hd_, bb = bb_;
   const int h = a * D;
   const int nkv = 2 * qb + 2;
   const int row0 = bb * s;
@@ -604,6 +605,27 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) sm100::tmem_dealloc<512>(tbase);
 }
 
+// One launch for both halves of the backward: CTA i takes work level i / (2 a b) (heaviest
+// first: dK/dV key block `level`, dQ query block nqb-1-level, both with the same step count
+// s/64 - 2 level ... 2 level + 2) and, within it, the dK/dV CTAs of every (head, sequence)
+// before the dQ ones.  The two kernels' partial last waves become one.
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    k_bwd_tc(const __grid_constant__ CUtensorMap kv128, const __grid_constant__ CUtensorMap kv64,
+             const __grid_constant__ CUtensorMap do64, const __grid_constant__ CUtensorMap do128,
+             const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a,
+             int b, float scale, float scale_log2) {
+  const int per = a * b;
+  const int level = static_cast<int>(blockIdx.x) / (2 * per);
+  int r = static_cast<int>(blockIdx.x) % (2 * per);
+  if (r < per)
+    dkdv_body<D>(kv128, kv64, do64, lse, delta, dqkv, s, a, scale, scale_log2, level, r % a, r / a);
+  else {
+    r -= per;
+    dq_body<D>(kv128, kv64, do128, lse, delta, dqkv, s, a, scale, scale_log2, level, r % a, r / a);
+  }
+}
+
 }  // namespace attn_bwd_tc
 
 template <int D>
@@ -611,10 +633,10 @@ static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout
                           const float* delta, cudaStream_t st) {
   using C1 = attn_bwd_tc::DkdvCfg<D>;
   using C2 = attn_bwd_tc::DqCfg<D>;
+  constexpr int SMEM = C1::SMEM > C2::SMEM ? C1::SMEM : C2::SMEM;
   static bool attr = false;
   if (!attr) {
-    ZB_CUDA(cudaFuncSetAttribute(attn_bwd_tc::k_dkdv_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1::SMEM));
-    ZB_CUDA(cudaFuncSetAttribute(attn_bwd_tc::k_dq_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
+    ZB_CUDA(cudaFuncSetAttribute(attn_bwd_tc::k_bwd_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr = true;
   }
   const int h = sh.a * D, rows = sh.b * sh.s;
@@ -623,12 +645,9 @@ static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout
   const CUtensorMap do64 = make_tmap(dout, h, rows, h, 64, 64);
   const CUtensorMap do128 = make_tmap(dout, h, rows, h, 64, 128);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
-  dim3 grid(sh.s / 128, sh.a, sh.b);
-  launch(PDL_ATTN, attn_bwd_tc::k_dkdv_tc<D>, grid, 384, C1::SMEM, st, kv128, kv64, do64, lse, delta, static_cast<bf16*>(dqkv),
-                                                         sh.s, sh.a, scale, scale * attn_bwd_tc::LOG2E);
-  ZB_LAUNCH_CHECK();
-  launch(PDL_ATTN, attn_bwd_tc::k_dq_tc<D>, grid, 384, C2::SMEM, st, kv128, kv64, do128, lse, delta, static_cast<bf16*>(dqkv),
-                                                       sh.s, sh.a, scale, scale * attn_bwd_tc::LOG2E);
+  const int grid = 2 * (sh.s / 128) * sh.a * sh.b;
+  launch(PDL_ATTN, attn_bwd_tc::k_bwd_tc<D>, grid, 384, SMEM, st, kv128, kv64, do64, do128, lse, delta,
+         static_cast<bf16*>(dqkv), sh.s, sh.a, sh.b, scale, scale * attn_bwd_tc::LOG2E);
   ZB_LAUNCH_CHECK();
 }
 
