@@ -100,6 +100,23 @@ template <int BN> struct Cfg {
 // output element type of an epilogue
 template <int EPI> using OutT = typename std::conditional<(EPI == EPI_F32_ACC || EPI == EPI_F32_STORE), float, bf16>::type;
 
+#ifdef ZB_GEMM_TRACE
+// timeline of CTA 0 (leader of pair 0) of k_gemm_tc2, globaltimer ns (measurement build only):
+// row 0 MMA warp has the accumulator (tempty), 1 last MMA of the tile issued, 2 epilogue warp 4
+// has the accumulator (tfull), 3 epilogue warp 4 released it, 4 epilogue warp 11 released it
+__device__ unsigned long long g_gtrace[8][64];
+__device__ __forceinline__ void gtr(int row, int n) {
+  if (blockIdx.x == 0 && n < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gtrace[row][n] = t;
+  }
+}
+#define GTR(row, n) gtr(row, n)
+#else
+#define GTR(row, n)
+#endif
+
 // byte offset of 16-byte piece j of row `lane` in a 32 x 128 B box, TMA 128B-swizzle layout
 __device__ __forceinline__ int swz(int lane, int j) { return lane * 128 + ((j ^ (lane & 7)) << 4); }
 
@@ -480,6 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t ph = 0, aph = 0;
       for (int t = cid; t < items; t += ncl) {
         sm100::mbar_wait_warp(&tempty[acc], aph ^ 1);
+        if (lane == 0) GTR(0, (t - cid) / ncl);
         sm100::tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         const int kb0 = kb_begin(t / tiles);
@@ -506,6 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ph ^= 1;
           }
         }
+        if (lane == 0) GTR(1, (t - cid) / ncl);
         if (sm100::elect_one()) sm100::mma_commit_pair(&tfull[acc], 0x3);
         __syncwarp();
         if (++acc == 2) {
@@ -540,6 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         sm100::tma_load_2d_hint(buf, &tmX, &xbar[warp - 4], ecol, erow, sm100::l2_evict_first());
       }
       sm100::mbar_wait(&tfull[acc], aph);
+      if (warp == 4 && lane == 0) GTR(2, (t - cid) / ncl);
       sm100::tc_fence_after();
       epilogue_chunks<EPI>(ep, &tmC, &tmX,
                            tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
@@ -552,6 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       sm100::tc_fence_before();
       __syncwarp();  // the warp's TMEM reads are complete (tmem_ld_wait + fence above): one remote arrival
       if (lane == 0) sm100::mbar_arrive_cluster(acc == 0 ? te0 : te1);
+      if (lane == 0 && (warp == 4 || warp == 11)) GTR(warp == 4 ? 3 : 4, (t - cid) / ncl);
       if (++acc == 2) {
         acc = 0;
         aph ^= 1;
@@ -856,3 +877,9 @@ void gemm(const GemmArgs& g, DType dt, cudaStream_t st) {
 }
 
 }  // namespace zb
+
+#ifdef ZB_GEMM_TRACE
+extern "C" int zb_dbg_gemm_trace(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::tc::g_gtrace, sizeof(unsigned long long) * 8 * 64));
+}
+#endif
