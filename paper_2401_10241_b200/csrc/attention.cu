@@ -239,16 +239,19 @@ __global__ void __launch_bounds__(NT) k_fwd_bf16(const bf16* __restrict__ qkv, b
 }
 
 // ------------------------------------------------------------------ backward: delta = rowsum(dO * O)
-template <typename T>
+template <typename T, int DC>
 __global__ void k_delta(const T* __restrict__ o, const T* __restrict__ dout, float* __restrict__ delta, int s, int a,
-                        int d, int rows) {
+                        int d_rt, int rows) {
   pdl_wait();
-  // one thread per (row, head): d/8 vector loads of each operand summed in order
+  // one thread per (row, head): d/8 vector loads of each operand summed in order (DC > 0: the
+  // head dim at compile time, every load of the thread in flight at once)
+  const int d = DC > 0 ? DC : d_rt;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= static_cast<int64_t>(rows) * a) return;
   const int row = static_cast<int>(t / a), hd = static_cast<int>(t % a);  // row in [0, b*s)
   const int64_t off = t * d;
   float acc = 0.f;
+#pragma unroll
   for (int i = 0; i < d; i += 8) {
     float x[8], y[8];
     Vec8<T>::load(o + off + i, x);
@@ -631,12 +634,15 @@ void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const vo
                         const float* lse, void* dqkv, float* delta, cudaStream_t st) {
   const int rows = sh.b * sh.s;
   const int blocks = static_cast<int>((static_cast<int64_t>(rows) * sh.a + 255) / 256);
-  if (dt == DT_BF16)
-    launch(PDL_OPS, attn::k_delta<bf16>, blocks, 256, 0, st, static_cast<const bf16*>(o), static_cast<const bf16*>(dout), delta,
-                                                sh.s, sh.a, sh.d, rows);
-  else
-    launch(PDL_OPS, attn::k_delta<float>, blocks, 256, 0, st, static_cast<const float*>(o), static_cast<const float*>(dout), delta,
-                                                 sh.s, sh.a, sh.d, rows);
+  if (dt == DT_BF16) {
+    auto kern = sh.d == 64 ? attn::k_delta<bf16, 64> : sh.d == 96 ? attn::k_delta<bf16, 96>
+              : sh.d == 128 ? attn::k_delta<bf16, 128> : attn::k_delta<bf16, 0>;
+    launch(PDL_OPS, kern, blocks, 256, 0, st, static_cast<const bf16*>(o), static_cast<const bf16*>(dout), delta, sh.s,
+           sh.a, sh.d, rows);
+  } else {
+    launch(PDL_OPS, attn::k_delta<float, 0>, blocks, 256, 0, st, static_cast<const float*>(o),
+           static_cast<const float*>(dout), delta, sh.s, sh.a, sh.d, rows);
+  }
   ZB_LAUNCH_CHECK();
   if (dt == DT_BF16 && !legacy_attention() && attention_bwd_tc(sh, qkv, dout, lse, dqkv, delta, st)) return;
   switch (sh.d) {
