@@ -1,3 +1,4 @@
-timeout 60 python -m pytest tests/test_gpu_attention.py -x -q 2>&1 | tail -1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_delta python scripts/micro/delta_one.py 2>&1 | grep -E "gpu__time" | tail -3
-ZB_LIB=libzb_old.so ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_delta python scripts/micro/delta_one.py 2>&1 | grep -E "gpu__time" | tail -3
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/tests_final.log 2>&1; tail -1 gpurun_out/tests_final.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/smoke.log
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_22l.csv python scripts/profile_step.py --layers 22 --m 1 > gpurun_out/launches.log 2>&1; echo ncu rc=$?
