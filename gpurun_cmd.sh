@@ -1,1 +1,1 @@
-timeout 900 python bench.py --config 6.2B --no-cpu-baseline > gpurun_out/bench_6p2b.json 2> gpurun_out/bench_6p2b.err; echo rc=$?; tail -2 gpurun_out/bench_6p2b.err
+for ps in 2 3 4 6; do echo per_sm=$ps; ZB_COLRED_PER_SM=$ps timeout 100 python scripts/ops_perf.py 2>&1 | grep -E "ln_bwd_total|bias_h|bias_4h"; done
