@@ -184,12 +184,30 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
+        _start_watchdog(rank)
         if args.family in ("zbv", "1f1bi"):
             return run_pipeline_chunked(args, cfg, rank, world, local)
         return run_pipeline(args, cfg, rank, world, local)
     if args.family in ("zbv", "1f1bi"):
         raise SystemExit("--family zbv / 1f1bi needs --gpus >= 2 (two model chunks per GPU)")
     return run_single(args, cfg)
+
+
+def _start_watchdog(rank):
+    """Multi-GPU runs only: the NCCL P2P path cannot be exercised on the one-GPU
+    development boxes, so a hang there ends the process with a message instead of
+    holding the node until the driver's own limit (ZB_BENCH_WATCHDOG_S, default 1200 s)."""
+    import threading
+    limit = float(os.environ.get("ZB_BENCH_WATCHDOG_S", "1200"))
+
+    def fire():
+        sys.stderr.write(f"bench.py rank {rank}: no result after {limit:.0f} s (watchdog), exiting\n")
+        sys.stderr.flush()
+        os._exit(3)
+
+    t = threading.Timer(limit, fire)
+    t.daemon = True
+    t.start()
 
 
 def run_single(args, cfg):
