@@ -81,13 +81,11 @@ zb_status_t zb_dbg_worker_plan(const zb_pass_t* passes, int32_t n, int32_t nv, i
 zb_status_t zb_dbg_speculative_counts(const zb_pass_t* passes, int32_t n, int32_t p, int32_t* out);
 
 /* Measurement builds only (not exported by the default libzb.so, so not declared here):
- *   make BUILD=build_trace OUT=libzb_trace.so EXTRA=-DZB_ATTN_TRACE   exports
- *     int zb_dbg_attn_trace(unsigned long long host[12 * 64])       (dK/dV CTA timeline)
- *     int zb_dbg_attn_fwd_trace(unsigned long long host[12 * 64])   (forward CTA timeline)
- *   make BUILD=build_gtrace OUT=libzb_gtrace.so EXTRA=-DZB_GEMM_TRACE exports
- *     int zb_dbg_gemm_trace(unsigned long long host[8 * 64])        (2-CTA GEMM CTA 0 timeline)
- * globaltimer nanoseconds per (event row, step); read by scripts/attn_trace.py,
- * scripts/attn_fwd_trace.py and scripts/gemm_trace.py. */
+ * `make BUILD=build_trace OUT=libzb_trace.so EXTRA=-DZB_ATTN_TRACE` adds the dK/dV and the
+ * forward CTA timelines (12 x 64 globaltimer stamps each), `make BUILD=build_gtrace
+ * OUT=libzb_gtrace.so EXTRA=-DZB_GEMM_TRACE` the 2-CTA GEMM's CTA-0 timeline (8 x 64);
+ * their readers are scripts/attn_trace.py, scripts/attn_fwd_trace.py and
+ * scripts/gemm_trace.py. */
 
 #ifdef __cplusplus
 }
