@@ -84,6 +84,25 @@ zb_status_t zb_schedule(int32_t p, int32_t m, int64_t T_F, int64_t T_B, int64_t 
                         int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family, zb_pass_t* out,
                         int32_t out_cap, zb_sim_t* sim);
 
+/* zb_schedule_per_stage: zb_schedule with PER-STAGE pass times T_F[p],
+ * T_B[p], T_W[p] (host int64 arrays) — "we first conducted a specific number
+ * of iterations for profiling, collecting ... T_F, T_B, T_W, and T_comm ...
+ * fed them into our automatic pipeline scheduling algorithm".  Stages
+ * of one pipeline differ (stage 0 holds the embedding, the last stage the LM
+ * head, P:169's partition).  The AUTO heuristic uses each stage's
+ * own times (DESIGN.md R-auto-stage); the simulator / bubble rate use them for
+ * every family.  Same errors as zb_schedule plus ZB_EINVAL for a NULL array. */
+zb_status_t zb_schedule_per_stage(int32_t p, int32_t m, const int64_t* T_F, const int64_t* T_B, const int64_t* T_W,
+                                  int64_t T_comm, int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family,
+                                  zb_pass_t* out, int32_t out_cap, zb_sim_t* sim);
+
+/* zb_partition: layers per stage when L layers are cut into p stages —
+ * P:169 "the first and last pipeline stage ... one fewer layer" when (L+2) is
+ * divisible by p (and the middle stages hold >= 2 layers), else an even split
+ * with the remainder on the middle stages first.  layers: host int32 [p].
+ * ZB_EINVAL unless 1 <= p <= min(L, 64). */
+zb_status_t zb_partition(int32_t L, int32_t p, int32_t* layers);
+
 /* zb_simulate: ASAP timing (App. F constraints (4)-(6) as execution
  * semantics) of arbitrary per-stage lists in `passes` (grouped by stage, each
  * stage in execution order), with per-stage times T_F[p], T_B[p], T_W[p]
@@ -249,6 +268,18 @@ zb_status_t zb_run_iteration_worker(zb_ctx_t* const* chunks, int32_t k, const zb
 
 /* Per-pass event times of the last ZB_RUN_TIMING run (syncs). */
 zb_status_t zb_ctx_read_stats(zb_ctx_t* ctx, zb_iter_stats_t* stats);
+
+/* Profiling step of P:169 ("we first conducted a specific number of iterations
+ * for profiling, collecting ... T_F, T_B, T_W"): collects the per-pass CUDA-event
+ * durations of the last ZB_RUN_TIMING run (each pass once; replayed Fs count as
+ * F) into the context's per-kind samples and returns the MEDIAN over all samples
+ * since the last reset, in integer ns: T_ns[0] = T_F, [1] = T_B, [2] = T_W
+ * (0 when a kind has no sample); n_samples[3] may be NULL.  The pass times
+ * exclude waits for messages (events are recorded after the stream waits).
+ * reset != 0 clears the samples (T_ns ignored).  Syncs the context's stream.
+ * Each timed run is collected once however often this is called; it does not
+ * disturb zb_ctx_read_stats. */
+zb_status_t zb_ctx_profile(zb_ctx_t* ctx, int32_t reset, int64_t* T_ns, int32_t* n_samples);
 
 /* ------------------------------------------------------------------------ */
 /* Optimizer with post-validation (§4, App. C)   */

@@ -246,6 +246,9 @@ def heuristic(p: int, m: int, TF: int, TB: int, TW: int, Tcomm: int, MB: int, MW
     away.  Returns per-stage pass lists (the order is the product)."""
     if Mlimit < MB:
         raise ValueError("M_limit below M_B: no F can ever run")
+    # per-stage times (P:169: the profiled T_F / T_B / T_W of each stage are what the
+    # scheduler is fed; DESIGN.md R-auto-stage): scalars mean the same time on every stage
+    TF, TB, TW = _per_stage(TF, p), _per_stage(TB, p), _per_stage(TW, p)
     nF, nB, nW = [0] * p, [0] * p, [0] * p
     pend = [deque() for _ in range(p)]
     mem, bub, busy = [0] * p, [0] * p, [0] * p
@@ -295,7 +298,7 @@ def heuristic(p: int, m: int, TF: int, TB: int, TW: int, Tcomm: int, MB: int, MW
                 if Bready:
                     pick = "B"
                 elif Fready:
-                    delays = (known(aB) and aB < t + TF) or (aB is None and TB + Tcomm < TF)
+                    delays = (known(aB) and aB < t + TF[s]) or (aB is None and TB[s] + Tcomm < TF[s])
                     if not delays or fill_warmup:
                         pick = "F"
             else:
@@ -313,7 +316,7 @@ def heuristic(p: int, m: int, TF: int, TB: int, TW: int, Tcomm: int, MB: int, MW
                     cands.append(aB)
                 r = min(cands) if cands else INF
                 others = max((bub[x] for x in range(p) if x != s), default=0)
-                if (nF[s] < m and mem[s] + MB > Mlimit and not Bready) or r - t >= TW or \
+                if (nF[s] < m and mem[s] + MB > Mlimit and not Bready) or r - t >= TW[s] or \
                         (nF[s] == m and nB[s] == m):
                     pick = "W"
                 elif r > t and bub[s] + (r - t) > others:
@@ -325,19 +328,19 @@ def heuristic(p: int, m: int, TF: int, TB: int, TW: int, Tcomm: int, MB: int, MW
             started[s] = True
             if pick == "F":
                 j = nF[s]; nF[s] += 1
-                endF[(s, j)] = t + TF
+                endF[(s, j)] = t + TF[s]
                 mem[s] += MB
-                busy[s] = t + TF
+                busy[s] = t + TF[s]
             elif pick == "B":
                 j = nB[s]; nB[s] += 1
-                endB[(s, j)] = t + TB
+                endB[(s, j)] = t + TB[s]
                 mem[s] += MW - MB
                 pend[s].append(j)
-                busy[s] = t + TB
+                busy[s] = t + TB[s]
             else:
                 j = pend[s].popleft(); nW[s] += 1
                 mem[s] -= MW
-                busy[s] = t + TW
+                busy[s] = t + TW[s]
             last[s] = pick
             lists[s].append((pick, j))
         nxt = INF

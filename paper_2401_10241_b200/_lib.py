@@ -84,6 +84,9 @@ _SIGS = {
                      C.POINTER(zb_sim_t)], _I32),
     "zb_schedule_chunked": ([_I32, _I32, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I32, C.POINTER(zb_pass_t),
                              _I32, C.POINTER(zb_sim_t)], _I32),
+    "zb_schedule_per_stage": ([_I32, _I32, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64), _I64, _I64, _I64, _I64,
+                               _I32, C.POINTER(zb_pass_t), _I32, C.POINTER(zb_sim_t)], _I32),
+    "zb_partition": ([_I32, _I32, C.POINTER(_I32)], _I32),
     "zb_simulate": ([_I32, _I32, C.POINTER(zb_pass_t), _I32, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64),
                      _I64, _I64, _I64, _I32, C.POINTER(zb_sim_t)], _I32),
     "zb_dbg_gemm": ([_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _P, _P, _I64, _I32, _P],
@@ -123,6 +126,7 @@ _SIGS = {
     "zb_run_iteration": ([_P, C.POINTER(zb_pass_t), _I32, _P, _P, _I32], _I32),
     "zb_run_iteration_local": ([C.POINTER(_P), _I32, C.POINTER(zb_pass_t), _I32, _P, _P, _I32], _I32),
     "zb_ctx_read_stats": ([_P, C.POINTER(zb_iter_stats_t)], _I32),
+    "zb_ctx_profile": ([_P, _I32, C.POINTER(_I64), C.POINTER(_I32)], _I32),
     "zb_post_validate_step": ([_P, C.POINTER(zb_optim_cfg_t)], _I32),
     "zb_post_validate_finish": ([_P, C.POINTER(zb_optim_cfg_t)], _I32),
     "zb_post_validate_local": ([C.POINTER(_P), _I32, C.POINTER(zb_optim_cfg_t)], _I32),

@@ -30,6 +30,31 @@ def schedule(family: str, p: int, m: int, T_F: int, T_B: int, T_W: int, T_comm: 
     return out, sim
 
 
+def schedule_per_stage(family: str, p: int, m: int, T_F: Sequence[int], T_B: Sequence[int], T_W: Sequence[int],
+                       T_comm: int = 0, M_limit: int = 0, M_B: int = 1, M_W: int = 1):
+    """zb_schedule_per_stage (per-stage profiled times) -> (passes, sim)."""
+    n = 3 * p * m
+    out = (zb_pass_t * n)()
+    sim = zb_sim_t()
+    arr = lambda x: (C.c_int64 * p)(*[int(v) for v in x])
+    check(lib.zb_schedule_per_stage(p, m, arr(T_F), arr(T_B), arr(T_W), int(T_comm), int(M_limit), int(M_B),
+                                    int(M_W), FAMILY[family], out, n, C.byref(sim)))
+    return out, sim
+
+
+def partition(L: int, p: int) -> List[int]:
+    """zb_partition: layers per stage."""
+    out = (C.c_int32 * p)()
+    check(lib.zb_partition(L, p, out))
+    return list(out)
+
+
+def stage_layers(L: int, p: int, stage: int) -> Tuple[int, int]:
+    parts = partition(L, p)
+    first = sum(parts[:stage])
+    return first, first + parts[stage]
+
+
 def schedule_chunked(family: str, p: int, m: int, chunks: int, T_F: int, T_B: int, T_W: int, T_comm: int = 0,
                      M_limit: int = 0, M_B: int = 1, M_W: int = 1):
     """zb_schedule_chunked ("zbv" | "1f1bi") -> (passes, sim).  passes are
@@ -96,7 +121,6 @@ def _stream(stream) -> Optional[int]:
 # ------------------------------------------------------------------ stage context
 
 def model_cfg(cfg, p: int, stage: int, m: int, n_slots: int, dtype: str = "bf16") -> zb_model_cfg_t:
-    from zb_synth import stage_layers
     first, last = stage_layers(cfg.L, p, stage)
     return zb_model_cfg_t(cfg.h, cfg.a, cfg.L, cfg.s, cfg.b, cfg.V, p, stage, first, last, m, n_slots,
                           ZB_DTYPE_BF16 if dtype == "bf16" else ZB_DTYPE_F32, 0)
@@ -137,8 +161,14 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
-            lib.zb_ctx_destroy(self.h)
+            lib.zb_ctx_destroy(self.h)       # drains the context's stream before freeing
             self.h = C.c_void_p()
+            # the arena was allocated on torch's current stream but written on self.stream
+            try:
+                if hasattr(self.stream, "wait_stream"):
+                    self.arena.record_stream(self.stream)
+            except Exception:
+                pass
 
     def __del__(self):
         try:
@@ -222,6 +252,14 @@ class Context:
         check(lib.zb_ctx_read_stats(self.h, C.byref(st)))
         n = st.n_passes
         return list(st.pass_start_ms[:n]), list(st.pass_end_ms[:n])
+
+    def profile(self, reset: bool = False):
+        """zb_ctx_profile: median (T_F, T_B, T_W) in ns over the timed runs since the
+        last reset, and the sample counts (P:169 profiling iterations)."""
+        t = (C.c_int64 * 3)()
+        n = (C.c_int32 * 3)()
+        check(lib.zb_ctx_profile(self.h, 1 if reset else 0, t, n))
+        return list(t), list(n)
 
     # optimizer --------------------------------------------------------------
     def post_validate_step(self, opt: zb_optim_cfg_t):

@@ -24,9 +24,9 @@ void begin_iteration(Ctx& c) {
 
 // Post-validation helpers (§4; Algorithm 1).
 void pv_local(Ctx& c) { grad_norm(c.grad, c.n_total, c.norm_part, c.nf_part, c.pv, c.stream); }
-void pv_apply(Ctx& c, const zb_optim_cfg_t& o) {
+void pv_apply(Ctx& c, const zb_optim_cfg_t& o, bool validation) {
   adamw_apply(c.theta, c.m, c.v, c.grad, c.shadow, c.n_total, c.n_wd, c.shadow ? c.n_shadow : 0, o.lr, o.beta1,
-              o.beta2, o.eps, o.weight_decay, c.pv, c.stream);
+              o.beta2, o.eps, o.weight_decay, c.pv, validation, c.stream);
   pv_finish_apply(c.pv, c.stream);
 }
 // copy src partial (sum, flag) -> dst partial_in / full, via a tiny device memcpy of the two fields
@@ -42,6 +42,38 @@ void copy_full(Ctx& src_with_partial, Ctx& dst, bool from_partial) {
   ZB_CUDA(cudaMemcpyAsync(&dst.pv->full_sumsq, sp, sizeof(double), cudaMemcpyDeviceToDevice, dst.stream));
   ZB_CUDA(cudaMemcpyAsync(&dst.pv->full_nf, sf, sizeof(int32_t), cudaMemcpyDeviceToDevice, dst.stream));
 }
+// ABI-boundary validation of a stage's pass list (zb.h promises ZB_EINVAL for bad
+// passes): every field in range, each (kind, microbatch) exactly once, F before B
+// before W per microbatch (P:46 dependencies), B / W on the slot their F used, and no
+// F reusing a slot whose previous microbatch has not run its W yet (the stash
+// lifetime F -> W).
+void check_stage_passes(const zb_pass_t* passes, int32_t n, int stage, int m, int n_slots) {
+  std::vector<int> pos[3];
+  for (auto& v : pos) v.assign(m, -1);
+  std::vector<int> slot_of(m, -1), slot_user(n_slots, -1);
+  int k = 0;
+  for (int i = 0; i < n; ++i) {
+    const zb_pass_t& q = passes[i];
+    if (q.stage != stage) continue;
+    if (q.kind < ZB_F || q.kind > ZB_W) throw Error(ZB_EINVAL, "pass kind out of range");
+    if (q.microbatch < 0 || q.microbatch >= m) throw Error(ZB_EINVAL, "pass microbatch out of range");
+    if (q.slot < 0 || q.slot >= n_slots) throw Error(ZB_EINVAL, "pass slot out of range");
+    const int j = q.microbatch;
+    if (pos[q.kind][j] >= 0) throw Error(ZB_EINVAL, "pass listed twice");
+    if (q.kind == ZB_F) {
+      if (slot_user[q.slot] >= 0) throw Error(ZB_EINVAL, "F reuses a stash slot before the W of its previous user");
+      slot_user[q.slot] = j;
+      slot_of[j] = q.slot;
+    } else {
+      if (pos[q.kind - 1][j] < 0) throw Error(ZB_EINVAL, "B before its F, or W before its B");
+      if (q.slot != slot_of[j]) throw Error(ZB_EINVAL, "B / W slot differs from the slot of its F");
+      if (q.kind == ZB_W) slot_user[q.slot] = -1;
+    }
+    pos[q.kind][j] = k++;
+  }
+  if (k != 3 * m) throw Error(ZB_EINVAL, "stage " + std::to_string(stage) + " needs 3m passes, got " + std::to_string(k));
+}
+
 void check_opt(const zb_optim_cfg_t* o) {
   if (o == nullptr) throw Error(ZB_EINVAL, "null optimizer config");
   if (o->lr * o->weight_decay == 1.0f) throw Error(ZB_ESTATE, "lr * weight_decay == 1: rollback undefined");
@@ -96,7 +128,13 @@ extern "C" zb_status_t zb_ctx_create(const zb_model_cfg_t* cfg, void* arena, siz
 
 extern "C" zb_status_t zb_ctx_destroy(zb_ctx_t* ctx) {
   ZB_TRY {
-    if (ctx) delete reinterpret_cast<Ctx*>(ctx);
+    if (ctx) {
+      // queued work still writes into the caller's arena: drain it before the caller may
+      // free / reuse the memory (a fault here is reported by the next CUDA call, not thrown)
+      Ctx* c = reinterpret_cast<Ctx*>(ctx);
+      (void)cudaStreamSynchronize(c->stream);
+      delete c;
+    }
     return ZB_OK;
   }
   ZB_CATCH
@@ -262,6 +300,7 @@ extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, 
   ZB_TRY {
     Ctx* c = C_(ctx);
     if (!passes || n <= 0) return set_error(ZB_EINVAL, "no passes");
+    check_stage_passes(passes, n, c->cfg.stage, c->cfg.m, static_cast<int>(c->slots.size()));
     if (c->comm) {
       run_iteration_nccl(*c, passes, n, tokens, labels, flags);
       return ZB_OK;
@@ -274,7 +313,7 @@ extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, 
     for (int i = 0; i < n; ++i) {
       const zb_pass_t& q = passes[i];
       if (q.stage != c->cfg.stage) continue;
-      if (flags & ZB_RUN_TIMING) c->timing_begin(c->n_timed);
+      if (flags & ZB_RUN_TIMING) c->timing_begin(c->n_timed, q.kind);
       if (q.kind == ZB_F)
         c->forward(q.microbatch, q.slot, tokens + static_cast<int64_t>(q.microbatch) * T, nullptr,
                    labels + static_cast<int64_t>(q.microbatch) * T);
@@ -307,7 +346,10 @@ extern "C" zb_status_t zb_run_iteration_worker(zb_ctx_t* const* chunks, int32_t 
   ZB_TRY {
     if (!chunks || k < 1 || !passes || n <= 0) return set_error(ZB_EINVAL, "bad arguments");
     std::vector<Ctx*> cs(k);
-    for (int i = 0; i < k; ++i) cs[i] = C_(chunks[i]);
+    for (int i = 0; i < k; ++i) {
+      cs[i] = C_(chunks[i]);
+      check_stage_passes(passes, n, cs[i]->cfg.stage, cs[i]->cfg.m, static_cast<int>(cs[i]->slots.size()));
+    }
     run_iteration_worker(cs, passes, n, tokens, labels, flags);
     return ZB_OK;
   }
@@ -329,6 +371,10 @@ extern "C" zb_status_t zb_run_iteration_local(zb_ctx_t* const* ctxs, int32_t p, 
       if (c[s]->stream != c[0]->stream) return set_error(ZB_EINVAL, "local stages must share one stream");
     }
     const int m = c[0]->cfg.m, T = c[0]->T;
+    for (int s = 0; s < p; ++s) {
+      if (c[s]->cfg.m != m) return set_error(ZB_EINVAL, "stages disagree on m");
+      check_stage_passes(passes, n, s, m, static_cast<int>(c[s]->slots.size()));
+    }
     std::vector<std::vector<const zb_pass_t*>> L(p);
     for (int i = 0; i < n; ++i) {
       if (passes[i].stage < 0 || passes[i].stage >= p) return set_error(ZB_EINVAL, "pass stage out of range");
@@ -376,7 +422,7 @@ extern "C" zb_status_t zb_run_iteration_local(zb_ctx_t* const* ctxs, int32_t p, 
             ready = done[ZB_B][s][j];
           if (!ready) break;
           Ctx& cs = *c[s];
-          if (flags & ZB_RUN_TIMING) cs.timing_begin(cs.n_timed);
+          if (flags & ZB_RUN_TIMING) cs.timing_begin(cs.n_timed, q.kind);
           if (q.kind == ZB_F) {
             const void* in = s == 0 ? static_cast<const void*>(tokens + static_cast<int64_t>(j) * T)
                                     : cs.slots[q.slot].L[0].x;
@@ -421,6 +467,41 @@ extern "C" zb_status_t zb_ctx_read_stats(zb_ctx_t* ctx, zb_iter_stats_t* st) {
   ZB_CATCH
 }
 
+// a1 "Profile": per-kind pass durations of the ZB_RUN_TIMING runs since the last
+// reset, medians in integer nanoseconds (the unit zb_schedule_per_stage takes).
+extern "C" zb_status_t zb_ctx_profile(zb_ctx_t* ctx, int32_t reset, int64_t* T_ns, int32_t* n_samples) {
+  ZB_TRY {
+    Ctx* c = C_(ctx);
+    if (reset) {
+      for (auto& v : c->prof_ns) v.clear();
+      c->prof_collected_run = c->timed_runs;
+      return ZB_OK;
+    }
+    if (!T_ns) return set_error(ZB_EINVAL, "null output");
+    ZB_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->timed_runs != c->prof_collected_run) {  // each timed run is collected once
+      for (int i = 0; i < c->n_timed; ++i) {
+        float ms = 0.f;
+        ZB_CUDA(cudaEventElapsedTime(&ms, c->ev_start[i], c->ev_end[i]));
+        c->prof_ns[c->ev_kind[i]].push_back(static_cast<int64_t>(static_cast<double>(ms) * 1e6 + 0.5));
+      }
+      c->prof_collected_run = c->timed_runs;
+    }
+    for (int k = 0; k < 3; ++k) {
+      std::vector<int64_t> v = c->prof_ns[k];
+      int64_t med = 0;
+      if (!v.empty()) {
+        std::sort(v.begin(), v.end());
+        med = v.size() % 2 ? v[v.size() / 2] : (v[v.size() / 2 - 1] + v[v.size() / 2]) / 2;
+      }
+      T_ns[k] = med;
+      if (n_samples) n_samples[k] = static_cast<int32_t>(v.size());
+    }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 // ------------------------------------------------------------------ optimizer / post-validation
 extern "C" zb_status_t zb_post_validate_step(zb_ctx_t* ctx, const zb_optim_cfg_t* o) {
   ZB_TRY {
@@ -449,7 +530,7 @@ extern "C" zb_status_t zb_post_validate_step(zb_ctx_t* ctx, const zb_optim_cfg_t
     } else {
       pv_decide_first(c->pv, o->clip, 0, c->stream);
     }
-    pv_apply(*c, *o);
+    pv_apply(*c, *o, false);
     if (c->comm && o->mode == ZB_OPT_PV) {  // validated inside the next iteration (or by _finish)
       c->pv_pending = true;
       c->pv_clip = o->clip;
@@ -476,7 +557,7 @@ extern "C" zb_status_t zb_post_validate_finish(zb_ctx_t* ctx, const zb_optim_cfg
       copy_full(*c, *c, true);
     }
     pv_decide_final(c->pv, o->clip, c->stream);
-    pv_apply(*c, *o);
+    pv_apply(*c, *o, true);
     return ZB_OK;
   }
   ZB_CATCH
@@ -487,7 +568,12 @@ extern "C" zb_status_t zb_post_validate_local(zb_ctx_t* const* ctxs, int32_t p, 
     check_opt(o);
     if (!ctxs || p < 1) return set_error(ZB_EINVAL, "bad arguments");
     std::vector<Ctx*> c(p);
-    for (int s = 0; s < p; ++s) c[s] = C_(ctxs[s]);
+    for (int s = 0; s < p; ++s) {
+      c[s] = C_(ctxs[s]);
+      if (c[s]->cfg.stage != s || c[s]->cfg.p != p) return set_error(ZB_EINVAL, "ctxs must be stages 0..p-1");
+      // the partial / full state moves between contexts with stream-ordered copies
+      if (c[s]->stream != c[0]->stream) return set_error(ZB_EINVAL, "local stages must share one stream");
+    }
     // partial chain 1 -> p (stage order summation)
     for (int s = 0; s < p; ++s) {
       pv_local(*c[s]);
@@ -500,7 +586,7 @@ extern "C" zb_status_t zb_post_validate_local(zb_ctx_t* const* ctxs, int32_t p, 
       pv_combine(c[s]->pv, c[s]->stream);
       if (o->mode == ZB_OPT_PV) {
         pv_decide_first(c[s]->pv, o->clip, 0, c[s]->stream);
-        pv_apply(*c[s], *o);
+        pv_apply(*c[s], *o, false);
       }
     }
     if (o->mode == ZB_OPT_SYNC) {  // all-reduced state first, then the conditioned step
@@ -512,7 +598,7 @@ extern "C" zb_status_t zb_post_validate_local(zb_ctx_t* const* ctxs, int32_t p, 
                                   cudaMemcpyDeviceToDevice, c[s]->stream));
         }
         pv_decide_first(c[s]->pv, o->clip, 1, c[s]->stream);
-        pv_apply(*c[s], *o);
+        pv_apply(*c[s], *o, false);
       }
       return ZB_OK;
     }
@@ -520,7 +606,7 @@ extern "C" zb_status_t zb_post_validate_local(zb_ctx_t* const* ctxs, int32_t p, 
     for (int s = p - 1; s >= 0; --s) {
       copy_full(*c[p - 1], *c[s], true);
       pv_decide_final(c[s]->pv, o->clip, c[s]->stream);
-      pv_apply(*c[s], *o);
+      pv_apply(*c[s], *o, true);
     }
     return ZB_OK;
   }

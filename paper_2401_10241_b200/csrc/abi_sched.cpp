@@ -56,34 +56,76 @@ static zb_status_t fill(const sched::Lists& lists, const std::vector<int64_t>& t
   return ZB_OK;
 }
 
+static zb_status_t schedule_impl(int32_t p, int32_t m, const std::vector<int64_t>& tf,
+                                 const std::vector<int64_t>& tb, const std::vector<int64_t>& tw, int64_t T_comm,
+                                 int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family, zb_pass_t* out,
+                                 int32_t out_cap, zb_sim_t* sim) {
+  for (int s = 0; s < p; ++s)
+    if (tf[s] < 0 || tb[s] < 0 || tw[s] < 0) return set_error(ZB_EINVAL, "times and memory must be >= 0");
+  if (T_comm < 0 || M_B < 0 || M_W < 0) return set_error(ZB_EINVAL, "times and memory must be >= 0");
+  if (out != nullptr && static_cast<int64_t>(out_cap) < 3LL * p * m) return set_error(ZB_ECAP, "out_cap < 3*p*m");
+  sched::Lists lists;
+  int chosen = -1;
+  bool fused = false;
+  switch (family) {
+    case ZB_1F1B: lists = sched::build_1f1b(p, m); fused = true; break;
+    case ZB_H1: lists = sched::build_zbh1(p, m); chosen = 4; break;
+    case ZB_H2: lists = sched::build_zbh2(p, m); chosen = 5; break;
+    case ZB_AUTO:
+      if (M_limit < M_B) return set_error(ZB_ELIMIT, "AUTO needs M_limit >= M_B");
+      lists = sched::auto_schedule(p, m, tf, tb, tw, T_comm, M_B, M_W, M_limit, &chosen);
+      break;
+    default: return set_error(ZB_EINVAL, "unknown family");
+  }
+  if (family != ZB_AUTO && M_limit > 0) {
+    auto pk = sched::memory_peaks(lists, M_B, M_W);
+    if (*std::max_element(pk.begin(), pk.end()) > M_limit)
+      return set_error(ZB_ELIMIT, "family peak memory exceeds M_limit");
+  }
+  return fill(lists, tf, tb, tw, T_comm, fused, M_B, M_W, chosen, out, out_cap, sim);
+}
+
 extern "C" zb_status_t zb_schedule(int32_t p, int32_t m, int64_t T_F, int64_t T_B, int64_t T_W, int64_t T_comm,
                                    int64_t M_limit, int64_t M_B, int64_t M_W, int32_t family, zb_pass_t* out,
                                    int32_t out_cap, zb_sim_t* sim) {
   ZB_TRY {
     if (p < 1 || p > ZB_MAX_STAGES || m < 1) return set_error(ZB_EINVAL, "need 1 <= p <= 64 and m >= 1");
-    if (T_F < 0 || T_B < 0 || T_W < 0 || T_comm < 0 || M_B < 0 || M_W < 0)
-      return set_error(ZB_EINVAL, "times and memory must be >= 0");
-    if (out != nullptr && static_cast<int64_t>(out_cap) < 3LL * p * m) return set_error(ZB_ECAP, "out_cap < 3*p*m");
-    sched::Lists lists;
-    int chosen = -1;
-    bool fused = false;
-    switch (family) {
-      case ZB_1F1B: lists = sched::build_1f1b(p, m); fused = true; break;
-      case ZB_H1: lists = sched::build_zbh1(p, m); chosen = 4; break;
-      case ZB_H2: lists = sched::build_zbh2(p, m); chosen = 5; break;
-      case ZB_AUTO:
-        if (M_limit < M_B) return set_error(ZB_ELIMIT, "AUTO needs M_limit >= M_B");
-        lists = sched::auto_schedule(p, m, T_F, T_B, T_W, T_comm, M_B, M_W, M_limit, &chosen);
-        break;
-      default: return set_error(ZB_EINVAL, "unknown family");
+    return schedule_impl(p, m, std::vector<int64_t>(p, T_F), std::vector<int64_t>(p, T_B),
+                         std::vector<int64_t>(p, T_W), T_comm, M_limit, M_B, M_W, family, out, out_cap, sim);
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_schedule_per_stage(int32_t p, int32_t m, const int64_t* T_F, const int64_t* T_B,
+                                             const int64_t* T_W, int64_t T_comm, int64_t M_limit, int64_t M_B,
+                                             int64_t M_W, int32_t family, zb_pass_t* out, int32_t out_cap,
+                                             zb_sim_t* sim) {
+  ZB_TRY {
+    if (p < 1 || p > ZB_MAX_STAGES || m < 1) return set_error(ZB_EINVAL, "need 1 <= p <= 64 and m >= 1");
+    if (!T_F || !T_B || !T_W) return set_error(ZB_EINVAL, "null per-stage time array");
+    return schedule_impl(p, m, std::vector<int64_t>(T_F, T_F + p), std::vector<int64_t>(T_B, T_B + p),
+                         std::vector<int64_t>(T_W, T_W + p), T_comm, M_limit, M_B, M_W, family, out, out_cap, sim);
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_partition(int32_t L, int32_t p, int32_t* layers) {
+  ZB_TRY {
+    if (p < 1 || p > ZB_MAX_STAGES || L < p || !layers) return set_error(ZB_EINVAL, "need 1 <= p <= min(L, 64)");
+    if (p == 1) {
+      layers[0] = L;
+    } else if ((L + 2) % p == 0 && (L + 2) / p >= 2) {  // first and last stage one layer fewer
+      const int mid = (L + 2) / p;
+      for (int s = 0; s < p; ++s) layers[s] = (s == 0 || s == p - 1) ? mid - 1 : mid;
+    } else {  // even split, remainder to the middle stages first, then stage 0, then p-1
+      for (int s = 0; s < p; ++s) layers[s] = L / p;
+      std::vector<int> order;
+      for (int s = 1; s < p - 1; ++s) order.push_back(s);
+      order.push_back(0);
+      order.push_back(p - 1);
+      for (int i = 0; i < L % p; ++i) layers[order[i % p]] += 1;
     }
-    if (family != ZB_AUTO && M_limit > 0) {
-      auto pk = sched::memory_peaks(lists, M_B, M_W);
-      if (*std::max_element(pk.begin(), pk.end()) > M_limit)
-        return set_error(ZB_ELIMIT, "family peak memory exceeds M_limit");
-    }
-    std::vector<int64_t> tf(p, T_F), tb(p, T_B), tw(p, T_W);
-    return fill(lists, tf, tb, tw, T_comm, fused, M_B, M_W, chosen, out, out_cap, sim);
+    return ZB_OK;
   }
   ZB_CATCH
 }

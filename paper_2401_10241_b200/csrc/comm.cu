@@ -523,7 +523,6 @@ struct StageExec {
       }
       case plan::OP_F:
       case plan::OP_REPLAY_F: {
-        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed);
         void* out = nullptr;
         if (!c.last) {
           last_act_buf = act_ring;
@@ -531,6 +530,7 @@ struct StageExec {
           out = cm.act_buf[act_ring];
           act_ring = (act_ring + 1) % static_cast<int>(cm.act_buf.size());
         }
+        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed, ZB_F);  // after the waits: pass time only
         const void* in = c.first ? static_cast<const void*>(tokens + static_cast<int64_t>(op.mb) * T) : sl->L[0].x;
         c.forward(op.mb, op.slot, in, out, c.last ? labels + static_cast<int64_t>(op.mb) * T : nullptr);
         if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
@@ -549,7 +549,6 @@ struct StageExec {
         break;
       }
       case plan::OP_B: {
-        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed);
         float* dx = nullptr;
         if (!c.first) {
           last_grad_buf = grad_ring;
@@ -557,6 +556,7 @@ struct StageExec {
           dx = cm.grad_buf[grad_ring];
           grad_ring = (grad_ring + 1) % static_cast<int>(cm.grad_buf.size());
         }
+        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed, ZB_B);
         c.backward_input(op.mb, op.slot, c.last ? nullptr : sl->dy32, dx);
         if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
         break;
@@ -568,7 +568,7 @@ struct StageExec {
         break;
       }
       case plan::OP_W: {
-        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed);
+        if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed, ZB_W);
         c.backward_weight(op.mb, op.slot);
         if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
         break;
@@ -600,7 +600,7 @@ void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* t
     pv_send_full(c);
     pv_decide_final(c.pv, c.pv_clip, c.stream);
     adamw_apply(c.theta, c.m, c.v, c.grad, c.shadow, c.n_total, c.n_wd, c.shadow ? c.n_shadow : 0, c.pv_opt[0],
-                c.pv_opt[1], c.pv_opt[2], c.pv_opt[3], c.pv_opt[4], c.pv, c.stream);
+                c.pv_opt[1], c.pv_opt[2], c.pv_opt[3], c.pv_opt[4], c.pv, true, c.stream);
     pv_finish_apply(c.pv, c.stream);
     c.pv_pending = false;
     // the host needs the outcome to know whether the speculative Fs must be replayed

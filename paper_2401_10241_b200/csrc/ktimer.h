@@ -18,7 +18,8 @@ namespace ktimer {
 // BIAS_GRAD, CE, OPT, MISC) carry algorithmic BYTES in the same field.
 enum Class : int {
   GEMM = 0, ATTN_FWD = 1, ATTN_BWD = 2, GEMM_F = 3, GEMM_B = 4, GEMM_W = 5,
-  LN_FWD = 6, LN_BWD = 7, LN_PARAM = 8, BIAS_GRAD = 9, CE = 10, OPT = 11, MISC = 12, N_CLASSES = 13
+  LN_FWD = 6, LN_BWD = 7, LN_PARAM = 8, BIAS_GRAD = 9, CE = 10, OPT = 11, MISC = 12, OPT_VALIDATE = 13,
+  N_CLASSES = 14
 };
 
 bool enabled();

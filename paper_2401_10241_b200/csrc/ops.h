@@ -67,9 +67,10 @@ void pv_decide_first(PvState* st, float clip, int sync_mode, cudaStream_t s);
 void pv_decide_final(PvState* st, float clip, cudaStream_t s);
 // Algorithm 1 over the flat parameter space, predicated on st->adam_mode.
 // Elements [0, n_wd) decay with weight_decay; [n_shadow) also refresh the bf16 shadow.
+// validation: the launch of the validation pass (zb_post_validate_finish) — timed separately.
 void adamw_apply(float* theta, float* m, float* v, const float* g, bf16* shadow, int64_t n, int64_t n_wd,
                  int64_t n_shadow, float lr, float b1, float b2, float eps, float wd, const PvState* st,
-                 cudaStream_t s);
+                 bool validation, cudaStream_t s);
 void pv_finish_apply(PvState* st, cudaStream_t s);  // advance t per the applied mode
 
 }  // namespace zb

@@ -183,8 +183,9 @@ std::vector<std::vector<int>> assign_slots(const Lists& lists, std::vector<int>*
 }
 
 // AUTO heuristic, one reading of §3.1; see DESIGN.md R-auto.
-Lists heuristic(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, int64_t MB, int64_t MW, int64_t Mlimit,
-                bool fill_warmup, bool skip_lead) {
+Lists heuristic(int p, int m, const std::vector<int64_t>& TF, const std::vector<int64_t>& TB,
+                const std::vector<int64_t>& TW, int64_t Tc, int64_t MB, int64_t MW, int64_t Mlimit, bool fill_warmup,
+                bool skip_lead) {
   if (Mlimit < MB) throw std::invalid_argument("M_limit below M_B");
   const int64_t UNKNOWN = -1, NA = -2;  // arrival states; >= 0 means known time
   std::vector<int> nF(p, 0), nB(p, 0), nW(p, 0);
@@ -230,7 +231,7 @@ Lists heuristic(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, in
         if (Bready) {
           pick = KIND_B;
         } else if (Fready) {
-          bool delays = (known(aB) && aB < t + TF) || (aB == UNKNOWN && TB + Tc < TF);
+          bool delays = (known(aB) && aB < t + TF[s]) || (aB == UNKNOWN && TB[s] + Tc < TF[s]);
           if (!delays || fill_warmup) pick = KIND_F;
         }
       } else {
@@ -258,7 +259,7 @@ Lists heuristic(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, in
             any_other = true;
           }
         if (!any_other) others = 0;
-        const bool gap_ok = !have_r || (r - t >= TW);
+        const bool gap_ok = !have_r || (r - t >= TW[s]);
         if ((nF[s] < m && mem[s] + MB > Mlimit && !Bready) || gap_ok || (nF[s] == m && nB[s] == m)) {
           pick = KIND_W;
         } else if (have_r && r > t && bub[s] + (r - t) > others) {
@@ -271,21 +272,21 @@ Lists heuristic(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, in
       int j;
       if (pick == KIND_F) {
         j = nF[s]++;
-        endF[s][j] = t + TF;
+        endF[s][j] = t + TF[s];
         mem[s] += MB;
-        busy[s] = t + TF;
+        busy[s] = t + TF[s];
       } else if (pick == KIND_B) {
         j = nB[s]++;
-        endB[s][j] = t + TB;
+        endB[s][j] = t + TB[s];
         mem[s] += MW - MB;
         pend[s].push_back(j);
-        busy[s] = t + TB;
+        busy[s] = t + TB[s];
       } else {
         j = pend[s].front();
         pend[s].pop_front();
         ++nW[s];
         mem[s] -= MW;
-        busy[s] = t + TW;
+        busy[s] = t + TW[s];
       }
       last[s] = pick;
       lists[s].push_back({pick, j});
@@ -315,8 +316,8 @@ Lists heuristic(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, in
   return lists;
 }
 
-Lists auto_schedule(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, int64_t MB, int64_t MW,
-                    int64_t Mlimit, int* chosen) {
+Lists auto_schedule(int p, int m, const std::vector<int64_t>& tf, const std::vector<int64_t>& tb,
+                    const std::vector<int64_t>& tw, int64_t Tc, int64_t MB, int64_t MW, int64_t Mlimit, int* chosen) {
   struct Cand {
     int idx;
     Lists l;
@@ -324,7 +325,7 @@ Lists auto_schedule(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc
   std::vector<Cand> cands;
   for (int fill = 0; fill < 2; ++fill)
     for (int skip = 0; skip < 2; ++skip)
-      cands.push_back({2 * fill + skip, heuristic(p, m, TF, TB, TW, Tc, MB, MW, Mlimit, fill, skip)});
+      cands.push_back({2 * fill + skip, heuristic(p, m, tf, tb, tw, Tc, MB, MW, Mlimit, fill, skip)});
   {
     Lists h1 = build_zbh1(p, m);
     auto pk = memory_peaks(h1, MB, MW);
@@ -333,7 +334,6 @@ Lists auto_schedule(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc
     pk = memory_peaks(h2, MB, MW);
     if (*std::max_element(pk.begin(), pk.end()) <= Mlimit) cands.push_back({5, h2});
   }
-  std::vector<int64_t> tf(p, TF), tb(p, TB), tw(p, TW);
   int best = -1;
   int64_t bc = 0, bp = 0;
   int bi = 0;

@@ -358,14 +358,17 @@ void Ctx::backward_weight(int mb, int slot_idx) {
   first_w_done = true;
 }
 
-void Ctx::timing_begin(int idx) {
+void Ctx::timing_begin(int idx, int kind) {
   while (static_cast<int>(ev_start.size()) <= idx) {
     cudaEvent_t a, b;
     ZB_CUDA(cudaEventCreate(&a));
     ZB_CUDA(cudaEventCreate(&b));
     ev_start.push_back(a);
     ev_end.push_back(b);
+    ev_kind.push_back(0);
   }
+  ev_kind[idx] = kind;
+  if (idx == 0) ++timed_runs;
   ZB_CUDA(cudaEventRecord(ev_start[idx], stream));
 }
 void Ctx::timing_end(int idx) { ZB_CUDA(cudaEventRecord(ev_end[idx], stream)); }

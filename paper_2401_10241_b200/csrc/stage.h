@@ -91,9 +91,13 @@ struct Ctx {
   float pv_clip = 1.f;
   float pv_opt[5] = {0, 0, 0, 0, 0};  // lr, beta1, beta2, eps, weight_decay of the pending step
 
-  // timing (ZB_RUN_TIMING)
+  // timing (ZB_RUN_TIMING): events around every pass of the last timed run, the pass
+  // kinds, and the per-kind durations collected by zb_ctx_profile (a1)
   std::vector<cudaEvent_t> ev_start, ev_end;
+  std::vector<int> ev_kind;
   int n_timed = 0;
+  std::vector<int64_t> prof_ns[3];
+  int64_t timed_runs = 0, prof_collected_run = 0;  // a timed run starts at pass index 0
 
   std::unique_ptr<Comm> comm;
 
@@ -104,7 +108,7 @@ struct Ctx {
   void backward_input(int mb, int slot, const void* dy, void* dx);
   void backward_weight(int mb, int slot);
 
-  void timing_begin(int idx);
+  void timing_begin(int idx, int kind);
   void timing_end(int idx);
 };
 

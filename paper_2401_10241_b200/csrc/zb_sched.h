@@ -23,10 +23,12 @@ struct SimResult {
 Lists build_1f1b(int p, int m);
 Lists build_zbh1(int p, int m);
 Lists build_zbh2(int p, int m);
-Lists heuristic(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, int64_t MB, int64_t MW, int64_t Mlimit,
-                bool fill_warmup, bool skip_lead);
-Lists auto_schedule(int p, int m, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, int64_t MB, int64_t MW,
-                    int64_t Mlimit, int* chosen);
+// per-stage times TF[p], TB[p], TW[p] (each stage's profiled times feed the scheduler)
+Lists heuristic(int p, int m, const std::vector<int64_t>& TF, const std::vector<int64_t>& TB,
+                const std::vector<int64_t>& TW, int64_t Tc, int64_t MB, int64_t MW, int64_t Mlimit, bool fill_warmup,
+                bool skip_lead);
+Lists auto_schedule(int p, int m, const std::vector<int64_t>& TF, const std::vector<int64_t>& TB,
+                    const std::vector<int64_t>& TW, int64_t Tc, int64_t MB, int64_t MW, int64_t Mlimit, int* chosen);
 SimResult simulate(const Lists& lists, const std::vector<int64_t>& TF, const std::vector<int64_t>& TB,
                    const std::vector<int64_t>& TW, int64_t Tcomm, bool fused);
 std::vector<int64_t> memory_peaks(const Lists& lists, int64_t MB, int64_t MW);

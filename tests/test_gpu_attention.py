@@ -5,16 +5,13 @@ on the same (bf16-rounded) inputs; head dims of every config (64 tiny, 96
 import numpy as np
 import pytest
 
-from zbtest_util import cuda_available
+from zbtest_util import assert_close, cuda_available
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA GPU")]
 
 CASES = [(1, 1024, 1, 64), (2, 256, 3, 64), (2, 192, 2, 96), (1, 256, 2, 128), (2, 200, 2, 96), (1, 130, 1, 128),
          (2, 384, 2, 96), (1, 1024, 2, 128), (3, 128, 1, 96)]
 
-
-def rel(x, ref):
-    return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-30))
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
@@ -51,13 +48,13 @@ def test_attention_parity(shape, dtype):
     dqkv_ref = om.causal_attention_bwd(dO, Q, P, b, s, a)
     ftol = 1e-5 if dtype == "f32" else 1e-2
     btol = 1e-5 if dtype == "f32" else 2e-2
-    assert rel(o.double().cpu().numpy(), O_ref) < ftol
-    assert rel(lse.double().cpu().numpy(), lse_ref) < 1e-5
+    assert_close(o.double().cpu().numpy(), O_ref, ftol, "O")
+    assert_close(lse.double().cpu().numpy(), lse_ref, 1e-5, "LSE")
     got = dqkv.double().cpu().numpy()
     assert np.isfinite(got).all()
     for i, name in enumerate("QKV"):
         blk = slice(i * h, (i + 1) * h)
-        assert rel(got[:, blk], dqkv_ref[:, blk]) < btol, name
+        assert_close(got[:, blk], dqkv_ref[:, blk], btol, "d" + name)
 
 
 @pytest.mark.parametrize("d", [96, 128])
@@ -83,4 +80,4 @@ def test_attention_fwd_divergent_lazy_rescale(d):
     api.dbg_attention_fwd(qkv, o, lse, b=b, s=s, a=a, d=d)
     torch.cuda.synchronize()
     O_ref, _ = om.causal_attention_fwd(qkv.double().cpu().numpy(), b, s, a)
-    assert rel(o.double().cpu().numpy(), O_ref) < 1e-2
+    assert_close(o.double().cpu().numpy(), O_ref, 1e-2, "O")

@@ -24,3 +24,16 @@ def test_full_width_layer_vs_oracle_and_repeatable(name):
     loss2, grads2, _ = gpu_run(cfg, 1, "bf16")
     assert loss2 == loss
     assert all(np.array_equal(grads[k], grads2[k]) for k in grads)
+
+
+@pytest.mark.parametrize("name", ["1.5B", "6.2B"])
+def test_full_width_multi_microbatch_two_stages_vs_oracle(name):
+    """The bench widths with b = 2 sequences per microbatch (b-batched attention),
+    m = 2 microbatches (the second W accumulates into the f32 grads with beta = 1
+    through the ordered split-K reduce-add) and p = 2 virtual stages (the f32
+    stage-boundary gradient, R-grad32), ZB-H1: loss and every gradient against
+    the fp64 oracle (normwise and elementwise)."""
+    cfg = zb_synth.CONFIGS[name].with_(L=2, b=2, m=2)
+    ref_loss, ref = oracle_grads(cfg, "bf16")
+    loss, grads, _ = gpu_run(cfg, 2, "bf16")
+    check_tolerance(loss, grads, ref_loss, ref, "bf16")

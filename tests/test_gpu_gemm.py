@@ -5,7 +5,7 @@ operand-major combination the stage passes use (gemm.h)."""
 import numpy as np
 import pytest
 
-from zbtest_util import cuda_available
+from zbtest_util import assert_close, cuda_available
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA GPU")]
 
@@ -18,9 +18,6 @@ def _gelu_grad(x):
     t = np.tanh(np.sqrt(2 / np.pi) * (x + 0.044715 * x ** 3))
     return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * np.sqrt(2 / np.pi) * (1 + 3 * 0.044715 * x * x)
 
-
-def rel(x, ref):
-    return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-30))
 
 
 CASES = [
@@ -77,10 +74,10 @@ def test_gemm_parity(case, dtype):
         got = Cbuf.double().cpu().numpy()
         want = ref + (C0 if (epi == 4 and beta) else 0)
         tol = 1e-5 if (dtype == "f32" or f32_out) else 6e-3
-        assert rel(got, want) < tol, (beta, rel(got, want))
+        assert_close(got, want, tol, f"C beta={beta}")
         if epi == 1:
             gg = aux.double().cpu().numpy()
-            assert rel(gg, _gelu(ref)) < (1e-5 if dtype == "f32" else 6e-3)
+            assert_close(gg, _gelu(ref), 1e-5 if dtype == "f32" else 6e-3, "GeLU aux")
 
 
 def test_split_k_w_is_deterministic():

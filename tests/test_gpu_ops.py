@@ -8,13 +8,10 @@ two-phase column reductions."""
 import numpy as np
 import pytest
 
-from zbtest_util import cuda_available
+from zbtest_util import assert_close, cuda_available
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA GPU")]
 
-
-def rel(x, ref):
-    return float(np.linalg.norm(np.ravel(x) - np.ravel(ref)) / max(np.linalg.norm(ref), 1e-30))
 
 
 LN_SHAPES = [(6144, 2304), (3072, 4096), (1024, 6144), (37, 64), (2000, 264), (300, 2304)]
@@ -49,12 +46,12 @@ def test_layernorm_fwd_bwd(rows, h, dtype):
     api.dbg_layernorm_bwd(DY, X, mean, rs, G, dx, gg, gb, rows=rows, h=h, resid=R, dx32=dx32, beta=1)
     torch.cuda.synchronize()
     ftol = 1e-5 if dtype == "f32" else 8e-3
-    assert rel(Y.double().cpu().numpy(), y_ref) < ftol
-    assert rel(rs.double().cpu().numpy(), rstd[:, 0]) < 1e-5
-    assert rel(dx32.double().cpu().numpy(), dx_ref) < 1e-5
-    assert rel(dx.double().cpu().numpy(), dx_ref) < ftol
-    assert rel(gg.double().cpu().numpy(), gg_ref + 3.0) < 1e-5
-    assert rel(gb.double().cpu().numpy(), gb_ref - 2.0) < 1e-5
+    assert_close(Y.double().cpu().numpy(), y_ref, ftol, "LN y")
+    assert_close(rs.double().cpu().numpy(), rstd[:, 0], 1e-5, "LN rstd")
+    assert_close(dx32.double().cpu().numpy(), dx_ref, 1e-5, "LN dx f32")
+    assert_close(dx.double().cpu().numpy(), dx_ref, ftol, "LN dx")
+    assert_close(gg.double().cpu().numpy(), gg_ref + 3.0, 1e-5, "LN dgamma")
+    assert_close(gb.double().cpu().numpy(), gb_ref - 2.0, 1e-5, "LN dbeta")
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
@@ -73,8 +70,8 @@ def test_bias_grad(rows, n, ld, dtype):
     o1 = out.clone()
     api.dbg_bias_grad(Y, out, rows=rows, n=n, ldy=ld, beta=0)
     torch.cuda.synchronize()
-    assert rel(o1.double().cpu().numpy(), ref + 1.5) < 1e-5
-    assert rel(out.double().cpu().numpy(), ref) < 1e-5
+    assert_close(o1.double().cpu().numpy(), ref + 1.5, 1e-5, "bias grad beta=1")
+    assert_close(out.double().cpu().numpy(), ref, 1e-5, "bias grad beta=0")
     again = torch.empty_like(out)
     api.dbg_bias_grad(Y, again, rows=rows, n=n, ldy=ld, beta=0)
     torch.cuda.synchronize()

@@ -130,3 +130,103 @@ def test_post_validation_equals_sync(name, p, iters, faults, scale):
                 assert np.allclose(b.theta[k], a.theta[k], rtol=1e-12, atol=1e-15), k
                 assert np.allclose(b.m[k], a.m[k], rtol=1e-12, atol=1e-15)
                 assert np.allclose(b.v[k], a.v[k], rtol=1e-12, atol=1e-18)
+
+
+# ------------------------------------------------------------------ independent pins of the global state
+# local_state / clip_coef / sync_step ("gradient clipping ... global norm ... NaN/INF
+# check") are pinned against torch's own implementations — torch.nn.utils.clip_grad_norm_
+# (global 2-norm, coef = max_norm / (norm + 1e-6) clamped to 1) and torch.optim.AdamW
+# (decoupled weight decay, bias-corrected moments) — an independent library, not a retyping.
+
+def _torch_sync_reference(params, grads, hyp, wd_of):
+    """torch CPU fp64: clip_grad_norm_ over ALL stages' grads, skip on a
+    non-finite norm, else torch.optim.AdamW.step() with per-tensor weight decay."""
+    import torch
+    names = [k for st in params for k in st]
+    flat_p = {k: v for st in params for k, v in st.items()}
+    flat_g = {k: v for st in grads for k, v in st.items()}
+    tp = {k: torch.nn.Parameter(torch.tensor(flat_p[k], dtype=torch.float64)) for k in names}
+    for k in names:
+        tp[k].grad = torch.tensor(flat_g[k], dtype=torch.float64)
+    norm = torch.nn.utils.clip_grad_norm_([tp[k] for k in names], max_norm=hyp.clip, error_if_nonfinite=False,
+                                          foreach=False)
+    groups = {}
+    for k in names:
+        groups.setdefault(wd_of(k, flat_p[k].shape), []).append(tp[k])
+    opt = torch.optim.AdamW([{"params": v, "weight_decay": w} for w, v in groups.items()], lr=hyp.lr,
+                            betas=(hyp.beta1, hyp.beta2), eps=hyp.eps, foreach=False)
+    stepped = bool(torch.isfinite(norm))
+    if stepped:
+        opt.step()
+    out = {}
+    for k in names:
+        st = opt.state.get(tp[k], {})
+        out[k] = (tp[k].detach().numpy(), st.get("exp_avg"), st.get("exp_avg_sq"))
+    return float(norm), stepped, out
+
+
+@pytest.mark.parametrize("case", ["clean", "clip", "nan", "inf"])
+def test_sync_step_matches_torch_clip_and_adamw(case):
+    rng = np.random.default_rng({"clean": 1, "clip": 2, "nan": 3, "inf": 4}[case])
+    p = 3
+    params = _make_stage_params(p, rng)
+    grads = _grads(params, rng, 0.05 if case != "clip" else 3.0)
+    if case == "nan":
+        grads[1]["s1.b"][2] = np.nan
+    if case == "inf":
+        grads[2]["s2.e"][0, 1] = -np.inf
+    hyp = oo.AdamWHyper(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, clip=1.0)
+    opts = [oo.StageOptimizer(pp, hyp) for pp in params]
+    action = oo.sync_step(opts, grads)
+    norm, stepped, ref = _torch_sync_reference(params, grads, hyp, lambda k, sh: oo.default_weight_decay(k, sh, 0.1))
+    # the oracle's global state against torch's total norm
+    S = sum(oo.local_state(g)[0] for g in grads)
+    nan = any(oo.local_state(g)[1] for g in grads)
+    assert nan == (not np.isfinite(norm))
+    if not nan:
+        assert abs(np.sqrt(S) - norm) <= 1e-13 * norm
+        assert (action == "clip") == (hyp.clip / (norm + 1e-6) < 1.0)
+        assert action == ("clip" if case == "clip" else "step")
+    else:
+        assert action == "skip" and not stepped
+    for o in opts:
+        assert o.t == (1 if stepped else 0)
+        for k in o.theta:
+            th, m, v = ref[k]
+            assert np.allclose(o.theta[k], th, rtol=1e-13, atol=1e-16), k
+            if stepped:
+                assert np.allclose(o.m[k], m.numpy(), rtol=1e-13, atol=1e-18), k
+                assert np.allclose(o.v[k], v.numpy(), rtol=1e-13, atol=1e-20), k
+            else:
+                assert np.array_equal(o.theta[k], params[[i for i in range(p) if k in params[i]][0]][k])
+
+
+def test_global_norm_hand_example():
+    """Gradients (3, 4) on one stage and (12,) on another: global norm 13
+    (P:149 'global gradient norm'); clip 1 -> coef 1 / (13 + 1e-6); clip 100 -> no clipping."""
+    g = [{"a": np.array([3.0, 4.0])}, {"b": np.array([12.0])}]
+    s = [oo.local_state(x) for x in g]
+    assert s[0] == (25.0, False) and s[1] == (144.0, False)
+    S = s[0][0] + s[1][0]
+    assert S == 169.0
+    assert oo.clip_coef(S, 1.0) == 1.0 / (13.0 + 1e-6)
+    assert oo.clip_coef(S, 100.0) > 1.0
+    assert oo.local_state({"a": np.array([1.0, np.nan])})[1] is True
+    assert oo.local_state({"a": np.array([np.inf])})[1] is True
+    # a sum of squares, not of absolute values or norms: (3,4) -> 25 (not 7, not 5)
+    assert oo.local_state({"a": np.array([3.0, -4.0])})[0] == 25.0
+
+
+def test_sync_step_clip_scales_gradient_by_coef():
+    """With lr small and fresh AdamW state, the first step's m = (1-b1) * coef * g:
+    the clipped gradient is recoverable and must equal clip_grad_norm_'s output."""
+    import torch
+    rng = np.random.default_rng(9)
+    g = {"w": rng.standard_normal((4, 3)) * 10.0}
+    hyp = oo.AdamWHyper(lr=1e-6, weight_decay=0.0, clip=1.0)
+    o = oo.StageOptimizer({"w": np.zeros((4, 3))}, hyp)
+    assert oo.sync_step([o], [g]) == "clip"
+    tg = torch.nn.Parameter(torch.zeros(4, 3, dtype=torch.float64))
+    tg.grad = torch.tensor(g["w"])
+    torch.nn.utils.clip_grad_norm_([tg], 1.0, foreach=False)
+    assert np.allclose(o.m["w"] / (1 - hyp.beta1), tg.grad.numpy(), rtol=1e-14, atol=0)

@@ -171,3 +171,64 @@ def test_chunked_errors():
         api.schedule_chunked("zbv", 4, 8, 3, 1, 1, 1)          # ZB-V needs 2 chunks
     with pytest.raises(ZbError):
         api.schedule_chunked("zbv", 40, 8, 2, 1, 1, 1)         # 80 virtual stages > 64
+
+
+def compare_per_stage(family, p, m, TF, TB, TW, Tc, MB, MW, lim):
+    passes, sim = api.schedule_per_stage(family, p, m, TF, TB, TW, Tc, M_limit=lim, M_B=MB, M_W=MW)
+    lists, maps, counts, osim, chosen = osch.schedule(family, p, m, list(TF), list(TB), list(TW), Tc, MB=MB, MW=MW,
+                                                      Mlimit=lim if (family == "auto" or lim > 0) else None)
+    assert api.stage_lists(passes, p) == [list(o) for o in lists], (family, p, m)
+    k = 0
+    for s in range(p):
+        for kind, j in lists[s]:
+            q = passes[k]
+            assert q.slot == maps[s][j]
+            assert q.start == osim["start"][(kind, s, j)] and q.end == osim["end"][(kind, s, j)]
+            k += 1
+    assert sim.cost == osim["cost"]
+    assert abs(sim.bubble_rate - osim["bubble_rate"]) < 1e-15
+    if family == "auto":
+        assert sim.chosen == chosen
+        assert max(sim.peak_bytes[:p]) <= lim
+    assert not osch.validate_schedule(lists, m)
+
+
+@pytest.mark.parametrize("family", ["1f1b", "zbh1", "zbh2", "auto"])
+def test_per_stage_times_grid(family):
+    """zb_schedule_per_stage (each stage's profiled times feed the scheduler):
+    heavier first / last stages (embedding, LM head) and random per-stage jitter."""
+    rnd = random.Random(7 + sum(map(ord, family)))
+    for p in (2, 3, 4, 8):
+        for m in sorted({p, 2 * p - 1, 3 * p}):
+            base = [rnd.randint(40, 100) for _ in range(3)]
+            TF = [base[0] + rnd.randint(0, 10) for _ in range(p)]
+            TB = [base[1] + rnd.randint(0, 15) for _ in range(p)]
+            TW = [base[2] + rnd.randint(0, 10) for _ in range(p)]
+            TB[-1] += rnd.randint(10, 40)            # LM head on the last stage
+            TF[0] += rnd.randint(0, 5)               # embedding on stage 0
+            Tc = rnd.randint(0, 4)
+            MB, MW = rnd.choice([(10, 10), (39, 32)])
+            lim = rnd.choice([p * MB, 2 * p * MB, 3 * p * MB]) if family == "auto" else 0
+            compare_per_stage(family, p, m, TF, TB, TW, Tc, MB, MW, lim)
+
+
+def test_per_stage_uniform_equals_scalar():
+    for p, m in ((4, 8), (8, 24)):
+        for fam in ("1f1b", "zbh1", "zbh2", "auto"):
+            a, sa = api.schedule(fam, p, m, 70, 90, 50, 3, M_limit=2 * p * 10, M_B=10, M_W=10)
+            b, sb = api.schedule_per_stage(fam, p, m, [70] * p, [90] * p, [50] * p, 3, M_limit=2 * p * 10, M_B=10,
+                                           M_W=10)
+            assert [(q.stage, q.microbatch, q.kind, q.slot, q.start, q.end) for q in a] == \
+                   [(q.stage, q.microbatch, q.kind, q.slot, q.start, q.end) for q in b]
+            assert sa.cost == sb.cost and sa.chosen == sb.chosen
+
+
+def test_partition_rule_in_library_matches_paper_rule():
+    """zb_partition == P:169's rule as written in the data module (first / last stage
+    one layer fewer when (L+2) % p == 0) for every (L, p) up to 80 x 64."""
+    import zb_synth
+    for L in range(1, 81):
+        for p in range(1, min(L, 64) + 1):
+            assert api.partition(L, p) == zb_synth.partition(L, p), (L, p)
+    assert api.partition(22, 8) == [2, 3, 3, 3, 3, 3, 3, 2]
+    assert api.partition(62, 8) == [7, 8, 8, 8, 8, 8, 8, 7]
