@@ -239,7 +239,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(0 if os.environ.get("ZB_SAME_DEVICE") == "1" else local)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
@@ -559,43 +559,21 @@ def gemm_traffic(model):
         return None, None
 
 
-def measure_tcomm_ns(rank, world, nbytes, iters=10):
-    """T_comm: one-way time of one boundary message (the f32 [T, h]
-    gradient) between adjacent stages, from a NCCL ping-pong over torch.distributed
-    (plumbing; the same link and size as the pipeline's P2P), max over pairs."""
+def dist_setup(local):
+    """torch.distributed plumbing: NCCL across GPUs; ZB_DIST_BACKEND=gloo (with
+    ZB_SAME_DEVICE=1 and ZB_NCCL_LIB = the 2-process / 1-GPU shim) runs N stages as N
+    processes on ONE device (tests/test_gpu_nccl_shim.py) — then the small collectives
+    of the bench move CPU tensors."""
     import torch
     import torch.distributed as dist
-    buf = torch.zeros(nbytes // 4, device="cuda")
-    best = []
-    for phase in (0, 1):                       # pairs (0,1),(2,3).. then (1,2),(3,4)..
-        partner = None
-        if (rank - phase) % 2 == 0 and rank + 1 < world and rank >= phase:
-            partner = rank + 1
-        elif (rank - phase) % 2 == 1 and rank - 1 >= phase:
-            partner = rank - 1
-        dist.barrier()
-        if partner is None:
-            continue
-        lead = rank < partner
-        times = []
-        for i in range(iters + 2):
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            if lead:
-                dist.send(buf, partner)
-                dist.recv(buf, partner)
-            else:
-                dist.recv(buf, partner)
-                dist.send(buf, partner)
-            e1.record()
-            torch.cuda.synchronize()
-            if i >= 2:
-                times.append(e0.elapsed_time(e1) / 2.0)
-        best.append(statistics.median(times))
-    t = torch.tensor([max(best) if best else 0.0], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return int(float(t) * 1e6)
+    backend = os.environ.get("ZB_DIST_BACKEND", "nccl")
+    dev = 0 if os.environ.get("ZB_SAME_DEVICE") == "1" else local
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        return "cuda"
+    dist.init_process_group(backend)
+    return "cpu"
 
 
 def run_pipeline(args, cfg, rank, world, local):
@@ -608,10 +586,10 @@ def run_pipeline(args, cfg, rank, world, local):
     from paper_2401_10241_b200._lib import lib
     import ctypes as C
 
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cdev = dist_setup(local)
     p, m = world, cfg.m
     mc = api.model_cfg(cfg, p, rank, m, 1, "bf16")
-    sb = torch.tensor([api.slot_bytes(mc)], device="cuda", dtype=torch.int64)
+    sb = torch.tensor([api.slot_bytes(mc)], device=cdev, dtype=torch.int64)
     dist.all_reduce(sb, op=dist.ReduceOp.MAX)
     slot_b = int(sb.item())
     lim = _mem_limit(cfg, args.family, p, slot_b)
@@ -664,7 +642,7 @@ def run_pipeline(args, cfg, rank, world, local):
         ctx.post_validate_finish(o)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda")
+        t = torch.tensor([e0.elapsed_time(e1) / steps], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
@@ -675,11 +653,14 @@ def run_pipeline(args, cfg, rank, world, local):
         ctx.post_validate_finish(opt)
         ctx.profile()
     t_ns, _ = ctx.profile()
-    mine = torch.tensor(t_ns, device="cuda", dtype=torch.int64)
+    mine = torch.tensor(t_ns, device=cdev, dtype=torch.int64)
     allT = [torch.zeros_like(mine) for _ in range(p)]
     dist.all_gather(allT, mine)
     TF, TB, TW = ([int(x[k]) for x in allT] for k in range(3))
-    tcomm = measure_tcomm_ns(rank, p, 4 * cfg.T * cfg.h)
+    # T_comm: one f32 [T, h] boundary-gradient message, round trip / 2, max over pairs (zb_ctx_comm_probe)
+    rt = torch.tensor([ctx.comm_probe(4 * cfg.T * cfg.h, 10)], device=cdev, dtype=torch.int64)
+    dist.all_reduce(rt, op=dist.ReduceOp.MAX)
+    tcomm = int(rt.item()) // 2
     passes, sim = api.schedule_per_stage(args.family, p, m, TF, TB, TW, tcomm, M_limit=lim, M_B=slot_b, M_W=slot_b)
     if max(1, sim.n_slots[rank]) > n_slots:
         raise SystemExit("profiled schedule needs more stash slots than allocated")
@@ -688,10 +669,10 @@ def run_pipeline(args, cfg, rank, world, local):
     torch.cuda.synchronize()
     nl = C.c_int64()
     lib.zb_dbg_launch_count(1, C.byref(nl))
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         ms = timed(passes, fused_main)
     lib.zb_dbg_launch_count(0, C.byref(nl))
-    nlt = torch.tensor([nl.value], device="cuda", dtype=torch.int64)
+    nlt = torch.tensor([nl.value], device=cdev, dtype=torch.int64)
     dist.all_reduce(nlt)                       # kernels launched by all ranks
     tokens_per_step = cfg.T * m
     value = tokens_per_step / (ms / 1000.0)
@@ -702,7 +683,7 @@ def run_pipeline(args, cfg, rank, world, local):
     lib.zb_dbg_kernel_timing(0, 0)
     a, b, n = C.c_double(), C.c_double(), C.c_int64()
     lib.zb_dbg_kernel_timing_read(0, C.byref(a), C.byref(b), C.byref(n))
-    gt = torch.tensor([a.value, b.value], device="cuda", dtype=torch.float64)
+    gt = torch.tensor([a.value, b.value], device=cdev, dtype=torch.float64)
     dist.all_reduce(gt)                        # GEMM ms and FLOPs summed over ranks
     # e2e: host inputs through the public call, loss read back every step
     e2e_ms = timed(passes, fused_main, host=True, steps=k_steps)
@@ -712,7 +693,7 @@ def run_pipeline(args, cfg, rank, world, local):
     starts, ends = ctx.stats()
     busy = sum(e - s for s, e in zip(starts, ends))
     span = ends[-1] - starts[0] if starts else 0.0
-    stat = torch.tensor([busy, span], device="cuda")
+    stat = torch.tensor([busy, span], device=cdev)
     gathered = [torch.zeros_like(stat) for _ in range(p)]
     dist.all_gather(gathered, stat)
     busys = [float(g[0]) for g in gathered]
@@ -780,7 +761,7 @@ def run_pipeline_chunked(args, cfg, rank, world, local):
     import torch.distributed as dist
     from paper_2401_10241_b200 import api
 
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cdev = dist_setup(local)
     p, m, chunks = world, cfg.m, 2
     nv = chunks * p
     fused = args.family == "1f1bi"
@@ -819,7 +800,7 @@ def run_pipeline_chunked(args, cfg, rank, world, local):
 
     run(args.warmup, 0)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -827,7 +808,7 @@ def run_pipeline_chunked(args, cfg, rank, world, local):
         run(args.steps, args.warmup)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t)
     value = cfg.T * m / (ms / 1000.0)

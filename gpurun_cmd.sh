@@ -1,5 +1,3 @@
-timeout 200 python -m pytest tests/test_gpu_ops.py -x -q 2>&1 | tail -1
-for i in 1 2; do
-echo NEW; timeout 100 python scripts/ops_perf.py 2>&1 | grep -E '"ln_fwd"|copy_bf16'
-echo OLD; ZB_LIB=libzb_old.so timeout 100 python scripts/ops_perf.py 2>&1 | grep -E '"ln_fwd"'
-done
+timeout 900 python scripts/torch_bf16_baseline_error.py 6.2B > gpurun_out/torch62.log 2>&1; tail -5 gpurun_out/torch62.log
+timeout 900 python scripts/torch_bf16_baseline_error.py 1.5B > gpurun_out/torch15.log 2>&1; tail -5 gpurun_out/torch15.log
+timeout 600 python scripts/elementwise_qkv.py 1.5B > gpurun_out/qkv15.json 2> gpurun_out/qkv15.err; tail -3 gpurun_out/qkv15.err

@@ -337,6 +337,15 @@ zb_status_t zb_nccl_unique_id(void* id128);
  * or in zb_post_validate_finish when no iteration follows. */
 zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* ids, int32_t rank, int32_t world);
 
+/* T_comm of P:127 / P:169 ("T_comm ... collected" during profiling): the median
+ * round trip, in ns, of one `bytes` message from this stage to stage+1 (activation
+ * channel) and back (gradient channel) over the attached transport, `iters` timed
+ * round trips after 2 warm-ups.  Collective: EVERY stage of the pipeline must call
+ * it with the same bytes / iters (each answers its upstream neighbour, then pings
+ * downstream).  roundtrip_ns = 0 on the last stage; T_comm = max over stages / 2.
+ * Blocks the host until the probe finished.  ZB_EINVAL without a transport. */
+zb_status_t zb_ctx_comm_probe(zb_ctx_t* ctx, size_t bytes, int32_t iters, int64_t* roundtrip_ns);
+
 /* Attach the k chunk contexts of worker `worker` of a chunked schedule (ZB-V,
  * 1F1B-I; contexts created as virtual stages v of nv): links to chunks on
  * other workers become 2-rank NCCL communicators, ids as for

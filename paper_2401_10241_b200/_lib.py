@@ -133,6 +133,7 @@ _SIGS = {
     "zb_ctx_read_pv_report": ([_P, C.POINTER(zb_pv_report_t)], _I32),
     "zb_nccl_unique_id": ([_P], _I32),
     "zb_ctx_attach_nccl": ([_P, _P, _I32, _I32], _I32),
+    "zb_ctx_comm_probe": ([_P, C.c_size_t, _I32, C.POINTER(_I64)], _I32),
     "zb_loopback_create": ([_I32, C.POINTER(_P)], _I32),
     "zb_loopback_destroy": ([_P], _I32),
     "zb_ctx_attach_loopback": ([_P, _P, _I32], _I32),

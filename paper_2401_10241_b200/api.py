@@ -228,6 +228,13 @@ class Context:
         buf = C.create_string_buffer(ids, len(ids))
         check(lib.zb_ctx_attach_nccl(self.h, buf, rank, world))
 
+    def comm_probe(self, nbytes: int, iters: int = 10) -> int:
+        """zb_ctx_comm_probe: median round trip (ns) of one message to stage+1 and back
+        (collective over the pipeline; 0 on the last stage)."""
+        v = C.c_int64()
+        check(lib.zb_ctx_comm_probe(self.h, int(nbytes), int(iters), C.byref(v)))
+        return v.value
+
     def attach_loopback(self, group: "Loopback"):
         """Attach to an in-process loopback group (rank = this context's stage)."""
         check(lib.zb_ctx_attach_loopback(self.h, group.h, self.stage))

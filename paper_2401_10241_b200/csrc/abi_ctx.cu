@@ -672,6 +672,17 @@ extern "C" zb_status_t zb_ctx_attach_loopback(zb_ctx_t* ctx, zb_loopback_t* grou
   ZB_CATCH
 }
 
+extern "C" zb_status_t zb_ctx_comm_probe(zb_ctx_t* ctx, size_t bytes, int32_t iters, int64_t* roundtrip_ns) {
+  ZB_TRY {
+    Ctx* c = C_(ctx);
+    if (!roundtrip_ns || iters < 1 || bytes == 0) return set_error(ZB_EINVAL, "bad probe arguments");
+    if (!c->comm) return set_error(ZB_EINVAL, "zb_ctx_comm_probe needs zb_ctx_attach_nccl / _loopback");
+    *roundtrip_ns = comm_probe(*c, bytes, iters);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 extern "C" zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* ids, int32_t rank, int32_t world) {
   ZB_TRY {
     Ctx* c = C_(ctx);

@@ -22,6 +22,7 @@
 
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -63,10 +64,17 @@ struct Nccl {
 Nccl& nccl() {
   static Nccl n;
   if (n.h) return n;
+  // ZB_NCCL_LIB: an explicit library path (tests: the 2-process / 1-GPU shim,
+  // tests/shim/nccl_ipc.cpp); otherwise the already-loaded / system libnccl.so.2.
+  const char* env = std::getenv("ZB_NCCL_LIB");
+  if (env && *env) {
+    n.h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    if (!n.h) throw Error(ZB_ENCCL, std::string("cannot load ZB_NCCL_LIB: ") + dlerror());
+  }
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
   for (const char* nm : names) {
-    n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
     if (n.h) break;
+    n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
   }
   if (!n.h) throw Error(ZB_ENCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
   n.get_id = reinterpret_cast<PGetId>(dlsym(n.h, "ncclGetUniqueId"));
@@ -181,6 +189,61 @@ void setup_comm(Ctx& c, Comm& cm) {
   ZB_CUDA(cudaMalloc(&cm.scalars, 64 + c.esz * static_cast<size_t>(c.T) * c.h));  // 4 PV messages + discard buffer
 }
 }  // namespace
+
+// T_comm probe: round trips of one `bytes` message per adjacent pair,
+// stage s -> s+1 on the activation channel and back on the gradient channel, timed on
+// the lower stage's channel streams.  Every stage first answers its upstream neighbour
+// (pong), then pings downstream, so the host-side enqueue order is deadlock-free for
+// both transports.  Returns the median round trip in ns (0 on the last stage).
+int64_t comm_probe(Ctx& c, size_t bytes, int iters) {
+  if (!c.comm) throw Error(ZB_EINVAL, "comm probe needs an attached transport");
+  Comm& cm = *c.comm;
+  const bool up = cm.rank > 0, down = cm.rank < cm.world - 1;
+  void *pong = nullptr, *ping = nullptr, *back = nullptr;
+  ZB_CUDA(cudaMalloc(&pong, bytes));
+  ZB_CUDA(cudaMalloc(&ping, bytes));
+  ZB_CUDA(cudaMalloc(&back, bytes));
+  ZB_CUDA(cudaMemset(ping, 0, bytes));
+  const int warm = 2;
+  std::vector<cudaEvent_t> t0(iters + warm), t1(iters + warm);
+  for (int i = 0; i < iters + warm; ++i) {
+    ZB_CUDA(cudaEventCreate(&t0[i]));
+    ZB_CUDA(cudaEventCreate(&t1[i]));
+  }
+  for (int i = 0; i < iters + warm; ++i) {
+    if (up) {
+      recvb(cm, C_ACT_FROM, pong, bytes);
+      order(cm, cm.stream[C_GRAD_TO], cm.stream[C_ACT_FROM]);
+      sendb(cm, C_GRAD_TO, pong, bytes);
+    }
+    if (down) {
+      ZB_CUDA(cudaEventRecord(t0[i], cm.stream[C_ACT_TO]));
+      sendb(cm, C_ACT_TO, ping, bytes);
+      order(cm, cm.stream[C_GRAD_FROM], cm.stream[C_ACT_TO]);
+      recvb(cm, C_GRAD_FROM, back, bytes);
+      ZB_CUDA(cudaEventRecord(t1[i], cm.stream[C_GRAD_FROM]));
+    }
+  }
+  for (int w = 0; w < 4; ++w)
+    if (cm.stream[w]) ZB_CUDA(cudaStreamSynchronize(cm.stream[w]));
+  std::vector<int64_t> rt;
+  if (down)
+    for (int i = warm; i < iters + warm; ++i) {
+      float ms = 0.f;
+      ZB_CUDA(cudaEventElapsedTime(&ms, t0[i], t1[i]));
+      rt.push_back(static_cast<int64_t>(static_cast<double>(ms) * 1e6 + 0.5));
+    }
+  for (int i = 0; i < iters + warm; ++i) {
+    cudaEventDestroy(t0[i]);
+    cudaEventDestroy(t1[i]);
+  }
+  cudaFree(pong);
+  cudaFree(ping);
+  cudaFree(back);
+  if (rt.empty()) return 0;
+  std::sort(rt.begin(), rt.end());
+  return rt[rt.size() / 2];
+}
 
 void attach_nccl(Ctx& c, const void* ids, int rank, int world) {
   auto cm = std::make_unique<Comm>();

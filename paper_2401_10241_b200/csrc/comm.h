@@ -85,6 +85,8 @@ void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* t
 // stage cfg.stage of cfg.p; post-validation must be finished before the next iteration.
 void run_iteration_worker(const std::vector<Ctx*>& chunks, const zb_pass_t* passes, int n, const int32_t* tokens,
                           const int32_t* labels, int flags);
+// Median round trip (ns) of one `bytes` message to stage+1 and back (0 on the last stage).
+int64_t comm_probe(Ctx& c, size_t bytes, int iters);
 // Post-validation chain messages over the attached communicators.
 void pv_recv_partial(Ctx& c);
 void pv_send_partial(Ctx& c);

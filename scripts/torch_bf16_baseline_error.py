@@ -3,6 +3,7 @@ flash SDPA) land from the fp64 oracle on the same config?  Context for the
 bf16 tolerance (DESIGN.md R-tol) — not part of the product path."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import json
 import numpy as np, torch, torch.nn.functional as F
 import zb_synth
 from oracle import model as om
@@ -37,6 +38,18 @@ def run(cfg):
     errs = {k: float(np.linalg.norm(P[k].grad.double().cpu().numpy() - ref[k]) / np.linalg.norm(ref[k])) for k in ref}
     e = sorted(errs.values(), reverse=True)
     print(cfg.name, "torch-bf16 loss", float(total), "oracle", ref_loss, "mean", np.mean(e), "max", e[0])
+    blocks = {}
+    for k in ref:
+        if k.endswith("qkv_w"):
+            g = P[k].grad.double().cpu().numpy()
+            for i, part in enumerate("QKV"):
+                r = ref[k][i * h:(i + 1) * h]
+                blocks[f"{k}.{part}"] = float(np.linalg.norm(g[i * h:(i + 1) * h] - r) / np.linalg.norm(r))
+    print(cfg.name, "torch-bf16 per-tensor", json.dumps({k: round(v, 4) for k, v in errs.items()}))
+    print(cfg.name, "torch-bf16 qkv blocks", json.dumps({k: round(v, 4) for k, v in blocks.items()}))
 
-run(zb_synth.CONFIGS["tiny"])
-run(zb_synth.ModelConfig("d64", h=64, a=1, L=4, s=256, b=2, V=512, p=4, m=3, family="zbh1"))
+if len(sys.argv) > 1:
+    run(zb_synth.CONFIGS[sys.argv[1]].with_(L=2, b=2, m=2))
+else:
+    run(zb_synth.CONFIGS["tiny"])
+    run(zb_synth.ModelConfig("d64", h=64, a=1, L=4, s=256, b=2, V=512, p=4, m=3, family="zbh1"))
