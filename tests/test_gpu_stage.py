@@ -74,7 +74,7 @@ def gpu_run(cfg, p, dtype, family="zbh1"):
 def check_tolerance(loss, grads, ref_loss, ref_grads, dtype):
     """per tensor the normwise relative error AND the elementwise
     bound (zbtest_util.close_report: f32 |x - ref| <= rtol*|ref| + rtol*rms(ref);
-    bf16 the row-aware floor with kappa = 4, DESIGN R-tol); f32 rtol 1e-5, bf16
+    bf16 the row-aware floor with kappa = sqrt(2 ln N), DESIGN R-tol); f32 rtol 1e-5, bf16
     rtol 2e-2 per tensor and normwise mean over tensors <= 1e-2."""
     rtol = 1e-5 if dtype == "f32" else 2e-2
     rep = {k: close_report(grads[k], ref_grads[k], rtol, bf16=dtype != "f32", exact_zero_rows=True) for k in ref_grads}

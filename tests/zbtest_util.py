@@ -33,14 +33,20 @@ def cuda_available() -> bool:
         return False
 
 
-BF16_KAPPA = 4.0
+def bf16_kappa(n):
+    """Elementwise counterpart of the normwise rtol (DESIGN R-tol): if the N element
+    errors were Gaussian at exactly the normwise tolerance (std = rtol * scale), their
+    largest would be ~sqrt(2 ln N) * rtol * scale; at least 3."""
+    import math
+    return max(3.0, math.sqrt(2.0 * math.log(max(n, 2))))
 
 
 def close_report(x, ref, rtol, bf16=False, exact_zero_rows=False):
     """SURVEY C15 / DESIGN R-tol: normwise ||x - ref||_2 / ||ref||_2 AND an elementwise
     bound |x - ref| <= rtol*|ref| + kappa*rtol*floor.
       f32 mode:  kappa = 1, floor = rms(ref)                        (SURVEY C15 as written)
-      bf16 mode: kappa = 4, floor = max(rms of the element's row, rms over the tensor's
+      bf16 mode: kappa = bf16_kappa(N) = max(3, sqrt(2 ln N)), floor = max(rms of the
+                 element's row, rms over the tensor's
                  non-zero rows)                                      (DESIGN R-tol derivation);
                  exact_zero_rows: a row the reference leaves exactly zero (an embedding
                  row no token touched) must be exactly zero
@@ -63,7 +69,7 @@ def close_report(x, ref, rtol, bf16=False, exact_zero_rows=False):
         if exact_zero_rows:       # rows the reference leaves exactly zero (untouched embedding rows)
             floor = np.where(row > 0, floor, 0.0)
         floor = floor * np.ones_like(r2)
-        bound = rtol * np.abs(r2) + BF16_KAPPA * rtol * floor
+        bound = rtol * np.abs(r2) + bf16_kappa(ref.size) * rtol * floor
         d2 = diff.reshape(r2.shape)
     else:
         rms = float(np.sqrt(np.mean(ref * ref)))
