@@ -22,6 +22,8 @@ extern "C" {
  * ZB_DTYPE_F32: everything f32 (SIMT kernel).
  * epi: 0 C = acc (+bias); 1 C = acc + bias, aux = GeLU(C); 2 C = aux + acc (+bias);
  *      3 C = acc * GeLU'(aux); 4 C(f32) = acc + (beta ? C : 0); 5 C(f32) = acc.
+ * epi 4 (W) with a_mn: a non-NULL `bias` is an OUTPUT, f32 [M]: (beta ? += : =) the
+ *      column sums sum_k A(m,k) (W's bias gradient, formed inside the GEMM). 
  * N and ldc must be multiples of 8; operands 16-byte aligned. */
 zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn,
                         const void* B, int64_t ldb, int32_t b_mn, int32_t epi, void* C, int64_t ldc,

@@ -22,6 +22,11 @@ extern "C" zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t 
     g.B = B; g.ldb = ldb; g.b_mn = b_mn != 0;
     g.epi = epi;
     g.ep = EpiArgs{C, ldc, bias, aux, ldaux, beta};
+    if (epi == EPI_F32_ACC && bias != nullptr) {  // W: `bias` receives the column sums of A (bias_out)
+      if (!a_mn) return set_error(ZB_EINVAL, "bias_out needs an MN-major A (the W contraction)");
+      g.ep.bias = nullptr;
+      g.ep.bias_out = const_cast<float*>(bias);
+    }
     gemm(g, static_cast<DType>(dtype), static_cast<cudaStream_t>(stream));
     return ZB_OK;
   }

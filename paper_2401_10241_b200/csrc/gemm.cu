@@ -18,6 +18,7 @@
 
 #include "gemm.h"
 #include "ktimer.h"
+#include "ops.h"
 #include "sm100.cuh"
 
 namespace zb {
@@ -394,14 +395,40 @@ template <int BN> struct Cfg2 {
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static constexpr int EPI_OFF = STAGES * STAGE;
   static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * kStageBytes;
-  static constexpr int SMEM = BAR_OFF + 1024 + 256;
+  static constexpr int CS_OFF = BAR_OFF + 512;  // column-sum combine buffer (16 x 8 floats)
+  static constexpr int SMEM = BAR_OFF + 1024 + 512 + 512;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI, typename TO>
+// Column sums of the A operand (W's bias gradient, A = dY MN-major) by warps 2-3 of each
+// CTA of the pair.  A stage holds the CTA's 128 M values x 64 K rows as two 64 x 64 boxes
+// (box b = M [64b, 64b+64), row r = k, 128 B per row, 16-B chunk j of row r at
+// r*128 + ((j ^ (r & 7)) << 4)).  Thread t (of 64) owns chunk c = t % 16 (8 M values) and
+// the rows r = t/16 (mod 4): per quarter-warp the 8 lanes read 8 distinct chunks of one
+// row (conflict-free).  The warps read a stage after its MMAs completed (the leader's
+// commit lands on mma_done) and release it to the producer (empty, 2 arrivals), so the
+// reads never race the refill; the sums are in a fixed order (deterministic).
+__device__ __forceinline__ void colsum_stage(const uint8_t* sa, int t, float* acc) {
+  const int c = t & 15, g = t >> 4;
+  const uint8_t* base = sa + (c >> 3) * 8192;
+  const int j = c & 7;
+#pragma unroll 4
+  for (int r = g; r < 64; r += 4) {
+    const uint4 q = *reinterpret_cast<const uint4*>(base + r * 128 + ((j ^ (r & 7)) << 4));
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] += __uint_as_float(w[i] << 16);
+      acc[2 * i + 1] += __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI, typename TO, bool CS = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const EpiArgs ep,
                int M, int N, int K) {
+  static_assert(!CS || (A_MN && EPI == EPI_F32_ACC), "column sums: W's A operand only");
   using C = Cfg2<BN>;
   constexpr int BM2 = 2 * BM;
   extern __shared__ uint8_t smem_raw[];
@@ -411,7 +438,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* xbar = tempty + 2;  // [kEpiWarps]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(xbar + kEpiWarps);
+  uint64_t* mdone = xbar + kEpiWarps;  // [STAGES] (CS: the stage's MMAs completed)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mdone + C::STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = sm100::cluster_ctarank();
@@ -419,7 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
       sm100::mbar_init(&full[i], 2);  // one arrival per CTA (+ both CTAs' TMA bytes)
-      sm100::mbar_init(&empty[i], 1);
+      sm100::mbar_init(&empty[i], CS ? 2 : 1);  // CS: released by the two column-sum warps
+      sm100::mbar_init(&mdone[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
@@ -516,7 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               sm100::mma_bf16_ss_pair(d, sm100::desc_adv(ad0, A_MN ? kk * 2048 : kk * 32),
                                       sm100::desc_adv(bd0, B_MN ? kk * 2048 : kk * 32), idesc,
                                       (kb != kb0 || kk != 0) ? 1u : 0u);
-            sm100::mma_commit_pair(&empty[stage], 0x3);
+            sm100::mma_commit_pair(CS ? &mdone[stage] : &empty[stage], 0x3);
           }
           __syncwarp();
           if (++stage == C::STAGES) {
@@ -532,6 +561,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           aph ^= 1;
         }
       }
+    }
+  } else if (CS && (warp == 2 || warp == 3)) {  // ---------------- column sums of A (both CTAs)
+    const int t = threadIdx.x - 64;
+    float* xbuf = reinterpret_cast<float*>(smem + C::CS_OFF);
+    int stage = 0;
+    uint32_t ph = 0;
+    for (int it = cid; it < items; it += ncl) {
+      int mt, nt;
+      tile_coords(it % tiles, num_m, num_n, mt, nt);
+      const int sp = it / tiles;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int kb = kb_begin(sp); kb < kb_begin(sp + 1); ++kb) {
+        sm100::mbar_wait(&mdone[stage], ph);
+        if (nt == 0) colsum_stage(smem + stage * C::STAGE, t, acc);
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&empty[stage]);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          ph ^= 1;
+        }
+      }
+      if (nt != 0) continue;
+      // combine the four row groups: (g0 + g1) in warp 2, (g2 + g3) in warp 3, then the warps
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+      if (warp == 3 && lane < 16)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xbuf[lane * 8 + i] = acc[i];
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+      if (warp == 2 && lane < 16) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += xbuf[lane * 8 + i];
+        const int m = mt * BM2 + static_cast<int>(rank) * BM + (lane >> 3) * 64 + (lane & 7) * 8;
+        float* dst = splits > 1 ? ep.bias_part + static_cast<int64_t>(sp) * M : ep.bias_out;
+        const bool add = splits == 1 && ep.beta != 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (m + i < M) dst[m + i] = add ? dst[m + i] + acc[i] : acc[i];
+      }
+      asm volatile("bar.sync 1, 64;" ::: "memory");  // xbuf is reused by the next tile
     }
   } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows)
     const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;  // see the 1-CTA kernel
@@ -730,7 +799,11 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
 struct SplitFlags {
   int32_t* dev = nullptr;
   int32_t base = 0;
+  float* part = nullptr;  // per-split bias partial sums [splits, M] (column-sum W GEMMs)
+  size_t part_cap = 0;
 };
+static std::mutex g_split_mu;
+static std::map<cudaStream_t, SplitFlags> g_split_bufs;
 static constexpr int kMaxFlagTiles = 4096;
 static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs& ep) {
   static int disabled = -1;
@@ -758,10 +831,8 @@ static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs&
   }
   if (force) best = force;
   if (best == 1) return;
-  static std::mutex mu;
-  static std::map<cudaStream_t, SplitFlags> bufs;
-  std::lock_guard<std::mutex> lock(mu);
-  SplitFlags& f = bufs[st];
+  std::lock_guard<std::mutex> lock(g_split_mu);
+  SplitFlags& f = g_split_bufs[st];
   if (!f.dev) {
     ZB_CUDA(cudaMalloc(&f.dev, sizeof(int32_t) * 16 * kMaxFlagTiles));
     ZB_CUDA(cudaMemsetAsync(f.dev, 0, sizeof(int32_t) * 16 * kMaxFlagTiles, st));  // ordered on st
@@ -776,10 +847,36 @@ static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs&
   f.base += best;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// per-split bias partials of a column-sum W GEMM (stream-private, grown on demand; the
+// previous user on the same stream has finished before the next GEMM reads / writes it)
+static float* bias_partials(cudaStream_t st, size_t n) {
+  std::lock_guard<std::mutex> lock(g_split_mu);
+  SplitFlags& f = g_split_bufs[st];
+  if (f.part_cap < n) {
+    if (f.part) {
+      ZB_CUDA(cudaStreamSynchronize(st));
+      ZB_CUDA(cudaFree(f.part));
+    }
+    ZB_CUDA(cudaMalloc(&f.part, n * sizeof(float)));
+    f.part_cap = n;
+  }
+  return f.part;
+}
+
+// out[m] = (beta ? out[m] : 0) + sum_s part[s][m], splits summed in order (deterministic)
+__global__ void k_bias_finalize(const float* __restrict__ part, int splits, int M, float* __restrict__ out, int beta) {
+  pdl_wait();
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  float v = part[m];
+  for (int s = 1; s < splits; ++s) v += part[static_cast<int64_t>(s) * M + m];
+  out[m] = beta ? out[m] + v : v;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI, bool CS = false>
 static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   using C = tc::Cfg2<BN>;
-  auto kern = tc::k_gemm_tc2<BN, A_MN, B_MN, EPI, bf16>;
+  auto kern = tc::k_gemm_tc2<BN, A_MN, B_MN, EPI, bf16, CS>;
   static bool attr = false;
   if (!attr) {
     ZB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -793,10 +890,17 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   if (EPI == EPI_F32_ACC) split_k_plan(tiles, static_cast<int>(ceil_div(g.K, tc::BK)), pairs, st, ep);
   const int items = tiles * ep.splits;
   const int grid = 2 * (items < pairs ? items : pairs);
+  if (CS && ep.splits > 1) ep.bias_part = bias_partials(st, static_cast<size_t>(ep.splits) * g.M);
   CUtensorMap tcm, txm;
   epi_tmaps<EPI>(g, tcm, txm);
   launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, ep, g.M, g.N, g.K);
   ZB_LAUNCH_CHECK();
+  if (CS && ep.splits > 1) {
+    launch(PDL_OPS, k_bias_finalize, static_cast<int>(ceil_div(g.M, 256)), 256, 0, st,
+           static_cast<const float*>(ep.bias_part), static_cast<int>(ep.splits), g.M, ep.bias_out,
+           static_cast<int>(ep.beta));
+    ZB_LAUNCH_CHECK();
+  }
 }
 
 // 2-CTA tiles when the problem fills at least one 256 x 256 pair tile; env ZB_GEMM_1CTA=1 forces 1-CTA.
@@ -809,16 +913,24 @@ static bool use_pair(const GemmArgs& g) {
   return !force1 && g.M >= 256 && g.N >= 256;
 }
 
+// returns true when the kernel also formed W's bias gradient (ep.bias_out)
 template <int BN, bool A_MN, bool B_MN, int EPI>
-static void launch_any(const GemmArgs& g, cudaStream_t st) {
-  if (BN == 256 && use_pair(g))
+static bool launch_any(const GemmArgs& g, cudaStream_t st) {
+  constexpr bool kCS = A_MN && EPI == EPI_F32_ACC && BN == 256;
+  if (BN == 256 && use_pair(g)) {
+    if (kCS && g.ep.bias_out != nullptr) {
+      launch_tc2<BN, A_MN, B_MN, EPI, kCS>(g, st);
+      return true;
+    }
     launch_tc2<BN, A_MN, B_MN, EPI>(g, st);
-  else
+  } else {
     launch_tc<BN, A_MN, B_MN, EPI>(g, st);
+  }
+  return false;
 }
 
 template <int BN, bool A_MN, bool B_MN>
-static void dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
+static bool dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
   switch (g.epi) {
     case EPI_STORE: return launch_any<BN, A_MN, B_MN, EPI_STORE>(g, st);
     case EPI_BIAS_GELU: return launch_any<BN, A_MN, B_MN, EPI_BIAS_GELU>(g, st);
@@ -831,7 +943,7 @@ static void dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
 }
 
 template <int BN>
-static void dispatch_major_tc(const GemmArgs& g, cudaStream_t st) {
+static bool dispatch_major_tc(const GemmArgs& g, cudaStream_t st) {
   if (!g.a_mn && !g.b_mn) return dispatch_epi_tc<BN, false, false>(g, st);
   if (!g.a_mn && g.b_mn) return dispatch_epi_tc<BN, false, true>(g, st);
   if (g.a_mn && g.b_mn) return dispatch_epi_tc<BN, true, true>(g, st);
@@ -861,19 +973,25 @@ static void dispatch_epi_f32(const GemmArgs& g, cudaStream_t st) {
 void gemm(const GemmArgs& g, DType dt, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
   if (g.N % 8 != 0 || g.ep.ldc % 8 != 0) throw CudaError("gemm: N and ldc must be multiples of 8");
+  if (g.ep.bias_out != nullptr && (g.epi != EPI_F32_ACC || !g.a_mn))
+    throw CudaError("gemm: bias_out is W's bias gradient (EPI_F32_ACC, MN-major A)");
   const int cls = g.a_mn ? ktimer::GEMM_W : (g.b_mn ? ktimer::GEMM_B : ktimer::GEMM_F);
   const int tk = ktimer::start(cls, 2.0 * g.M * g.N * static_cast<double>(g.K), st);
+  bool bias_done = false;
   if (dt == DT_F32) {
     if (!g.a_mn && !g.b_mn) dispatch_epi_f32<false, false>(g, st);
     else if (!g.a_mn && g.b_mn) dispatch_epi_f32<false, true>(g, st);
     else if (g.a_mn && g.b_mn) dispatch_epi_f32<true, true>(g, st);
     else dispatch_epi_f32<true, false>(g, st);
   } else if (g.N <= 128) {
-    dispatch_major_tc<128>(g, st);
+    bias_done = dispatch_major_tc<128>(g, st);
   } else {
-    dispatch_major_tc<256>(g, st);
+    bias_done = dispatch_major_tc<256>(g, st);
   }
   ktimer::stop(tk, st);
+  // paths without the in-kernel column sums (f32 parity mode, 1-CTA tiles): separate kernel
+  if (g.ep.bias_out != nullptr && !bias_done)
+    bias_grad(dt, g.A, g.lda, g.ep.bias_out, g.K, g.M, g.ep.beta, st);
 }
 
 }  // namespace zb

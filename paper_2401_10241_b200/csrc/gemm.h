@@ -42,6 +42,11 @@ struct EpiArgs {
   int32_t splits = 1;
   int32_t flag_base = 0;
   int32_t* flags = nullptr;
+  // W's bias gradient (EPI_F32_ACC only): bias_out[m] (beta ? += : =) sum_k A(m, k), the
+  // column sums of dY (P:46's W of a bias).  The 2-CTA kernel forms them from the A tiles it
+  // already streams (column-sum warps, gemm.cu); other paths fall back to ops.h bias_grad.
+  float* bias_out = nullptr;
+  float* bias_part = nullptr;  // set by gemm(): per-split partial sums [splits, M]
 };
 
 struct GemmArgs {

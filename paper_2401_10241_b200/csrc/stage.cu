@@ -10,7 +10,8 @@
 //                 (deterministic chunk partials) are taken here (DESIGN.md R-ln).
 // W  (per layer)  dW += dY^T X for fc2 (dX', G), fc1 (dU, LN2), proj (dX1, O),
 //                 qkv (dQKV, LN1) with f32 accumulation into the persistent grads,
-//                 bias grads = column sums; stage 0: embedding scatter.
+//                 bias grads = column sums of dY formed inside the same GEMMs;
+//                 stage 0: embedding scatter.
 // In-place reuse keeps M_W = M_B: dU over U, dX1 over X1, dX over X, dQKV
 // pointer-swapped with QKV.
 #include <algorithm>
@@ -234,18 +235,17 @@ static void lin_dgrad(Ctx& c, const void* dY, const void* W, void* dX, int M, in
   g.ep = EpiArgs{dX, N, nullptr, aux, N, 0};
   gemm(g, c.dt, c.stream);
 }
-// dW [M = n_out, N = n_in] (+)= dY[T, M]^T X[T, N]
-static void lin_wgrad(Ctx& c, const void* dY, const void* X, float* dW, int M, int N, int K, int beta) {
+// dW [M = n_out, N = n_in] (+)= dY[T, M]^T X[T, N]; db [M] (+)= column sums of dY (W of the
+// bias), formed inside the same GEMM from the dY tiles it streams (gemm.h bias_out)
+static void lin_wgrad(Ctx& c, const void* dY, const void* X, float* dW, float* db, int M, int N, int K, int beta) {
   GemmArgs g{};
   g.M = M; g.N = N; g.K = K;
   g.A = dY; g.lda = M; g.a_mn = true;
   g.B = X; g.ldb = N; g.b_mn = true;
   g.epi = EPI_F32_ACC;
   g.ep = EpiArgs{dW, N, nullptr, nullptr, 0, beta};
+  g.ep.bias_out = db;
   gemm(g, c.dt, c.stream);
-}
-static void bias_grad(Ctx& c, const void* dY, float* db, int N, int beta) {
-  zb::bias_grad(c.dt, dY, N, db, c.T, N, beta, c.stream);
 }
 static void ln_bwd(Ctx& c, const float* dy, const void* x, const float* mu, const float* rs, const float* g,
                    const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta) {
@@ -298,7 +298,7 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
     lin_fwd(*this, sl.lnf, head_w, nullptr, logits, T, V, H, EPI_F32_STORE, nullptr);
     cross_entropy(dt, logits, sl.lab, dlogits, loss_rows, loss_acc, T, V,
                   1.0f / (static_cast<float>(T) * static_cast<float>(cfg.m)), stream);
-    lin_wgrad(*this, dlogits, sl.lnf, g_head_w, V, H, T, beta);  // head W eagerly (C8 reading)
+    lin_wgrad(*this, dlogits, sl.lnf, g_head_w, nullptr, V, H, T, beta);  // head W eagerly (C8 reading)
     lin_dgrad(*this, dlogits, head_w, d_ln, T, H, V, EPI_F32_STORE, nullptr);
     ln_bwd(*this, d_ln, sl.xl, sl.muf, sl.rsf, lnf_g, nullptr, g32_dx, sl.dy, g_lnf_g, g_lnf_b, beta);
     dx2_32 = g32_dx;
@@ -339,14 +339,10 @@ void Ctx::backward_weight(int mb, int slot_idx) {
     LayerAct& A = sl.L[l];
     const LayerW& w = lw[l];
     void* dx2 = l == Ls - 1 ? sl.dy : sl.L[l + 1].x;
-    lin_wgrad(*this, dx2, A.g, w.g_fc2_w, H, 4 * H, T, beta);
-    bias_grad(*this, dx2, w.g_fc2_b, H, beta);
-    lin_wgrad(*this, A.u, A.ln2, w.g_fc1_w, 4 * H, H, T, beta);
-    bias_grad(*this, A.u, w.g_fc1_b, 4 * H, beta);
-    lin_wgrad(*this, A.x1, A.o, w.g_proj_w, H, H, T, beta);
-    bias_grad(*this, A.x1, w.g_proj_b, H, beta);
-    lin_wgrad(*this, A.qkv, A.ln1, w.g_qkv_w, 3 * H, H, T, beta);
-    bias_grad(*this, A.qkv, w.g_qkv_b, 3 * H, beta);
+    lin_wgrad(*this, dx2, A.g, w.g_fc2_w, w.g_fc2_b, H, 4 * H, T, beta);
+    lin_wgrad(*this, A.u, A.ln2, w.g_fc1_w, w.g_fc1_b, 4 * H, H, T, beta);
+    lin_wgrad(*this, A.x1, A.o, w.g_proj_w, w.g_proj_b, H, H, T, beta);
+    lin_wgrad(*this, A.qkv, A.ln1, w.g_qkv_w, w.g_qkv_b, 3 * H, H, T, beta);
   }
   if (first) {
     if (!first_w_done) {

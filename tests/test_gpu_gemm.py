@@ -80,6 +80,37 @@ def test_gemm_parity(case, dtype):
             assert_close(gg, _gelu(ref), 1e-5 if dtype == "f32" else 6e-3, "GeLU aux")
 
 
+@pytest.mark.parametrize("M,N,K", [(2304, 2304, 6144), (9216, 2304, 6144), (768, 512, 1000), (300, 264, 520),
+                                   (6912, 2304, 3072), (512, 512, 4096)])
+def test_w_gemm_bias_column_sums(M, N, K):
+    """W's bias gradient formed inside the W GEMM (column-sum warps over the dY tiles,
+    gemm.h bias_out) against the plain column sums in fp64; split-K shapes (partials
+    summed in order) and ragged tails; beta = 0 overwrites, beta = 1 accumulates; bitwise
+    repeatable.  The dW output is unchanged by the fused sums."""
+    import torch
+    from paper_2401_10241_b200 import api
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    A = (torch.randn(K, M, generator=g) * 0.5).bfloat16().cuda()
+    B = (torch.randn(K, N, generator=g) * 0.5).bfloat16().cuda()
+    Ad, Bd = A.double().cpu().numpy(), B.double().cpu().numpy()
+    want_c = Ad.T @ Bd
+    want_b = Ad.sum(0)
+    C = torch.zeros(M, N, dtype=torch.float32).cuda()
+    db = torch.full((M,), 7.0, dtype=torch.float32).cuda()
+    api.dbg_gemm(A, B, C, M=M, N=N, K=K, a_mn=True, b_mn=True, epi=4, bias=db, beta=0)
+    torch.cuda.synchronize()
+    assert_close(C.double().cpu().numpy(), want_c, 1e-5, "dW")
+    assert_close(db.double().cpu().numpy(), want_b, 1e-5, "db beta=0")
+    first = db.clone()
+    api.dbg_gemm(A, B, C, M=M, N=N, K=K, a_mn=True, b_mn=True, epi=4, bias=db, beta=1)
+    torch.cuda.synchronize()
+    assert_close(db.double().cpu().numpy(), 2 * want_b, 1e-5, "db beta=1")
+    again = torch.zeros_like(db)
+    api.dbg_gemm(A, B, C, M=M, N=N, K=K, a_mn=True, b_mn=True, epi=4, bias=again, beta=0)
+    torch.cuda.synchronize()
+    assert torch.equal(again, first)
+
+
 def test_split_k_w_is_deterministic():
     """The ordered split-K of W (gemm.cu split_k_plan) sums in one fixed order:
     repeated accumulations are bitwise identical (P:196 needs this across schedules)."""
