@@ -1,3 +1,2 @@
-timeout 900 python scripts/torch_bf16_baseline_error.py 6.2B > gpurun_out/torch62.log 2>&1; tail -5 gpurun_out/torch62.log
-timeout 900 python scripts/torch_bf16_baseline_error.py 1.5B > gpurun_out/torch15.log 2>&1; tail -5 gpurun_out/torch15.log
-timeout 600 python scripts/elementwise_qkv.py 1.5B > gpurun_out/qkv15.json 2> gpurun_out/qkv15.err; tail -3 gpurun_out/qkv15.err
+timeout 600 python -m pytest tests/test_gpu_gemm.py -q -x --timeout 300 -p no:cacheprovider 2>&1 | tail -3
+timeout 600 python scripts/gemm_w_bias.py 2>&1 | tail -12

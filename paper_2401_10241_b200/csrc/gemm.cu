@@ -404,17 +404,23 @@ template <int BN> struct Cfg2 {
 // (box b = M [64b, 64b+64), row r = k, 128 B per row, 16-B chunk j of row r at
 // r*128 + ((j ^ (r & 7)) << 4)).  Thread t (of 64) owns chunk c = t % 16 (8 M values) and
 // the rows r = t/16 (mod 4): per quarter-warp the 8 lanes read 8 distinct chunks of one
-// row (conflict-free).  The warps read a stage after its MMAs completed (the leader's
-// commit lands on mma_done) and release it to the producer (empty, 2 arrivals), so the
-// reads never race the refill; the sums are in a fixed order (deterministic).
+// row (conflict-free).  The k-blocks of an M block are shared out over its num_n tiles
+// (tile nt reads k-blocks kb = nt mod num_n), so every tile delays only ~1/num_n of its
+// stages: for those the leader's MMA commit lands on mdone, the warps read the stage and
+// release it to the producer (empty); the other stages go straight back.  Each tile writes
+// its partial sums (zeros if it read nothing); k_bias_finalize adds the (split, n-tile)
+// partials in a fixed order (deterministic).
 __device__ __forceinline__ void colsum_stage(const uint8_t* sa, int t, float* acc) {
   const int c = t & 15, g = t >> 4;
-  const uint8_t* base = sa + (c >> 3) * 8192;
+  // shared-window address: a generic pointer after the alignment arithmetic would compile to LD.E
+  const uint32_t base = sm100::smem_addr(sa) + (c >> 3) * 8192;
   const int j = c & 7;
 #pragma unroll 4
   for (int r = g; r < 64; r += 4) {
-    const uint4 q = *reinterpret_cast<const uint4*>(base + r * 128 + ((j ^ (r & 7)) << 4));
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t w[4];
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "r"(base + r * 128 + ((j ^ (r & 7)) << 4)));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       acc[2 * i] += __uint_as_float(w[i] << 16);
@@ -438,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* xbar = tempty + 2;  // [kEpiWarps]
-  uint64_t* mdone = xbar + kEpiWarps;  // [STAGES] (CS: the stage's MMAs completed)
+  uint64_t* mdone = xbar + kEpiWarps;  // [STAGES] CS: MMAs of a stage the column sums read completed
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mdone + C::STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -447,7 +453,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
       sm100::mbar_init(&full[i], 2);  // one arrival per CTA (+ both CTAs' TMA bytes)
-      sm100::mbar_init(&empty[i], CS ? 2 : 1);  // CS: released by the two column-sum warps
+      // one arrival: the MMA commit, or (CS, a stage the column sums read) the column-sum warps
+      sm100::mbar_init(&empty[i], 1);
       sm100::mbar_init(&mdone[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -530,6 +537,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         sm100::tc_fence_after();
         const uint32_t d = tbase + acc * BN;
         const int kb0 = kb_begin(t / tiles);
+        int mt_, nt_;
+        tile_coords(t % tiles, num_m, num_n, mt_, nt_);
         for (int kb = kb0; kb < kb_begin(t / tiles + 1); ++kb) {
           sm100::mbar_wait_warp(&full[stage], ph);
           sm100::tc_fence_after();
@@ -545,7 +554,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               sm100::mma_bf16_ss_pair(d, sm100::desc_adv(ad0, A_MN ? kk * 2048 : kk * 32),
                                       sm100::desc_adv(bd0, B_MN ? kk * 2048 : kk * 32), idesc,
                                       (kb != kb0 || kk != 0) ? 1u : 0u);
-            sm100::mma_commit_pair(CS ? &mdone[stage] : &empty[stage], 0x3);
+            // CS: the stages whose column sums this tile forms (kb = nt mod num_n) go through the
+            // column-sum warps, which release them to the producer; the others straight back
+            sm100::mma_commit_pair(CS && kb % num_n == nt_ ? &mdone[stage] : &empty[stage], 0x3);
           }
           __syncwarp();
           if (++stage == C::STAGES) {
@@ -564,41 +575,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (CS && (warp == 2 || warp == 3)) {  // ---------------- column sums of A (both CTAs)
     const int t = threadIdx.x - 64;
-    float* xbuf = reinterpret_cast<float*>(smem + C::CS_OFF);
+    const uint32_t xs = sm100::smem_addr(smem + C::CS_OFF);
     int stage = 0;
-    uint32_t ph = 0;
+    uint32_t mph = 0;  // per-stage parity of mdone (a stage completes mdone phases only when read)
     for (int it = cid; it < items; it += ncl) {
       int mt, nt;
       tile_coords(it % tiles, num_m, num_n, mt, nt);
       const int sp = it / tiles;
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int kb = kb_begin(sp); kb < kb_begin(sp + 1); ++kb) {
-        sm100::mbar_wait(&mdone[stage], ph);
-        if (nt == 0) colsum_stage(smem + stage * C::STAGE, t, acc);
-        __syncwarp();
-        if (lane == 0) sm100::mbar_arrive(&empty[stage]);
-        if (++stage == C::STAGES) {
-          stage = 0;
-          ph ^= 1;
+        if (kb % num_n == nt) {  // this tile's share of the M block's column sums
+          sm100::mbar_wait(&mdone[stage], (mph >> stage) & 1u);
+          mph ^= 1u << stage;
+          colsum_stage(smem + stage * C::STAGE, t, acc);
+          asm volatile("bar.sync 1, 64;" ::: "memory");  // both warps have read the stage
+          if (t == 0) sm100::mbar_arrive(&empty[stage]);
         }
+        if (++stage == C::STAGES) stage = 0;
       }
-      if (nt != 0) continue;
       // combine the four row groups: (g0 + g1) in warp 2, (g2 + g3) in warp 3, then the warps
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
       if (warp == 3 && lane < 16)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) xbuf[lane * 8 + i] = acc[i];
+        for (int i = 0; i < 8; ++i)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(xs + (lane * 8 + i) * 4), "f"(acc[i]) : "memory");
       asm volatile("bar.sync 1, 64;" ::: "memory");
       if (warp == 2 && lane < 16) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += xbuf[lane * 8 + i];
+        for (int i = 0; i < 8; ++i) {
+          float o;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(xs + (lane * 8 + i) * 4) : "memory");
+          acc[i] += o;
+        }
         const int m = mt * BM2 + static_cast<int>(rank) * BM + (lane >> 3) * 64 + (lane & 7) * 8;
-        float* dst = splits > 1 ? ep.bias_part + static_cast<int64_t>(sp) * M : ep.bias_out;
-        const bool add = splits == 1 && ep.beta != 0;
+        float* dst = ep.bias_part + static_cast<int64_t>(sp * num_n + nt) * M;  // summed by k_bias_finalize
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-          if (m + i < M) dst[m + i] = add ? dst[m + i] + acc[i] : acc[i];
+          if (m + i < M) dst[m + i] = acc[i];
       }
       asm volatile("bar.sync 1, 64;" ::: "memory");  // xbuf is reused by the next tile
     }
@@ -799,7 +813,7 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
 struct SplitFlags {
   int32_t* dev = nullptr;
   int32_t base = 0;
-  float* part = nullptr;  // per-split bias partial sums [splits, M] (column-sum W GEMMs)
+  float* part = nullptr;  // bias partial sums [splits * n-tiles, M] (column-sum W GEMMs)
   size_t part_cap = 0;
 };
 static std::mutex g_split_mu;
@@ -863,7 +877,7 @@ static float* bias_partials(cudaStream_t st, size_t n) {
   return f.part;
 }
 
-// out[m] = (beta ? out[m] : 0) + sum_s part[s][m], splits summed in order (deterministic)
+// out[m] = (beta ? out[m] : 0) + sum_s part[s][m], the (split, n-tile) partials in order (deterministic)
 __global__ void k_bias_finalize(const float* __restrict__ part, int splits, int M, float* __restrict__ out, int beta) {
   pdl_wait();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
@@ -890,14 +904,15 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   if (EPI == EPI_F32_ACC) split_k_plan(tiles, static_cast<int>(ceil_div(g.K, tc::BK)), pairs, st, ep);
   const int items = tiles * ep.splits;
   const int grid = 2 * (items < pairs ? items : pairs);
-  if (CS && ep.splits > 1) ep.bias_part = bias_partials(st, static_cast<size_t>(ep.splits) * g.M);
+  const int num_n = static_cast<int>(ceil_div(g.N, BN));
+  if (CS) ep.bias_part = bias_partials(st, static_cast<size_t>(ep.splits) * num_n * g.M);
   CUtensorMap tcm, txm;
   epi_tmaps<EPI>(g, tcm, txm);
   launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, ep, g.M, g.N, g.K);
   ZB_LAUNCH_CHECK();
-  if (CS && ep.splits > 1) {
+  if (CS) {
     launch(PDL_OPS, k_bias_finalize, static_cast<int>(ceil_div(g.M, 256)), 256, 0, st,
-           static_cast<const float*>(ep.bias_part), static_cast<int>(ep.splits), g.M, ep.bias_out,
+           static_cast<const float*>(ep.bias_part), static_cast<int>(ep.splits * num_n), g.M, ep.bias_out,
            static_cast<int>(ep.beta));
     ZB_LAUNCH_CHECK();
   }

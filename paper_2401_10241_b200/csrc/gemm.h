@@ -46,7 +46,7 @@ struct EpiArgs {
   // column sums of dY (P:46's W of a bias).  The 2-CTA kernel forms them from the A tiles it
   // already streams (column-sum warps, gemm.cu); other paths fall back to ops.h bias_grad.
   float* bias_out = nullptr;
-  float* bias_part = nullptr;  // set by gemm(): per-split partial sums [splits, M]
+  float* bias_part = nullptr;  // set by gemm(): partial sums [splits * n-tiles, M]
 };
 
 struct GemmArgs {
