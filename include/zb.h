@@ -227,8 +227,17 @@ zb_status_t zb_stage_backward_weight(zb_ctx_t* ctx, int32_t mb, int32_t slot);
 
 enum { ZB_RUN_HOST_INPUTS = 1, /* tokens / labels are host pointers: H2D inside the call */
        ZB_RUN_TIMING = 2,      /* record CUDA events at every pass boundary               */
-       ZB_RUN_FUSED_BW = 4     /* 1F1B: send the input gradient after the W that follows  */
-                               /* its B (the monolithic backward of the baseline, C5)     */ };
+       ZB_RUN_FUSED_BW = 4,    /* 1F1B: send the input gradient after the W that follows  */
+                               /* its B (the monolithic backward of the baseline, C5)     */
+       ZB_RUN_GROUP_W = 8      /* W-grouping ("W ... anywhere after    */
+                               /* the corresponding B"): up to 4 W passes that are ADJACENT */
+                               /* in a stage's list run as one contraction per linear with */
+                               /* K = k*T (one f32 gradient read-modify-write for k         */
+                               /* microbatches).  The sums are grouped differently, so      */
+                               /* results are bitwise equal between runs / runtimes with    */
+                               /* the same adjacency, within tolerance otherwise.  Not for  */
+                               /* zb_run_iteration_worker.  A timed group records one event */
+                               /* pair; zb_ctx_profile counts it as k W passes of 1/k each. */ };
 
 typedef struct {
   int32_t n_passes;

@@ -29,6 +29,13 @@ zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const vo
                         const void* B, int64_t ldb, int32_t b_mn, int32_t epi, void* C, int64_t ldc,
                         const float* bias, void* aux, int64_t ldaux, int32_t beta, void* stream);
 
+/* W-grouping contraction (bf16): C[M,N] (beta ? += : =) sum over the nseg
+ * segments s of A_s^T B_s with A_s = dY_s [K/nseg, M] and B_s = X_s [K/nseg, N] (dev,
+ * row-major, MN-major operands, K/nseg a multiple of 64); bias_out (nullable, f32 [M]) gets
+ * the column sums of all A_s the same way.  nseg in 1..4. */
+zb_status_t zb_dbg_gemm_wgroup(int32_t M, int32_t N, int32_t K, int32_t nseg, const void* const* A_seg,
+                               const void* const* B_seg, float* C, float* bias_out, int32_t beta, void* stream);
+
 /* Causal multi-head attention forward on a packed qkv [b*s, 3h] (Q, K, V
  * column blocks, head k at columns k*d of each): o [b*s, h], lse [b, a, s] f32. */
 zb_status_t zb_dbg_attention_fwd(int32_t dtype, int32_t b, int32_t s, int32_t a, int32_t d, const void* qkv,

@@ -20,7 +20,7 @@ FAMILY = {"1f1b": ZB_1F1B, "zbh1": ZB_H1, "zbh2": ZB_H2, "auto": ZB_AUTO}
 ZB_V, ZB_1F1B_I = 4, 5
 CHUNKED_FAMILY = {"zbv": ZB_V, "1f1bi": ZB_1F1B_I}
 ZB_DTYPE_BF16, ZB_DTYPE_F32 = 0, 1
-ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING = 1, 2
+ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_RUN_FUSED_BW, ZB_RUN_GROUP_W = 1, 2, 4, 8
 ZB_OPT_SYNC, ZB_OPT_PV = 0, 1
 ZB_MAX_STAGES = 64
 
@@ -91,6 +91,7 @@ _SIGS = {
                      _I64, _I64, _I64, _I32, C.POINTER(zb_sim_t)], _I32),
     "zb_dbg_gemm": ([_I32, _I32, _I32, _I32, _P, _I64, _I32, _P, _I64, _I32, _I32, _P, _I64, _P, _P, _I64, _I32, _P],
                     _I32),
+    "zb_dbg_gemm_wgroup": ([_I32, _I32, _I32, _I32, C.POINTER(_P), C.POINTER(_P), _P, _P, _I32, _P], _I32),
     "zb_dbg_layernorm_fwd": ([_I32, _P, _P, _P, _P, _P, _P, _I32, _I32, C.c_float, _P], _I32),
     "zb_dbg_layernorm_bwd": ([_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _I32, _I32, _P], _I32),
     "zb_dbg_bias_grad": ([_I32, _P, _I64, _P, _I32, _I32, _I32, _P], _I32),

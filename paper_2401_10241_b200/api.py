@@ -10,7 +10,8 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from ._lib import (CHUNKED_FAMILY, FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING,
+from ._lib import (CHUNKED_FAMILY, FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_FUSED_BW,
+                   ZB_RUN_GROUP_W, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING,
                    ACTIONS, check, lib, zb_iter_stats_t, zb_model_cfg_t, zb_optim_cfg_t, zb_pass_t, zb_pv_report_t,
                    zb_sim_t)
 
@@ -240,8 +241,10 @@ class Context:
         check(lib.zb_ctx_attach_loopback(self.h, group.h, self.stage))
         self._group = group
 
-    def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False, fused=False):
-        flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0) | (4 if fused else 0)
+    def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False, fused=False,
+                      group_w=False):
+        flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0) | \
+            (ZB_RUN_FUSED_BW if fused else 0) | (ZB_RUN_GROUP_W if group_w else 0)
         tp = tokens.ctypes.data if host_inputs and tokens is not None else _ptr(tokens)
         lp = labels.ctypes.data if host_inputs and labels is not None else _ptr(labels)
         check(lib.zb_run_iteration(self.h, passes, len(passes), tp, lp, flags))
@@ -317,9 +320,10 @@ def optim_cfg(lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, clip=1
     return zb_optim_cfg_t(lr, beta1, beta2, eps, weight_decay, clip, ZB_OPT_PV if mode == "pv" else ZB_OPT_SYNC)
 
 
-def run_local(ctxs: Sequence[Context], passes, tokens, labels, host_inputs=False, timing=False):
+def run_local(ctxs: Sequence[Context], passes, tokens, labels, host_inputs=False, timing=False, group_w=False):
     arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
-    flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0)
+    flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0) | \
+        (ZB_RUN_GROUP_W if group_w else 0)
     tp = tokens.ctypes.data if host_inputs else _ptr(tokens)
     lp = labels.ctypes.data if host_inputs else _ptr(labels)
     check(lib.zb_run_iteration_local(arr, len(ctxs), passes, len(passes), tp, lp, flags))
@@ -367,6 +371,15 @@ def dbg_gemm(A, B, C_out, *, M, N, K, a_mn=False, b_mn=False, epi=0, bias=None, 
     ldaux = ldaux if ldaux is not None else (aux.shape[-1] if aux is not None else 0)
     check(lib.zb_dbg_gemm(dtype, M, N, K, _ptr(A), lda, int(a_mn), _ptr(B), ldb, int(b_mn), epi, _ptr(C_out), ldc,
                           _ptr(bias), _ptr(aux), ldaux, beta, _stream(stream)))
+
+
+def dbg_gemm_wgroup(A_segs, B_segs, C_out, *, M, N, bias=None, beta=0, stream=None):
+    """zb_dbg_gemm_wgroup: C (+)= sum_s A_s^T B_s over nseg = len(A_segs) segments."""
+    n = len(A_segs)
+    K = sum(int(a.shape[0]) for a in A_segs)
+    ap = (C.c_void_p * n)(*[a.data_ptr() for a in A_segs])
+    bp = (C.c_void_p * n)(*[b.data_ptr() for b in B_segs])
+    check(lib.zb_dbg_gemm_wgroup(M, N, K, n, ap, bp, _ptr(C_out), _ptr(bias), beta, _stream(stream)))
 
 
 def dbg_layernorm_fwd(x, g, b, y, mean, rstd, *, rows, h, eps=1e-5, stream=None):

@@ -5,6 +5,7 @@
 
 #include "abi_util.h"
 #include "comm.h"
+#include "gemm.h"
 #include "stage.h"
 
 using namespace zb;
@@ -310,17 +311,31 @@ extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, 
     begin_iteration(*c);
     const int T = c->T;
     c->n_timed = 0;
-    for (int i = 0; i < n; ++i) {
-      const zb_pass_t& q = passes[i];
-      if (q.stage != c->cfg.stage) continue;
+    std::vector<const zb_pass_t*> mine;
+    for (int i = 0; i < n; ++i)
+      if (passes[i].stage == c->cfg.stage) mine.push_back(&passes[i]);
+    for (size_t i = 0; i < mine.size(); ++i) {
+      const zb_pass_t& q = *mine[i];
+      if (q.kind == ZB_W) {
+        int mbs[kMaxSeg], sls[kMaxSeg], k = 0;
+        const int gmax = (flags & ZB_RUN_GROUP_W) ? kMaxSeg : 1;
+        while (k < gmax && i + k < mine.size() && mine[i + k]->kind == ZB_W) {
+          mbs[k] = mine[i + k]->microbatch;
+          sls[k] = mine[i + k]->slot;
+          ++k;
+        }
+        if (flags & ZB_RUN_TIMING) c->timing_begin(c->n_timed, ZB_W, k);
+        c->backward_weight_group(mbs, sls, k);
+        if (flags & ZB_RUN_TIMING) c->timing_end(c->n_timed++);
+        i += k - 1;
+        continue;
+      }
       if (flags & ZB_RUN_TIMING) c->timing_begin(c->n_timed, q.kind);
       if (q.kind == ZB_F)
         c->forward(q.microbatch, q.slot, tokens + static_cast<int64_t>(q.microbatch) * T, nullptr,
                    labels + static_cast<int64_t>(q.microbatch) * T);
-      else if (q.kind == ZB_B)
-        c->backward_input(q.microbatch, q.slot, nullptr, nullptr);
       else
-        c->backward_weight(q.microbatch, q.slot);
+        c->backward_input(q.microbatch, q.slot, nullptr, nullptr);
       if (flags & ZB_RUN_TIMING) c->timing_end(c->n_timed++);
     }
     return ZB_OK;
@@ -432,7 +447,22 @@ extern "C" zb_status_t zb_run_iteration_local(zb_ctx_t* const* ctxs, int32_t p, 
             void* dx = s > 0 ? c[s - 1]->slots[slot[s - 1][j]].dy32 : nullptr;
             cs.backward_input(j, q.slot, s < p - 1 ? cs.slots[q.slot].dy32 : nullptr, dx);
           } else {
-            cs.backward_weight(j, q.slot);
+            // W-grouping: the W passes adjacent to this one in the stage's list (their Bs precede
+            // this W in list order, so they are done)
+            int mbs[kMaxSeg], sls[kMaxSeg], k = 0;
+            const int gmax = (flags & ZB_RUN_GROUP_W) ? kMaxSeg : 1;
+            while (k < gmax && pos[s] + k < L[s].size() && L[s][pos[s] + k]->kind == ZB_W) {
+              mbs[k] = L[s][pos[s] + k]->microbatch;
+              sls[k] = L[s][pos[s] + k]->slot;
+              ++k;
+            }
+            if (flags & ZB_RUN_TIMING) cs.ev_group[cs.n_timed] = k;
+            cs.backward_weight_group(mbs, sls, k);
+            for (int i = 1; i < k; ++i) {  // the group's other passes are done too
+              done[ZB_W][s][mbs[i]] = 1;
+              ++pos[s];
+              --remaining;
+            }
           }
           if (flags & ZB_RUN_TIMING) cs.timing_end(cs.n_timed++);
           done[q.kind][s][j] = 1;
@@ -483,7 +513,9 @@ extern "C" zb_status_t zb_ctx_profile(zb_ctx_t* ctx, int32_t reset, int64_t* T_n
       for (int i = 0; i < c->n_timed; ++i) {
         float ms = 0.f;
         ZB_CUDA(cudaEventElapsedTime(&ms, c->ev_start[i], c->ev_end[i]));
-        c->prof_ns[c->ev_kind[i]].push_back(static_cast<int64_t>(static_cast<double>(ms) * 1e6 + 0.5));
+        const int g = c->ev_group[i];  // a grouped W entry covers g W passes
+        for (int k = 0; k < g; ++k)
+          c->prof_ns[c->ev_kind[i]].push_back(static_cast<int64_t>(static_cast<double>(ms) * 1e6 / g + 0.5));
       }
       c->prof_collected_run = c->timed_runs;
     }

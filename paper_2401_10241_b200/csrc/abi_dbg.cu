@@ -34,6 +34,30 @@ extern "C" zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t 
 }
 
 
+extern "C" zb_status_t zb_dbg_gemm_wgroup(int32_t M, int32_t N, int32_t K, int32_t nseg, const void* const* A_seg,
+                                          const void* const* B_seg, float* C, float* bias_out, int32_t beta,
+                                          void* stream) {
+  ZB_TRY {
+    if (M <= 0 || N <= 0 || K <= 0 || nseg < 1 || nseg > kMaxSeg || !A_seg || !B_seg || !C)
+      return set_error(ZB_EINVAL, "bad grouped W arguments");
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = K;
+    g.A = A_seg[0]; g.lda = M; g.a_mn = true;
+    g.B = B_seg[0]; g.ldb = N; g.b_mn = true;
+    g.epi = EPI_F32_ACC;
+    g.ep = EpiArgs{C, N, nullptr, nullptr, 0, beta};
+    g.ep.bias_out = bias_out;
+    g.nseg = nseg;
+    for (int i = 0; i < nseg; ++i) {
+      g.A_seg[i] = A_seg[i];
+      g.B_seg[i] = B_seg[i];
+    }
+    gemm(g, DT_BF16, static_cast<cudaStream_t>(stream));
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 extern "C" zb_status_t zb_dbg_attention_fwd(int32_t dtype, int32_t b, int32_t s, int32_t a, int32_t d,
                                             const void* qkv, void* o, float* lse, void* stream) {
   ZB_TRY {

@@ -33,6 +33,7 @@
 #include <string>
 
 #include "abi_util.h"
+#include "gemm.h"
 #include "ops.h"
 #include "plan.h"
 #include "stage.h"
@@ -640,6 +641,17 @@ struct StageExec {
         throw Error(ZB_EINVAL, "StageExec: unexpected op");
     }
   }
+  // W-grouping (ZB_RUN_GROUP_W): k adjacent W ops as one contraction per linear
+  void exec_w_group(const plan::Op* ops, int k) {
+    int mbs[kMaxSeg], sls[kMaxSeg];
+    for (int i = 0; i < k; ++i) {
+      mbs[i] = ops[i].mb;
+      sls[i] = ops[i].slot;
+    }
+    if (flags & ZB_RUN_TIMING) c.timing_begin(c.n_timed, ZB_W, k);
+    c.backward_weight_group(mbs, sls, k);
+    if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
+  }
 };
 
 void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* tokens, const int32_t* labels,
@@ -655,6 +667,13 @@ void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* t
   bool switched = false;
   for (size_t k = 0; k < ops.size(); ++k) {
     const plan::Op op = ops[k];
+    if (op.type == plan::OP_W && (flags & ZB_RUN_GROUP_W)) {
+      int g = 1;
+      while (g < kMaxSeg && k + g < ops.size() && ops[k + g].type == plan::OP_W) ++g;
+      ex.exec_w_group(&ops[k], g);
+      k += g - 1;
+      continue;
+    }
     if (op.type != plan::OP_VALIDATE) {
       ex.exec(op);
       continue;

@@ -429,11 +429,17 @@ __device__ __forceinline__ void colsum_stage(const uint8_t* sa, int t, float* ac
   }
 }
 
+// W-grouping: per-segment A / B tensor maps (segment s = k-blocks [s kbseg, (s+1) kbseg))
+struct SegMaps {
+  CUtensorMap a[kMaxSeg], b[kMaxSeg];
+  int nseg, kbseg;
+};
+
 template <int BN, bool A_MN, bool B_MN, int EPI, typename TO, bool CS = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const EpiArgs ep,
-               int M, int N, int K) {
+               int M, int N, int K, const __grid_constant__ SegMaps sg) {
   static_assert(!CS || (A_MN && EPI == EPI_F32_ACC), "column sums: W's A operand only");
   using C = Cfg2<BN>;
   constexpr int BM2 = 2 * BM;
@@ -469,6 +475,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     sm100::tma_prefetch(&tmB);
     sm100::tma_prefetch(&tmC);
     sm100::tma_prefetch(&tmX);
+    for (int i = 0; i < sg.nseg; ++i) {
+      sm100::tma_prefetch(&sg.a[i]);
+      sm100::tma_prefetch(&sg.b[i]);
+    }
   }
   if (warp == 2) sm100::tmem_alloc_pair<C::TMEM_COLS>(tslot);
   sm100::tc_fence_before();
@@ -506,18 +516,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             sm100::mbar_arrive_cluster(fbar);
           uint8_t* sa = smem + stage * C::STAGE;
           uint8_t* sb = sa + A_BYTES;
-          const int k0 = kb * BK;
+          int k0 = kb * BK;
+          const CUtensorMap* mA = &tmA;
+          const CUtensorMap* mB = &tmB;
+          if (sg.nseg > 1) {  // W-grouping: the k-block's microbatch segment
+            const int sgi = kb / sg.kbseg;
+            mA = &sg.a[sgi];
+            mB = &sg.b[sgi];
+            k0 = (kb - sgi * sg.kbseg) * BK;
+          }
           if (!A_MN) {
-            sm100::tma_load_2d_pair(sa, &tmA, fbar, k0, m0);
+            sm100::tma_load_2d_pair(sa, mA, fbar, k0, m0);
           } else {
-            sm100::tma_load_2d_pair(sa, &tmA, fbar, m0, k0);
-            sm100::tma_load_2d_pair(sa + 8192, &tmA, fbar, m0 + 64, k0);
+            sm100::tma_load_2d_pair(sa, mA, fbar, m0, k0);
+            sm100::tma_load_2d_pair(sa + 8192, mA, fbar, m0 + 64, k0);
           }
           if (!B_MN) {
-            sm100::tma_load_2d_pair(sb, &tmB, fbar, k0, n0);
+            sm100::tma_load_2d_pair(sb, mB, fbar, k0, n0);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 128; ++i) sm100::tma_load_2d_pair(sb + i * 8192, &tmB, fbar, n0 + 64 * i, k0);
+            for (int i = 0; i < BN / 128; ++i) sm100::tma_load_2d_pair(sb + i * 8192, mB, fbar, n0 + 64 * i, k0);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -896,8 +914,22 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
     ZB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  CUtensorMap ta = A_MN ? make_tmap(g.A, g.M, g.K, g.lda, 64, 64) : make_tmap(g.A, g.K, g.M, g.lda, 64, tc::BM);
-  CUtensorMap tb = B_MN ? make_tmap(g.B, g.N, g.K, g.ldb, 64, 64) : make_tmap(g.B, g.K, g.N, g.ldb, 64, BN / 2);
+  tc::SegMaps sg{};
+  sg.nseg = g.nseg > 1 ? g.nseg : 1;
+  CUtensorMap ta, tb;
+  if (sg.nseg > 1) {  // W-grouping: one map pair per microbatch segment (MN-major W operands)
+    const int kseg = g.K / sg.nseg;
+    sg.kbseg = kseg / tc::BK;
+    for (int i = 0; i < sg.nseg; ++i) {
+      sg.a[i] = make_tmap(g.A_seg[i], g.M, kseg, g.lda, 64, 64);
+      sg.b[i] = make_tmap(g.B_seg[i], g.N, kseg, g.ldb, 64, 64);
+    }
+    ta = sg.a[0];
+    tb = sg.b[0];
+  } else {
+    ta = A_MN ? make_tmap(g.A, g.M, g.K, g.lda, 64, 64) : make_tmap(g.A, g.K, g.M, g.lda, 64, tc::BM);
+    tb = B_MN ? make_tmap(g.B, g.N, g.K, g.ldb, 64, 64) : make_tmap(g.B, g.K, g.N, g.ldb, 64, BN / 2);
+  }
   const int tiles = static_cast<int>(ceil_div(g.M, 2 * tc::BM) * ceil_div(g.N, BN));
   const int pairs = num_sms() / 2;
   EpiArgs ep = g.ep;
@@ -908,7 +940,7 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   if (CS) ep.bias_part = bias_partials(st, static_cast<size_t>(ep.splits) * num_n * g.M);
   CUtensorMap tcm, txm;
   epi_tmaps<EPI>(g, tcm, txm);
-  launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, ep, g.M, g.N, g.K);
+  launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, ep, g.M, g.N, g.K, sg);
   ZB_LAUNCH_CHECK();
   if (CS) {
     launch(PDL_OPS, k_bias_finalize, static_cast<int>(ceil_div(g.M, 256)), 256, 0, st,
@@ -987,6 +1019,25 @@ static void dispatch_epi_f32(const GemmArgs& g, cudaStream_t st) {
 
 void gemm(const GemmArgs& g, DType dt, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
+  if (g.nseg > 1) {
+    if (g.nseg > kMaxSeg || !g.a_mn || !g.b_mn || g.epi != EPI_F32_ACC || g.K % g.nseg || (g.K / g.nseg) % 64)
+      throw CudaError("gemm: W-grouping needs the W contraction, <= 4 segments of a multiple of 64 tokens");
+    // the 2-CTA tcgen05 kernel walks the segments inside one accumulation; elsewhere (f32 parity
+    // mode, small 1-CTA shapes) the segments are accumulated one after the other
+    if (dt == DT_F32 || g.N <= 128 || !use_pair(g)) {
+      const int kseg = g.K / g.nseg;
+      for (int i = 0; i < g.nseg; ++i) {
+        GemmArgs s1 = g;
+        s1.nseg = 1;
+        s1.K = kseg;
+        s1.A = g.A_seg[i];
+        s1.B = g.B_seg[i];
+        if (i > 0) s1.ep.beta = 1;
+        gemm(s1, dt, st);
+      }
+      return;
+    }
+  }
   if (g.N % 8 != 0 || g.ep.ldc % 8 != 0) throw CudaError("gemm: N and ldc must be multiples of 8");
   if (g.ep.bias_out != nullptr && (g.epi != EPI_F32_ACC || !g.a_mn))
     throw CudaError("gemm: bias_out is W's bias gradient (EPI_F32_ACC, MN-major A)");

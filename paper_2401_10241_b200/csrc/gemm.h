@@ -49,6 +49,8 @@ struct EpiArgs {
   float* bias_part = nullptr;  // set by gemm(): partial sums [splits * n-tiles, M]
 };
 
+constexpr int kMaxSeg = 4;
+
 struct GemmArgs {
   int32_t M, N, K;
   const void* A;
@@ -59,6 +61,13 @@ struct GemmArgs {
   bool b_mn;
   int32_t epi;
   EpiArgs ep;
+  // W-grouping: the K = T tokens of nseg microbatches as ONE
+  // contraction — segment s covers K rows [s K/nseg, (s+1) K/nseg) of A and B at
+  // A_seg[s] / B_seg[s] (same lda / ldb; MN-major W operands only; K/nseg % 64 == 0).
+  // nseg <= 1: A / B as above.
+  int32_t nseg = 1;
+  const void* A_seg[kMaxSeg] = {nullptr, nullptr, nullptr, nullptr};
+  const void* B_seg[kMaxSeg] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 // Throws zb::CudaError on launch failure / unsupported shapes.

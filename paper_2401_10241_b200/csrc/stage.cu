@@ -330,31 +330,59 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
 }
 
 // ------------------------------------------------------------------ W
-void Ctx::backward_weight(int mb, int slot_idx) {
-  (void)mb;
-  Slot& sl = slots.at(slot_idx);
+void Ctx::backward_weight(int mb, int slot_idx) { backward_weight_group(&mb, &slot_idx, 1); }
+
+// W of k microbatches at once (W-grouping; P:59 lets a W run anywhere after
+// its B): each linear's dW (+ its bias column sums) is ONE contraction over K = k T tokens
+// whose segments are the k slots' (dY, X) operands, so at b = 1 (T = 1024) the f32
+// gradient read-modify-write is amortised over k microbatches.  k = 1 is the plain W.
+void Ctx::backward_weight_group(const int* mbs, const int* slot_idx, int k) {
+  (void)mbs;
+  if (k < 1 || k > kMaxSeg) throw std::invalid_argument("W group of 1..4 microbatches");
+  std::vector<Slot*> sl(k);
+  for (int i = 0; i < k; ++i) sl[i] = &slots.at(slot_idx[i]);
   const int H = h;
   const int beta = first_w_done ? 1 : 0;
+  auto wgrad = [&](auto dy_of, auto x_of, float* dW, float* db, int M, int N) {
+    GemmArgs g{};
+    g.M = M; g.N = N; g.K = k * T;
+    g.A = dy_of(*sl[0]); g.lda = M; g.a_mn = true;
+    g.B = x_of(*sl[0]); g.ldb = N; g.b_mn = true;
+    g.epi = EPI_F32_ACC;
+    g.ep = EpiArgs{dW, N, nullptr, nullptr, 0, beta};
+    g.ep.bias_out = db;
+    if (k > 1) {
+      g.nseg = k;
+      for (int i = 0; i < k; ++i) {
+        g.A_seg[i] = dy_of(*sl[i]);
+        g.B_seg[i] = x_of(*sl[i]);
+      }
+    }
+    gemm(g, dt, stream);
+  };
   for (int l = Ls - 1; l >= 0; --l) {
-    LayerAct& A = sl.L[l];
     const LayerW& w = lw[l];
-    void* dx2 = l == Ls - 1 ? sl.dy : sl.L[l + 1].x;
-    lin_wgrad(*this, dx2, A.g, w.g_fc2_w, w.g_fc2_b, H, 4 * H, T, beta);
-    lin_wgrad(*this, A.u, A.ln2, w.g_fc1_w, w.g_fc1_b, 4 * H, H, T, beta);
-    lin_wgrad(*this, A.x1, A.o, w.g_proj_w, w.g_proj_b, H, H, T, beta);
-    lin_wgrad(*this, A.qkv, A.ln1, w.g_qkv_w, w.g_qkv_b, 3 * H, H, T, beta);
+    const bool top = l == Ls - 1;
+    wgrad([&](Slot& q) -> const void* { return top ? q.dy : q.L[l + 1].x; },
+          [&](Slot& q) -> const void* { return q.L[l].g; }, w.g_fc2_w, w.g_fc2_b, H, 4 * H);
+    wgrad([&](Slot& q) -> const void* { return q.L[l].u; }, [&](Slot& q) -> const void* { return q.L[l].ln2; },
+          w.g_fc1_w, w.g_fc1_b, 4 * H, H);
+    wgrad([&](Slot& q) -> const void* { return q.L[l].x1; }, [&](Slot& q) -> const void* { return q.L[l].o; },
+          w.g_proj_w, w.g_proj_b, H, H);
+    wgrad([&](Slot& q) -> const void* { return q.L[l].qkv; }, [&](Slot& q) -> const void* { return q.L[l].ln1; },
+          w.g_qkv_w, w.g_qkv_b, 3 * H, H);
   }
   if (first) {
     if (!first_w_done) {
       ZB_CUDA(cudaMemsetAsync(g_wte, 0, sizeof(float) * static_cast<size_t>(V) * H, stream));
       ZB_CUDA(cudaMemsetAsync(g_wpe, 0, sizeof(float) * static_cast<size_t>(s) * H, stream));
     }
-    embed_bwd(dt, sl.tok, sl.L[0].x, g_wte, g_wpe, keys, T, s, H, stream);
+    for (int i = 0; i < k; ++i) embed_bwd(dt, sl[i]->tok, sl[i]->L[0].x, g_wte, g_wpe, keys, T, s, H, stream);
   }
   first_w_done = true;
 }
 
-void Ctx::timing_begin(int idx, int kind) {
+void Ctx::timing_begin(int idx, int kind, int group) {
   while (static_cast<int>(ev_start.size()) <= idx) {
     cudaEvent_t a, b;
     ZB_CUDA(cudaEventCreate(&a));
@@ -362,8 +390,10 @@ void Ctx::timing_begin(int idx, int kind) {
     ev_start.push_back(a);
     ev_end.push_back(b);
     ev_kind.push_back(0);
+    ev_group.push_back(1);
   }
   ev_kind[idx] = kind;
+  ev_group[idx] = group;
   if (idx == 0) ++timed_runs;
   ZB_CUDA(cudaEventRecord(ev_start[idx], stream));
 }

@@ -94,7 +94,7 @@ struct Ctx {
   // timing (ZB_RUN_TIMING): events around every pass of the last timed run, the pass
   // kinds, and the per-kind durations collected by zb_ctx_profile (a1)
   std::vector<cudaEvent_t> ev_start, ev_end;
-  std::vector<int> ev_kind;
+  std::vector<int> ev_kind, ev_group;  // kind of the timed entry; W passes it covers (W-grouping)
   int n_timed = 0;
   std::vector<int64_t> prof_ns[3];
   int64_t timed_runs = 0, prof_collected_run = 0;  // a timed run starts at pass index 0
@@ -107,8 +107,9 @@ struct Ctx {
   void forward(int mb, int slot, const void* in, void* out, const int32_t* labels);
   void backward_input(int mb, int slot, const void* dy, void* dx);
   void backward_weight(int mb, int slot);
+  void backward_weight_group(const int* mbs, const int* slots, int k);  // W-grouping (k <= 4)
 
-  void timing_begin(int idx, int kind);
+  void timing_begin(int idx, int kind, int group = 1);
   void timing_end(int idx);
 };
 
