@@ -154,8 +154,16 @@ typedef struct {
   int32_t n_slots;          /* activation-stash slots (zb_sim_t.n_slots[stage])                 */
   int32_t dtype;            /* ZB_DTYPE_BF16: tcgen05 bf16 GEMMs, f32 accumulation;             */
                             /* ZB_DTYPE_F32: f32 everywhere (1e-5 parity mode)                   */
-  int32_t reserved;
+  int32_t flags;            /* ZB_CFG_* below (0 = defaults)                                    */
 } zb_model_cfg_t;
+
+/* zb_model_cfg_t.flags.  The last stage's LM-head weight gradient dW_head += dlogits^T LN_f
+ * is a W computation and by default runs in the stage's W pass: the bf16 dlogits
+ * [T, V] of a microbatch stay in its stash slot from B to W (M_B / M_W of the last stage grow
+ * by 2 T V bytes; the B pass loses one T x V x h GEMM, which balances the head-carrying stage,
+ * DESIGN.md R-head).  ZB_CFG_HEAD_W_EAGER runs it inside B instead (round-1 behaviour, no
+ * dlogits stash).  Gradients are bitwise identical either way (same per-microbatch order). */
+enum { ZB_CFG_HEAD_W_EAGER = 1 };
 
 typedef struct zb_ctx zb_ctx_t;
 

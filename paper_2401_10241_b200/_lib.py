@@ -22,6 +22,7 @@ CHUNKED_FAMILY = {"zbv": ZB_V, "1f1bi": ZB_1F1B_I}
 ZB_DTYPE_BF16, ZB_DTYPE_F32 = 0, 1
 ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_RUN_FUSED_BW, ZB_RUN_GROUP_W = 1, 2, 4, 8
 ZB_OPT_SYNC, ZB_OPT_PV = 0, 1
+ZB_CFG_HEAD_W_EAGER = 1
 ZB_MAX_STAGES = 64
 
 ACTIONS = {0: "none", 1: "step", 2: "skip", 3: "defer", 4: "rollback", 5: "rollback+redo", 6: "deferred-step",
@@ -47,7 +48,7 @@ class zb_sim_t(C.Structure):
 
 class zb_model_cfg_t(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("h", "a", "L", "s", "b", "V", "p", "stage", "layer_first", "layer_last",
-                                         "m", "n_slots", "dtype", "reserved")]
+                                         "m", "n_slots", "dtype", "flags")]
 
 
 class zb_iter_stats_t(C.Structure):

@@ -11,7 +11,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from ._lib import (CHUNKED_FAMILY, FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_FUSED_BW,
-                   ZB_RUN_GROUP_W, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING,
+                   ZB_RUN_GROUP_W, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_CFG_HEAD_W_EAGER,
                    ACTIONS, check, lib, zb_iter_stats_t, zb_model_cfg_t, zb_optim_cfg_t, zb_pass_t, zb_pv_report_t,
                    zb_sim_t)
 
@@ -121,10 +121,11 @@ def _stream(stream) -> Optional[int]:
 
 # ------------------------------------------------------------------ stage context
 
-def model_cfg(cfg, p: int, stage: int, m: int, n_slots: int, dtype: str = "bf16") -> zb_model_cfg_t:
+def model_cfg(cfg, p: int, stage: int, m: int, n_slots: int, dtype: str = "bf16",
+              head_w_eager: bool = False) -> zb_model_cfg_t:
     first, last = stage_layers(cfg.L, p, stage)
     return zb_model_cfg_t(cfg.h, cfg.a, cfg.L, cfg.s, cfg.b, cfg.V, p, stage, first, last, m, n_slots,
-                          ZB_DTYPE_BF16 if dtype == "bf16" else ZB_DTYPE_F32, 0)
+                          ZB_DTYPE_BF16 if dtype == "bf16" else ZB_DTYPE_F32, 1 if head_w_eager else 0)
 
 
 def arena_bytes(mc: zb_model_cfg_t) -> int:
@@ -142,10 +143,11 @@ def slot_bytes(mc: zb_model_cfg_t) -> int:
 class Context:
     """One pipeline stage (zb_ctx_t) with a torch-allocated device arena."""
 
-    def __init__(self, cfg, p: int, stage: int, m: int, n_slots: int, dtype: str = "bf16", stream=None):
+    def __init__(self, cfg, p: int, stage: int, m: int, n_slots: int, dtype: str = "bf16", stream=None,
+                 head_w_eager: bool = False):
         import torch
         self.cfg, self.p, self.stage, self.m, self.dtype = cfg, p, stage, m, dtype
-        self.mc = model_cfg(cfg, p, stage, m, n_slots, dtype)
+        self.mc = model_cfg(cfg, p, stage, m, n_slots, dtype, head_w_eager)
         self.nbytes = arena_bytes(self.mc)
         self.arena = torch.empty(self.nbytes, dtype=torch.uint8, device="cuda")
         self.stream = stream if stream is not None else torch.cuda.current_stream()

@@ -3,14 +3,15 @@
 // F  (per layer)  LN1 -> QKV = LN1 Wqkv^T + b -> causal attention -> X1 = X + O Wproj^T + b
 //                 -> LN2 -> U = LN2 Wfc1^T + b, G = GeLU(U) -> X' = X1 + G Wfc2^T + b
 //                 stage 0 starts with the embedding; the last stage ends with LN_f.
-// B  (reverse)    last stage: logits = LN_f Whead^T, cross-entropy -> dlogits,
-//                 dWhead (eager), d LN_f; per layer: dU = (dX' Wfc2) * GeLU'(U),
+// B  (reverse)    last stage: logits = LN_f Whead^T, cross-entropy -> dlogits (kept in the
+//                 slot for W), d LN_f; per layer: dU = (dX' Wfc2) * GeLU'(U),
 //                 dLN2 = dU Wfc1, dX1 = dX' + LN2_bwd, dO = dX1 Wproj, dQKV = attn_bwd,
 //                 dLN1 = dQKV Wqkv, dX = dX1 + LN1_bwd; LayerNorm gamma/beta grads
 //                 (deterministic chunk partials) are taken here (DESIGN.md R-ln).
 // W  (per layer)  dW += dY^T X for fc2 (dX', G), fc1 (dU, LN2), proj (dX1, O),
 //                 qkv (dQKV, LN1) with f32 accumulation into the persistent grads,
 //                 bias grads = column sums of dY formed inside the same GEMMs;
+//                 last stage: dWhead += dlogits^T LN_f (ZB_CFG_HEAD_W_EAGER: in B);
 //                 stage 0: embedding scatter.
 // In-place reuse keeps M_W = M_B: dU over U, dX1 over X1, dX over X, dQKV
 // pointer-swapped with QKV.
@@ -68,6 +69,7 @@ size_t carve(Ctx& c, uint8_t* base) {
   c.V = g.V; c.s = g.s; c.b = g.b; c.T = g.b * g.s;
   c.first = g.stage == 0;
   c.last = g.stage == g.p - 1;
+  c.head_w_eager = (g.flags & ZB_CFG_HEAD_W_EAGER) != 0;
   const int64_t h = c.h, T = c.T, V = c.V, Ls = c.Ls;
 
   // ---- flat parameter offsets (elements, 64-element aligned)
@@ -175,9 +177,11 @@ size_t carve(Ctx& c, uint8_t* base) {
       sl.lnf = bp.take_bytes(T * h * e);
       sl.muf = bp.take<float>(T);
       sl.rsf = bp.take<float>(T);
+      sl.dlogits = c.head_w_eager ? nullptr : bp.take_bytes(T * V * e);
     } else {
       sl.xl = sl.lnf = nullptr;
       sl.muf = sl.rsf = nullptr;
+      sl.dlogits = nullptr;
     }
   }
   // ---- scratch
@@ -189,7 +193,7 @@ size_t carve(Ctx& c, uint8_t* base) {
   c.delta = bp.take<float>(static_cast<size_t>(c.a) * T);
   if (c.last) {
     c.logits = bp.take<float>(T * V);
-    c.dlogits = bp.take_bytes(T * V * e);
+    c.dlogits = c.head_w_eager ? bp.take_bytes(T * V * e) : nullptr;  // deferred: per slot
     c.loss_rows = bp.take<float>(T);
     c.lab_stage = bp.take<int32_t>(static_cast<size_t>(g.m) * T);
   }
@@ -295,11 +299,12 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
   // dgrad GEMMs now and the wgrad GEMMs in W.
   const float* dx2_32;
   if (last) {
+    void* dl = head_w_eager ? dlogits : sl.dlogits;
     lin_fwd(*this, sl.lnf, head_w, nullptr, logits, T, V, H, EPI_F32_STORE, nullptr);
-    cross_entropy(dt, logits, sl.lab, dlogits, loss_rows, loss_acc, T, V,
+    cross_entropy(dt, logits, sl.lab, dl, loss_rows, loss_acc, T, V,
                   1.0f / (static_cast<float>(T) * static_cast<float>(cfg.m)), stream);
-    lin_wgrad(*this, dlogits, sl.lnf, g_head_w, nullptr, V, H, T, beta);  // head W eagerly (C8 reading)
-    lin_dgrad(*this, dlogits, head_w, d_ln, T, H, V, EPI_F32_STORE, nullptr);
+    if (head_w_eager) lin_wgrad(*this, dl, sl.lnf, g_head_w, nullptr, V, H, T, beta);  // C8 eager option
+    lin_dgrad(*this, dl, head_w, d_ln, T, H, V, EPI_F32_STORE, nullptr);
     ln_bwd(*this, d_ln, sl.xl, sl.muf, sl.rsf, lnf_g, nullptr, g32_dx, sl.dy, g_lnf_g, g_lnf_b, beta);
     dx2_32 = g32_dx;
   } else {
@@ -360,6 +365,9 @@ void Ctx::backward_weight_group(const int* mbs, const int* slot_idx, int k) {
     }
     gemm(g, dt, stream);
   };
+  if (last && !head_w_eager)  // the LM head's W: dW_head += dlogits^T LN_f
+    wgrad([&](Slot& q) -> const void* { return q.dlogits; }, [&](Slot& q) -> const void* { return q.lnf; },
+          g_head_w, nullptr, V, H);
   for (int l = Ls - 1; l >= 0; --l) {
     const LayerW& w = lw[l];
     const bool top = l == Ls - 1;

@@ -40,6 +40,7 @@ struct LayerAct {
 
 struct Slot {
   std::vector<LayerAct> L;
+  void* dlogits;  // last stage, head W in the W pass: bf16 / f32 [T, V] from B to W (else null)
   void* dy;       // gradient of the stage output, activation dtype (GEMM operand in B and W)
   float* dy32;    // the same gradient in f32 as received from stage+1 (residual chain, R-grad32)
   void* xl;
@@ -60,6 +61,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int T = 0, h = 0, a = 0, d = 0, Ls = 0, V = 0, s = 0, b = 0;
   bool first = false, last = false;
+  bool head_w_eager = false;  // ZB_CFG_HEAD_W_EAGER: dW_head inside B (no dlogits stash)
 
   // parameters (flat)
   int64_t n_total = 0, n_wd = 0, n_shadow = 0;

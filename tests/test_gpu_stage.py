@@ -276,3 +276,33 @@ def test_chunked_schedules_vs_oracle_and_bitwise(dtype):
         assert loss == base_loss, fam
         for k in base:
             assert np.array_equal(grads[k], base[k]), (fam, k)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_head_weight_gradient_in_w_equals_eager(dtype):
+    """DESIGN R-head: the LM head's dW runs in the last stage's W pass (dlogits kept in the
+    slot) by default; ZB_CFG_HEAD_W_EAGER runs it inside B.  Same per-microbatch order ->
+    bitwise identical gradients; the deferred mode's last-stage slot holds 2 T V more bytes."""
+    import torch
+    from paper_2401_10241_b200 import api
+    cfg = SHAPES["d96"].with_(m=3)
+    p = 2
+    passes, sim = api.schedule("zbh1", p, cfg.m, 10, 11, 6)
+    tok, lab = inputs(cfg)
+    tin, tl = torch.from_numpy(tok).cuda(), torch.from_numpy(lab).cuda()
+    out = []
+    for eager in (False, True):
+        ctxs = []
+        for s in range(p):
+            c = api.Context(cfg, p, s, cfg.m, max(1, sim.n_slots[s]), dtype=dtype, head_w_eager=eager)
+            prm = zb_synth.make_stage_params(cfg, p, s)
+            c.set_params([prm[n] for n, _, _ in zb_synth.param_specs(cfg, p, s)])
+            ctxs.append(c)
+        api.run_local(ctxs, passes, tin, tl)
+        out.append((ctxs[-1].loss(), [c.get_grads() for c in ctxs], [api.slot_bytes(c.mc) for c in ctxs]))
+    (l0, g0, b0), (l1, g1, b1) = out
+    assert l0 == l1
+    for a, b in zip(g0, g1):
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    esz = 2 if dtype == "bf16" else 4
+    assert b0[0] == b1[0] and b0[-1] - b1[-1] >= cfg.T * cfg.V * esz
