@@ -505,7 +505,7 @@ def profile_p8(cfg, stream, reps=4):
     for f in (1, 2):
         _, sim = api.schedule_per_stage("auto", p, cfg.m, TF, TB, TW, tcomm_us, M_limit=f * p * mb, M_B=mb, M_W=mb)
         res[f"auto_{f}pMB"] = round(sim.bubble_rate, 4)
-    # ZB-V: two chunks of half a middle stage per worker (P:404), per-chunk times
+    # ZB-V: two chunks of half a middle stage per worker (P:318), per-chunk times
     half = {k: per_stage[1][k] // 2 for k in "FBW"}
     _, sim = api.schedule_chunked("zbv", p, cfg.m, 2, half["F"], half["B"], half["W"], tcomm_us)
     res["zbv"] = round(sim.bubble_rate, 4)

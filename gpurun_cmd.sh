@@ -1,2 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_wgroup.py -q -x --timeout 600 -p no:cacheprovider 2>&1 | tail -15
-timeout 600 python scripts/gemm_wgroup_perf.py 2>&1 | tail -10
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > gpurun_out/smi.txt 2>&1
+timeout 2400 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > gpurun_out/gputests.log 2>&1; echo "tests rc $?" >> gpurun_out/gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?" >> gpurun_out/smoke.log
+timeout 1200 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/bench.log
+tail -3 gpurun_out/gputests.log; tail -2 gpurun_out/smoke.log; tail -c 3000 gpurun_out/bench.log

@@ -115,10 +115,10 @@ zb_status_t zb_simulate(int32_t p, int32_t m, zb_pass_t* passes, int32_t n, cons
 
 /* Schedules whose workers hold several model chunks ("virtual stages"
  * v in [0, chunks * p)), each chunk a contiguous block of layers:
- *   ZB_V      (chunks must be 2; PAPER.md §6, P:400-415): V placement — v < p
- *             on worker v, v >= p on worker 2p-1-v (P:404); the three-phase
- *             construction of P:410-411 and the W right-shift within M_limit
- *             (P:413), DESIGN.md R-zbv.  sim->chosen: 0 construction, 1 / 2
+ *   ZB_V      (chunks must be 2; PAPER.md §6, P:318-324): V placement — v < p
+ *             on worker v, v >= p on worker 2p-1-v (P:318); the three-phase
+ *             construction of P:322 and the W right-shift within M_limit
+ *             (P:324), DESIGN.md R-zbv.  sim->chosen: 0 construction, 1 / 2
  *             W right-shift rule "gap" / "fill", whichever simulates fastest.
  *   ZB_1F1B_I (interleaved 1F1B, the Table 4 baseline): v on worker
  *             v mod p, Megatron-LM order (R-1f1bi), fused backward
@@ -271,7 +271,7 @@ zb_status_t zb_run_iteration_local(zb_ctx_t* const* ctxs, int32_t p, const zb_pa
                                    const int32_t* tokens, const int32_t* labels, int32_t flags);
 
 /* One iteration of a WORKER that holds k model chunks of a chunked schedule
- * (zb_schedule_chunked: ZB-V, 1F1B-I; PAPER.md §6 P:400-415).  chunks[k]: the
+ * (zb_schedule_chunked: ZB-V, 1F1B-I; PAPER.md §6 P:318-324).  chunks[k]: the
  * worker's chunk contexts, each created as virtual stage v of nv = chunks*p
  * (cfg.stage = v, cfg.p = nv) and attached to a transport (zb_ctx_attach_loopback
  * with rank v); passes: the full zb_schedule_chunked output (grouped by worker).

@@ -1,11 +1,11 @@
 """Oracle schedules with several model chunks per worker — ZB-V (PAPER.md
-section 6, P:400-415) and interleaved 1F1B (1F1B-I, P:193) — test
+section 6, P:318-324) and interleaved 1F1B (1F1B-I, P:193) — test
 infrastructure only.
 
 ZB-V splits the model into 2p chunks ("virtual stages" v in [0, 2p)) and
 places them in a V: worker w holds v = w (its first chunk, c = 0) and
 v = 2p-1-w (its second chunk, c = 1), "layers 1-2 and layers 15-16 on worker
-1" for 16 layers and 4 stages (P:404).  The forward of a microbatch runs
+1" for 16 layers and 4 stages (P:318).  The forward of a microbatch runs
 v = 0 .. 2p-1 (down the workers, then back up); its backward runs
 v = 2p-1 .. 0.  A pass is (kind, v, j); a schedule is one list per worker in
 execution order.  Times and memory are PER CHUNK here: one chunk pass takes
@@ -13,15 +13,15 @@ T_F / T_B / T_W, retains M_B / M_W (a chunk holds half a stage's layers, so
 these are half the stage figures of section 2).
 
 Followed passages
-  * Placement and dependencies: P:404-406 ("sequentially allocating model
+  * Placement and dependencies: P:318-320 ("sequentially allocating model
     chunks to workers ... then reversing the order"; "both the forward pass
     and backward pass for each microbatch originate from the same worker").
-  * Three phases (P:410-411): warm-up of 2p-i Fs of the first chunk and i-1
+  * Three phases (P:322): warm-up of 2p-i Fs of the first chunk and i-1
     of the second on worker i (1-indexed); steady 1F-1B-1W groups, "p-i
     groups for the second chunk" first, then alternating one group of the
     second and one of the first chunk until the worker's Fs are issued;
     drain with "B being prioritized and W filling the bubbles".
-  * W right-shift within the memory limit (P:413): "we can straightforwardly
+  * W right-shift within the memory limit (P:324): "we can straightforwardly
     shift all W to the right, within the memory constraint ... to fill the
     bubbles in the schedule's tail".
 Readings (DESIGN.md R-zbv; Fig. 6 itself is missing from PAPER.md):
@@ -51,7 +51,7 @@ INF = float("inf")
 
 
 def worker_of(p: int, v: int) -> int:
-    """V placement (P:404): v < p on worker v, else on worker 2p-1-v."""
+    """V placement (P:318): v < p on worker v, else on worker 2p-1-v."""
     return v if v < p else 2 * p - 1 - v
 
 
@@ -61,7 +61,7 @@ def chunk_v(p: int, w: int, c: int) -> int:
 
 
 # --------------------------------------------------------------------------
-# construction (P:410-411 under unit times)
+# construction (P:322 under unit times)
 # --------------------------------------------------------------------------
 
 def build_zbv(p: int, m: int) -> VLists:
@@ -300,7 +300,7 @@ def validate_v(lists: VLists, p: int, m: int) -> List[str]:
 
 
 # --------------------------------------------------------------------------
-# W right-shift within the memory limit (P:413)
+# W right-shift within the memory limit (P:324)
 # --------------------------------------------------------------------------
 
 def shift_w(lists: VLists, p: int, TF: int, TB: int, TW: int, Tcomm: int, MB: int, MW: int, Mlimit: int,

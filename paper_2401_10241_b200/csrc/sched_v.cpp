@@ -1,7 +1,7 @@
 // Host schedules with several model chunks ("virtual stages") per worker:
-// ZB-V (PAPER.md §6, P:400-415) and interleaved 1F1B (1F1B-I, P:193), plus
+// ZB-V (PAPER.md §6, P:318-324) and interleaved 1F1B (1F1B-I, P:193), plus
 // the virtual-stage simulator (App. F (4)-(6) with a placement), per-worker
-// Delta-M memory and the ZB-V W right-shift under M_limit (P:413).
+// Delta-M memory and the ZB-V W right-shift under M_limit (P:324).
 // Readings: DESIGN.md R-zbv / R-1f1bi (identical to oracle/zbv.py, which the
 // tests compare pass for pass).
 #include <algorithm>
@@ -28,7 +28,7 @@ struct EndTable {
 };
 }  // namespace
 
-// ---------------------------------------------------------------- ZB-V construction (P:410-411, unit times)
+// ---------------------------------------------------------------- ZB-V construction (P:322, unit times)
 VLists build_zbv(int p, int m) {
   if (p < 1 || m < 1) throw std::invalid_argument("p, m >= 1");
   const int V = 2 * p;
@@ -264,7 +264,7 @@ std::vector<std::vector<int>> assign_slots_v(const VLists& lists, int nv, std::v
   return slots;
 }
 
-// ---------------------------------------------------------------- ZB-V W right-shift (P:413)
+// ---------------------------------------------------------------- ZB-V W right-shift (P:324)
 VLists zbv_shift_w(const VLists& lists, int p, int64_t TF, int64_t TB, int64_t TW, int64_t Tc, int64_t MB, int64_t MW,
                    int64_t Mlimit, bool fill) {
   const int nv = 2 * p;

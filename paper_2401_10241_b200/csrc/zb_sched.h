@@ -34,7 +34,7 @@ SimResult simulate(const Lists& lists, const std::vector<int64_t>& TF, const std
 std::vector<int64_t> memory_peaks(const Lists& lists, int64_t MB, int64_t MW);
 std::vector<std::vector<int>> assign_slots(const Lists& lists, std::vector<int>* counts);
 
-// ---- several model chunks per worker (sched_v.cpp): ZB-V (P:400-415), 1F1B-I (P:193)
+// ---- several model chunks per worker (sched_v.cpp): ZB-V (P:318-324), 1F1B-I (P:193)
 struct VPass {
   int kind;
   int v;  // virtual stage (model chunk) in [0, chunks * p)

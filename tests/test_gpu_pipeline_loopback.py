@@ -191,7 +191,7 @@ def _chunk_contexts(cfg, p, family, dtype, own_streams):
 
 @pytest.mark.parametrize("family", ["zbv", "1f1bi"])
 def test_loopback_chunked_workers_equal_virtual_stages(family):
-    """p = 4 workers x 2 chunks (P:404 V placement / cyclic 1F1B-I), each worker
+    """p = 4 workers x 2 chunks (P:318 V placement / cyclic 1F1B-I), each worker
     one host thread running zb_run_iteration_worker in its own pass order over
     the loopback transport; two iterations with the post-validated step between
     (steps in ascending v, finishes in descending v per worker).  Reference: the

@@ -264,7 +264,7 @@ def gpu_run_chunked(cfg, p, chunks, family, dtype):
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_chunked_schedules_vs_oracle_and_bitwise(dtype):
-    """ZB-V (P:400-415) and 1F1B-I (P:193) on BASELINE configs[0] (8 layers,
+    """ZB-V (P:318-324) and 1F1B-I (P:193) on BASELINE configs[0] (8 layers,
     p = 4 workers x 2 chunks of one layer): within tolerance of the oracle and
     bitwise equal to 1F1B over the same 8 chunks."""
     cfg = zb_synth.CONFIGS["tiny"]

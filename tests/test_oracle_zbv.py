@@ -1,8 +1,8 @@
-"""Pins for oracle/zbv.py (ZB-V, PAPER.md section 6, P:400-415).
+"""Pins for oracle/zbv.py (ZB-V, PAPER.md section 6, P:318-324).
 
-* P:410: worker i's warm-up is 2p-1 Fs, 2p-i of the first chunk and i-1 of
+* P:322: worker i's warm-up is 2p-1 Fs, 2p-i of the first chunk and i-1 of
   the second; then p-i F-B-W groups of the second chunk.
-* P:409: "Under the condition T_F=T_B=T_W, ZB-V achieves zero bubble with a
+* P:320: "Under the condition T_F=T_B=T_W, ZB-V achieves zero bubble with a
   peak activations memory of pM_B" and the peak is "inherently balanced
   across all workers" — exact, for every p <= 8 and m >= 2p-1.
 * simulate_v with one virtual stage per worker == the Table-2/Table-4-pinned
@@ -12,7 +12,7 @@
   whose p and m Table 8 also profiles) ZB-V lies within 0.01 of the printed
   rate and below ZB-H2, ZB-H1, 1F1B (P:433's claims); the exact profile of
   the ZB-V runs is not printed, hence the tolerance.
-* W right-shift (P:413): never increases the simulated cost (SPEC S:238) and
+* W right-shift (P:324): never increases the simulated cost (SPEC S:238) and
   never exceeds M_limit; unit times leave the construction unchanged.
 """
 import random

@@ -1,4 +1,4 @@
-"""Worker plans of chunked schedules (ZB-V P:400-415, 1F1B-I P:193): the op list
+"""Worker plans of chunked schedules (ZB-V P:318-324, 1F1B-I P:193): the op list
 comm.cu's worker runner executes (plan.h worker_plan — every chunk's
 per-virtual-stage plan merged in the worker's pass order), checked on CPU:
 
