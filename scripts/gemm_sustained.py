@@ -7,7 +7,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2401_10241_b200 import api
 
-ap = argparse.ArgumentParser(); ap.add_argument("--secs", type=float, default=2.0); a = ap.parse_args()
+ap = argparse.ArgumentParser(); ap.add_argument("--secs", type=float, default=2.0)
+ap.add_argument("--model", default="1.5B", choices=["1.5B", "6.2B"]); a = ap.parse_args()
 
 def timed_loop(fn, secs):
     fn(); torch.cuda.synchronize()
@@ -38,7 +39,7 @@ def case(name, M, N, K, a_mn, b_mn, epi):
     print(json.dumps({"shape": name, "MNK": [M, N, K], "epi": epi, "ours_tflops": round(o, 1),
                       "cublas_tflops": round(c, 1), "ratio": round(o / c, 3)}), flush=True)
 
-T, h, V = 6144, 2304, 50304
+T, h, V = (6144, 2304, 50304) if a.model == "1.5B" else (3072, 4096, 50304)
 for sh in [("F qkv", T, 3 * h, h, False, False, 0), ("F proj+resid", T, h, h, False, False, 2),
            ("F fc1+gelu", T, 4 * h, h, False, False, 1), ("F fc2+resid", T, h, 4 * h, False, False, 2),
            ("B fc2 (gelu bwd)", T, 4 * h, h, False, True, 3), ("B fc1 (f32 out)", T, h, 4 * h, False, True, 5),

@@ -7,7 +7,9 @@ microbatch), next to the algorithmic (compulsory) bytes of the same shapes."""
 import csv, collections, json, re, sys
 
 src, out = sys.argv[1], sys.argv[2]
-L, h, T, V = 22, 2304, 6144, 50304   # 1.5B step of bench.py (c2, b = 6, s = 1024)
+model = sys.argv[3] if len(sys.argv) > 3 else "1.5B"
+# bench.py steps: c2 (1.5B, b = 6) and c3 (6.2B, b = 3), s = 1024
+L, h, T, V = {"1.5B": (22, 2304, 6144, 50304), "6.2B": (30, 4096, 3072, 50304)}[model]
 rows = list(csv.reader(open(src)))
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[hi]
@@ -35,10 +37,17 @@ w = [T * 3 * h * e + T * h * e + 3 * h * h * 8, T * h * e * 2 + h * h * 8, T * 4
 alg_layer = (sum(f) + sum(bw) + sum(w)) / 12
 alg_head = (T * h * e + V * h * e + T * V * 4 + T * V * e + V * h * e + T * h * 4 + T * V * e + T * h * e + V * h * 8) / 3
 alg = (n_layer * alg_layer + n_head * alg_head) / (n_layer + n_head)
-json.dump({"dram_bytes_per_launch": round(mean), "algorithmic_bytes_per_launch": round(alg),
-           "ratio": round(mean / alg, 3), "launches_captured": len(launches),
-           "layer_gemm_mean_bytes": round(sum(layer) / len(layer)), "head_gemm_mean_bytes": round(sum(head) / len(head)),
-           "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, one 1.5B microbatch (2 layers + head), "
-                     "weighted to the bench step (22 layers x 12 + 3 head GEMMs); " + src.split("/")[-1]},
-          open(out, "w"), indent=1)
+rec = {"model": model, "dram_bytes_per_launch": round(mean), "algorithmic_bytes_per_launch": round(alg),
+       "ratio": round(mean / alg, 3), "launches_captured": len(launches),
+       "layer_gemm_mean_bytes": round(sum(layer) / len(layer)), "head_gemm_mean_bytes": round(sum(head) / len(head)),
+       "source": f"ncu dram__bytes_read.sum + dram__bytes_write.sum, one {model} microbatch (2 layers + head), "
+                 f"weighted to the bench step ({L} layers x 12 + 3 head GEMMs); " + src.split("/")[-1]}
+try:   # one record per model (bench.py gemm_traffic looks its model up)
+    allrec = json.load(open(out))
+    if "dram_bytes_per_launch" in allrec:
+        allrec = {allrec.get("model", "1.5B"): allrec}
+except (OSError, ValueError):
+    allrec = {}
+allrec[model] = rec
+json.dump(allrec, open(out, "w"), indent=1)
 print(open(out).read())
