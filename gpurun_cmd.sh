@@ -1,13 +1,15 @@
 mkdir -p gpurun_out
 export PATH=/usr/local/cuda/bin:$PATH
-# 1. launch list of one 6.2B microbatch (4 layers + head + optimizer)
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/r02_launches_6p2b_4layer_m1.csv python scripts/profile_step.py --config 6.2B --layers 4 --m 1 > gpurun_out/launch.log 2>&1
-# 2. GEMM DRAM bytes (2 layers + head)
-timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --profile-from-start off -k regex:k_gemm --csv --log-file gpurun_out/r02_gemm_dram_6p2b_2layer_m1.csv python scripts/profile_step.py --config 6.2B --layers 2 --m 1 > gpurun_out/dram.log 2>&1
-# 3. sustained GEMM vs cuBLAS at the 6.2B shapes
-timeout 600 python scripts/gemm_sustained.py --model 6.2B --secs 1.5 > gpurun_out/r02_gemm_sustained_6p2b.jsonl 2>&1
-# 4. attention perf at both shapes
-timeout 300 python scripts/attn_perf.py > gpurun_out/r02_attn_perf.jsonl 2>&1
-# 5. full ncu of the attention kernels at the 6.2B shape
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fwd_tc\|k_bwd_tc -c 2 -o gpurun_out/r02_attn_6p2b python scripts/attn_one.py 3 1024 32 128 > gpurun_out/ncu_attn.log 2>&1
-tail -3 gpurun_out/*.log; cat gpurun_out/r02_gemm_sustained_6p2b.jsonl gpurun_out/r02_attn_perf.jsonl
+timeout 1200 python -m pytest tests/test_gpu_dp_shim.py tests/test_gpu_nccl_shim.py -q -x --timeout 900 -p no:cacheprovider > gpurun_out/dp.log 2>&1; echo "rc $?" >> gpurun_out/dp.log
+S=gpurun_out/r02_sanitizer.txt
+echo "# compute-sanitizer, round 2 (B200)" > $S
+run() { echo "## $1 $2" >> $S; timeout 900 compute-sanitizer --tool $1 --print-limit 20 python -m pytest $2 -q -x -p no:cacheprovider --timeout 800 2>&1 | grep -v "^$" | tail -8 >> $S; }
+run racecheck "tests/test_gpu_attention.py -k bf16-b2s256a3d64"
+run racecheck "tests/test_gpu_attention.py -k bf16-b1s256a2d128"
+run racecheck "tests/test_gpu_gemm.py -k bf16-1024x192"
+run racecheck "tests/test_gpu_gemm.py -k bf16-512x512x4096"
+run memcheck "tests/test_gpu_ops.py"
+run memcheck "tests/test_gpu_pipeline_loopback.py -k clean"
+run synccheck "tests/test_gpu_gemm.py -k bf16"
+run memcheck "tests/test_gpu_wgroup.py"
+tail -5 gpurun_out/dp.log; cat $S

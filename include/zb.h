@@ -237,7 +237,7 @@ enum { ZB_RUN_HOST_INPUTS = 1, /* tokens / labels are host pointers: H2D inside 
        ZB_RUN_TIMING = 2,      /* record CUDA events at every pass boundary               */
        ZB_RUN_FUSED_BW = 4,    /* 1F1B: send the input gradient after the W that follows  */
                                /* its B (the monolithic backward of the baseline, C5)     */
-       ZB_RUN_GROUP_W = 8      /* W-grouping ("W ... anywhere after    */
+       ZB_RUN_GROUP_W = 8,     /* W-grouping ("W ... anywhere after    */
                                /* the corresponding B"): up to 4 W passes that are ADJACENT */
                                /* in a stage's list run as one contraction per linear with */
                                /* K = k*T (one f32 gradient read-modify-write for k         */
@@ -245,7 +245,15 @@ enum { ZB_RUN_HOST_INPUTS = 1, /* tokens / labels are host pointers: H2D inside 
                                /* results are bitwise equal between runs / runtimes with    */
                                /* the same adjacency, within tolerance otherwise.  Not for  */
                                /* zb_run_iteration_worker.  A timed group records one event */
-                               /* pair; zb_ctx_profile counts it as k W passes of 1/k each. */ };
+                               /* pair; zb_ctx_profile counts it as k W passes of 1/k each. */
+       ZB_RUN_DP_REORDER = 16  /* data parallelism (zb_ctx_attach_dp), App. A       */
+                               /* the W passes at the tail of the stage's list   */
+                               /* are reordered to cluster the computations of each         */
+                               /* parameter, whose gradient all-reduce then starts while    */
+                               /* the next parameter's computations run.  Without it the    */
+                               /* tail keeps its W-major order (all-reduces start only      */
+                               /* inside the last W).  Sub-computations of the tail are not */
+                               /* timed (ZB_RUN_TIMING).                                    */ };
 
 typedef struct {
   int32_t n_passes;
@@ -373,6 +381,22 @@ zb_status_t zb_ctx_comm_probe(zb_ctx_t* ctx, size_t bytes, int32_t iters, int64_
  * worker with zb_run_iteration_worker.  ZB_ENCCL if libnccl is unavailable. */
 zb_status_t zb_ctx_attach_nccl_chunks(zb_ctx_t* const* chunks, int32_t k, const void* ids, int32_t nv,
                                       const int32_t* worker_of, int32_t worker);
+
+/* Data parallelism (App. A): D replicas of the
+ * pipeline, each fed its own microbatches; stage s of replica r is one process
+ * (GPU).  Attach the replicas of one stage to a D-rank NCCL communicator (id128:
+ * one ncclUniqueId per stage, identical on its D ranks; dp_rank in [0, D)).  For
+ * p > 1 attach the P2P transport (zb_ctx_attach_nccl) FIRST.  zb_run_iteration then
+ * sums the stage's gradients over the replicas with in-place f32 all-reduces, one
+ * per W unit (the LM head; per layer fc2, fc1, proj, qkv; the embedding — each
+ * issued on a side stream right after the computation that completes it) plus one
+ * for the vector region (LayerNorm gammas / betas, biases), before the iteration
+ * returns to the post-validation step; ZB_RUN_DP_REORDER reorders the tail Ws per
+ * parameter (App. A).  The cross-entropy mean runs over all T m D tokens, so
+ * zb_ctx_read_loss returns this replica's share of the global loss.  dp_world = 1
+ * is allowed (no communicator; the plan runner with the reordered tail).
+ * ZB_ENCCL if libnccl is missing or lacks ncclAllReduce. */
+zb_status_t zb_ctx_attach_dp(zb_ctx_t* ctx, const void* id128, int32_t dp_rank, int32_t dp_world);
 
 /* In-process loopback group (test transport for one GPU): world stage
  * contexts of ONE process attach to the same group and are then driven

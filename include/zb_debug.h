@@ -80,6 +80,16 @@ zb_status_t zb_dbg_kernel_timing_read(int32_t cls, double* total_ms, double* tot
 zb_status_t zb_dbg_stage_plan(const zb_pass_t* passes, int32_t n, int32_t p, int32_t m, int32_t stage,
                               int32_t pv_pending, int32_t amend, int32_t fused, int32_t* out_ops, int32_t cap,
                               int32_t* n_out);
+/* The same plan with the data-parallel tail (plan.h dp_tail, SURVEY §8(f)4 /
+ * App. A): the trailing W ops become types 10 WP {microbatch, unit (message
+ * index field), slot} and 11 ALLREDUCE {-1, unit or -1 for the vector region,
+ * -1}; n_units W units per pass (zb_dbg_w_units), reorder != 0 clusters them
+ * per unit (ZB_RUN_DP_REORDER). */
+zb_status_t zb_dbg_dp_plan(const zb_pass_t* passes, int32_t n, int32_t p, int32_t m, int32_t stage,
+                           int32_t pv_pending, int32_t amend, int32_t fused, int32_t n_units, int32_t reorder,
+                           int32_t* out_ops, int32_t cap, int32_t* n_out);
+/* W units of a context's W pass and the all-reduce calls its DP communicator issued. */
+zb_status_t zb_dbg_w_units(zb_ctx_t* ctx, int32_t* n_units, int64_t* dp_reduces);
 /* n'_s, the number of speculative warm-up Fs of each stage (plan.h). */
 /* Merged op list of one worker of a chunked schedule (plan.h worker_plan):
  * 5 ints per op: type, microbatch, message index, slot, chunk (virtual stage).

@@ -20,7 +20,7 @@ FAMILY = {"1f1b": ZB_1F1B, "zbh1": ZB_H1, "zbh2": ZB_H2, "auto": ZB_AUTO}
 ZB_V, ZB_1F1B_I = 4, 5
 CHUNKED_FAMILY = {"zbv": ZB_V, "1f1bi": ZB_1F1B_I}
 ZB_DTYPE_BF16, ZB_DTYPE_F32 = 0, 1
-ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_RUN_FUSED_BW, ZB_RUN_GROUP_W = 1, 2, 4, 8
+ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_RUN_FUSED_BW, ZB_RUN_GROUP_W, ZB_RUN_DP_REORDER = 1, 2, 4, 8, 16
 ZB_OPT_SYNC, ZB_OPT_PV = 0, 1
 ZB_CFG_HEAD_W_EAGER = 1
 ZB_MAX_STAGES = 64
@@ -100,6 +100,10 @@ _SIGS = {
     "zb_dbg_attention_bwd": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
     "zb_dbg_stage_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, _I32, _I32, _I32, C.POINTER(_I32), _I32,
                            C.POINTER(_I32)], _I32),
+    "zb_dbg_dp_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                        C.POINTER(_I32), _I32, C.POINTER(_I32)], _I32),
+    "zb_dbg_w_units": ([_P, C.POINTER(_I32), C.POINTER(_I64)], _I32),
+    "zb_ctx_attach_dp": ([_P, _P, _I32, _I32], _I32),
     "zb_dbg_worker_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, C.POINTER(_I32), _I32, C.POINTER(_I32),
                             _I32, C.POINTER(_I32)], _I32),
     "zb_ctx_attach_nccl_chunks": ([C.POINTER(_P), _I32, _P, _I32, C.POINTER(_I32), _I32], _I32),

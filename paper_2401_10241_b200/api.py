@@ -11,7 +11,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from ._lib import (CHUNKED_FAMILY, FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_FUSED_BW,
-                   ZB_RUN_GROUP_W, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_CFG_HEAD_W_EAGER,
+                   ZB_RUN_DP_REORDER, ZB_RUN_GROUP_W, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_CFG_HEAD_W_EAGER,
                    ACTIONS, check, lib, zb_iter_stats_t, zb_model_cfg_t, zb_optim_cfg_t, zb_pass_t, zb_pv_report_t,
                    zb_sim_t)
 
@@ -231,6 +231,18 @@ class Context:
         buf = C.create_string_buffer(ids, len(ids))
         check(lib.zb_ctx_attach_nccl(self.h, buf, rank, world))
 
+    def attach_dp(self, id128: bytes, dp_rank: int, dp_world: int):
+        """zb_ctx_attach_dp: the D-rank gradient all-reduce communicator of this stage's
+        replicas (after attach_nccl when p > 1)."""
+        buf = C.create_string_buffer(id128, 128) if id128 else None
+        check(lib.zb_ctx_attach_dp(self.h, buf, dp_rank, dp_world))
+
+    def w_units(self):
+        """(W units of this stage's W pass, data-parallel all-reduces issued so far)."""
+        n, r = C.c_int32(), C.c_int64()
+        check(lib.zb_dbg_w_units(self.h, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
     def comm_probe(self, nbytes: int, iters: int = 10) -> int:
         """zb_ctx_comm_probe: median round trip (ns) of one message to stage+1 and back
         (collective over the pipeline; 0 on the last stage)."""
@@ -244,9 +256,10 @@ class Context:
         self._group = group
 
     def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False, fused=False,
-                      group_w=False):
+                      group_w=False, dp_reorder=False):
         flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0) | \
-            (ZB_RUN_FUSED_BW if fused else 0) | (ZB_RUN_GROUP_W if group_w else 0)
+            (ZB_RUN_FUSED_BW if fused else 0) | (ZB_RUN_GROUP_W if group_w else 0) | \
+            (ZB_RUN_DP_REORDER if dp_reorder else 0)
         tp = tokens.ctypes.data if host_inputs and tokens is not None else _ptr(tokens)
         lp = labels.ctypes.data if host_inputs and labels is not None else _ptr(labels)
         check(lib.zb_run_iteration(self.h, passes, len(passes), tp, lp, flags))
@@ -345,6 +358,17 @@ def attach_nccl_chunks(chunks: Sequence[Context], ids: bytes, nv: int, worker_of
     buf = C.create_string_buffer(ids, len(ids))
     wo = (C.c_int32 * nv)(*worker_of)
     check(lib.zb_ctx_attach_nccl_chunks(arr, len(chunks), buf, nv, wo, worker))
+
+
+def dp_plan(passes, p: int, m: int, stage: int, n_units: int, reorder: bool, pending=False, amend=False,
+            fused=False):
+    """zb_dbg_dp_plan -> [(type, microbatch, msg, slot)] (10 WP: msg = W unit; 11 ALLREDUCE)."""
+    cap = 8 * len(passes) * (n_units + 1) + 64
+    buf = (C.c_int32 * (4 * cap))()
+    n = C.c_int32()
+    check(lib.zb_dbg_dp_plan(passes, len(passes), p, m, stage, int(pending), int(amend), int(fused), n_units,
+                             int(reorder), buf, cap, C.byref(n)))
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(n.value)]
 
 
 def worker_plan(passes, nv: int, m: int, worker: int, worker_of: Sequence[int], fused: bool = False):

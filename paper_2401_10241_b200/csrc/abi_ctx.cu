@@ -20,6 +20,7 @@ Ctx* C_(zb_ctx_t* p) {
 void begin_iteration(Ctx& c) {
   c.first_b_done = false;
   c.first_w_done = false;
+  c.unit_w_done.assign(c.n_w_units(), 0);
   ZB_CUDA(cudaMemsetAsync(c.loss_acc, 0, sizeof(double), c.stream));
 }
 
@@ -721,6 +722,28 @@ extern "C" zb_status_t zb_ctx_attach_nccl(zb_ctx_t* ctx, const void* ids, int32_
     if (!ids || world < 1 || rank < 0 || rank >= world) return set_error(ZB_EINVAL, "bad NCCL arguments");
     if (world != c->cfg.p || rank != c->cfg.stage) return set_error(ZB_EINVAL, "rank / world must be stage / p");
     attach_nccl(*c, ids, rank, world);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_ctx_attach_dp(zb_ctx_t* ctx, const void* id128, int32_t dp_rank, int32_t dp_world) {
+  ZB_TRY {
+    Ctx* c = C_(ctx);
+    if ((!id128 && dp_world > 1) || dp_world < 1 || dp_rank < 0 || dp_rank >= dp_world)
+      return set_error(ZB_EINVAL, "bad data-parallel arguments");
+    if (c->dp) return set_error(ZB_ESTATE, "data parallelism already attached");
+    attach_dp(*c, id128, dp_rank, dp_world);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+extern "C" zb_status_t zb_dbg_w_units(zb_ctx_t* ctx, int32_t* n_units, int64_t* dp_reduces) {
+  ZB_TRY {
+    Ctx* c = C_(ctx);
+    if (n_units) *n_units = c->n_w_units();
+    if (dp_reduces) *dp_reduces = dp_reduce_count(*c);
     return ZB_OK;
   }
   ZB_CATCH

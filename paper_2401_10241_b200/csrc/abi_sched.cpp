@@ -269,6 +269,27 @@ extern "C" zb_status_t zb_dbg_stage_plan(const zb_pass_t* passes, int32_t n, int
   ZB_CATCH
 }
 
+extern "C" zb_status_t zb_dbg_dp_plan(const zb_pass_t* passes, int32_t n, int32_t p, int32_t m, int32_t stage,
+                                      int32_t pv_pending, int32_t amend, int32_t fused, int32_t n_units,
+                                      int32_t reorder, int32_t* out_ops, int32_t cap, int32_t* n_out) {
+  ZB_TRY {
+    if (!passes || p < 1 || m < 1 || stage < 0 || stage >= p || n_units < 1 || !out_ops || !n_out)
+      return set_error(ZB_EINVAL, "zb_dbg_dp_plan: bad arguments");
+    auto ops = plan::dp_tail(plan::stage_plan(passes, n, p, m, stage, pv_pending != 0, amend != 0, fused != 0),
+                             n_units, reorder != 0);
+    *n_out = static_cast<int32_t>(ops.size());
+    if (static_cast<int32_t>(ops.size()) > cap) return set_error(ZB_ECAP, "plan longer than cap");
+    for (size_t i = 0; i < ops.size(); ++i) {
+      out_ops[4 * i] = ops[i].type;
+      out_ops[4 * i + 1] = ops[i].mb;
+      out_ops[4 * i + 2] = ops[i].msg;
+      out_ops[4 * i + 3] = ops[i].slot;
+    }
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
 extern "C" zb_status_t zb_dbg_speculative_counts(const zb_pass_t* passes, int32_t n, int32_t p, int32_t* out) {
   ZB_TRY {
     if (!passes || p < 1 || !out) return set_error(ZB_EINVAL, "bad arguments");

@@ -49,8 +49,9 @@ typedef int (*PInit)(void**, int, ncclUniqueId_t, int);
 typedef int (*PSendRecv)(const void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*PRecv)(void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*PDestroy)(void*);
+typedef int (*PAllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 typedef const char* (*PErr)(int);
-constexpr int kNcclUint8 = 1;
+constexpr int kNcclUint8 = 1, kNcclFloat32 = 7, kNcclSum = 0;
 
 struct Nccl {
   void* h = nullptr;
@@ -60,13 +61,14 @@ struct Nccl {
   PRecv recv = nullptr;
   PDestroy destroy = nullptr;
   PErr err = nullptr;
+  PAllReduce all_reduce = nullptr;  // data parallelism only (checked by attach_dp)
 };
 
 Nccl& nccl() {
   static Nccl n;
   if (n.h) return n;
   // ZB_NCCL_LIB: an explicit library path (tests: the 2-process / 1-GPU shim,
-  // tests/shim/nccl_ipc.cpp); otherwise the already-loaded / system libnccl.so.2.
+  // tests/shim/nccl_ipc.cu); otherwise the already-loaded / system libnccl.so.2.
   const char* env = std::getenv("ZB_NCCL_LIB");
   if (env && *env) {
     n.h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
@@ -84,6 +86,7 @@ Nccl& nccl() {
   n.recv = reinterpret_cast<PRecv>(dlsym(n.h, "ncclRecv"));
   n.destroy = reinterpret_cast<PDestroy>(dlsym(n.h, "ncclCommDestroy"));
   n.err = reinterpret_cast<PErr>(dlsym(n.h, "ncclGetErrorString"));
+  n.all_reduce = reinterpret_cast<PAllReduce>(dlsym(n.h, "ncclAllReduce"));
   if (!n.get_id || !n.init || !n.send || !n.recv || !n.destroy || !n.err) {
     n.h = nullptr;
     throw Error(ZB_ENCCL, "libnccl.so.2 lacks ncclSend / ncclRecv");
@@ -271,6 +274,80 @@ void attach_nccl(Ctx& c, const void* ids, int rank, int world) {
   setup_comm(c, *cm);
   c.comm = std::move(cm);
 }
+
+// ---------------------------------------------------------------- data parallelism
+// The D replicas of one stage share a D-rank communicator; gradient all-reduces (f32 sum, in
+// place) run on its own stream, ordered after the W unit that completes them by an event, so
+// they overlap the stage's remaining W work (App. A).  The compute stream waits for the last
+// all-reduce at the end of the iteration (before the post-validation norm and the step).
+DpComm::~DpComm() {
+  if (stream) cudaStreamSynchronize(stream);
+  if (comm) nccl().destroy(comm);
+  if (stream) cudaStreamDestroy(stream);
+  for (auto e : ev) cudaEventDestroy(e);
+}
+
+cudaEvent_t DpComm::event() {
+  if (ev.size() < 256) {
+    cudaEvent_t e;
+    ZB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+    return e;
+  }
+  cudaEvent_t e = ev[ev_next];
+  ev_next = (ev_next + 1) % static_cast<int>(ev.size());
+  return e;
+}
+
+void attach_dp(Ctx& c, const void* id128, int dp_rank, int dp_world) {
+  if (dp_world < 1 || dp_rank < 0 || dp_rank >= dp_world) throw Error(ZB_EINVAL, "bad data-parallel rank / world");
+  auto d = std::make_unique<DpComm>();
+  d->rank = dp_rank;
+  d->world = dp_world;
+  if (dp_world > 1) {
+    if (!nccl().all_reduce) throw Error(ZB_ENCCL, "libnccl lacks ncclAllReduce");
+    ncclUniqueId_t u;
+    std::memcpy(&u, id128, 128);
+    nck(nccl().init(&d->comm, dp_world, u, dp_rank), "ncclCommInitRank (data parallel)");
+  }
+  ZB_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  if (!c.comm) {  // p = 1: the plan runner needs a (transport-less) stage communicator
+    if (c.cfg.p != 1) throw Error(ZB_EINVAL, "attach the P2P transport (zb_ctx_attach_nccl) before data parallelism");
+    auto cm = std::make_unique<Comm>();
+    cm->rank = 0;
+    cm->world = 1;
+    setup_comm(c, *cm);
+    c.comm = std::move(cm);
+  }
+  c.dp = std::move(d);
+  c.dp_world = dp_world;
+}
+
+// all-reduce of W unit u's gradient (u = -1: the vector region) after everything enqueued so
+// far on the compute stream
+void dp_all_reduce(Ctx& c, int u) {
+  DpComm& d = *c.dp;
+  int64_t off = 0, cnt = 0;
+  c.unit_grad_range(u, &off, &cnt);
+  cudaEvent_t e = d.event();
+  ZB_CUDA(cudaEventRecord(e, c.stream));
+  ZB_CUDA(cudaStreamWaitEvent(d.stream, e, 0));
+  if (d.world > 1 && cnt > 0)
+    nck(nccl().all_reduce(c.grad + off, c.grad + off, static_cast<size_t>(cnt), kNcclFloat32, kNcclSum, d.comm,
+                          d.stream),
+        "ncclAllReduce");
+  ++d.reduces;
+}
+
+// the compute stream waits for every all-reduce issued so far
+void dp_join(Ctx& c) {
+  DpComm& d = *c.dp;
+  cudaEvent_t e = d.event();
+  ZB_CUDA(cudaEventRecord(e, d.stream));
+  ZB_CUDA(cudaStreamWaitEvent(c.stream, e, 0));
+}
+
+int64_t dp_reduce_count(const Ctx& c) { return c.dp ? c.dp->reduces : 0; }
 
 // ---------------------------------------------------------------- in-process loopback transport
 namespace {
@@ -567,6 +644,7 @@ struct StageExec {
     if (c.first && !tokens) throw Error(ZB_EINVAL, "tokens required on stage 0");
     if (c.last && !labels) throw Error(ZB_EINVAL, "labels required on the last stage");
     c.first_b_done = c.first_w_done = false;
+    c.unit_w_done.assign(c.n_w_units(), 0);
     ZB_CUDA(cudaMemsetAsync(c.loss_acc, 0, sizeof(double), c.stream));
     c.n_timed = 0;
   }
@@ -637,9 +715,24 @@ struct StageExec {
         if (flags & ZB_RUN_TIMING) c.timing_end(c.n_timed++);
         break;
       }
+      case plan::OP_WP: {  // one W unit of one tail microbatch (data parallelism)
+        const int sl1[1] = {op.slot};
+        c.weight_unit(op.msg, sl1, 1);
+        break;
+      }
+      case plan::OP_ALLREDUCE: {
+        dp_all_reduce(c, op.msg);
+        break;
+      }
       default:
         throw Error(ZB_EINVAL, "StageExec: unexpected op");
     }
+  }
+  // k adjacent OP_WP of the same unit as one contraction (ZB_RUN_GROUP_W)
+  void exec_wp_group(const plan::Op* ops, int k) {
+    int sls[kMaxSeg];
+    for (int i = 0; i < k; ++i) sls[i] = ops[i].slot;
+    c.weight_unit(ops[0].msg, sls, k);
   }
   // W-grouping (ZB_RUN_GROUP_W): k adjacent W ops as one contraction per linear
   void exec_w_group(const plan::Op* ops, int k) {
@@ -664,9 +757,21 @@ void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* t
   std::vector<plan::Op> ops = plan::stage_plan(passes, n, p, m, s, pending, false, fused);
   std::vector<plan::Op> ops_amend;
   if (pending) ops_amend = plan::stage_plan(passes, n, p, m, s, true, true, fused);
+  if (c.dp) {  // the tail Ws as per-unit sub-computations + all-reduces (plan.h dp_tail)
+    const bool reorder = (flags & ZB_RUN_DP_REORDER) != 0;
+    ops = plan::dp_tail(ops, c.n_w_units(), reorder);
+    if (pending) ops_amend = plan::dp_tail(ops_amend, c.n_w_units(), reorder);
+  }
   bool switched = false;
   for (size_t k = 0; k < ops.size(); ++k) {
     const plan::Op op = ops[k];
+    if (op.type == plan::OP_WP && (flags & ZB_RUN_GROUP_W)) {
+      int g = 1;
+      while (g < kMaxSeg && k + g < ops.size() && ops[k + g].type == plan::OP_WP && ops[k + g].msg == op.msg) ++g;
+      ex.exec_wp_group(&ops[k], g);
+      k += g - 1;
+      continue;
+    }
     if (op.type == plan::OP_W && (flags & ZB_RUN_GROUP_W)) {
       int g = 1;
       while (g < kMaxSeg && k + g < ops.size() && ops[k + g].type == plan::OP_W) ++g;
@@ -696,6 +801,7 @@ void run_iteration_nccl(Ctx& c, const zb_pass_t* passes, int n, const int32_t* t
       switched = true;
     }
   }
+  if (c.dp) dp_join(c);
 }
 
 void run_iteration_worker(const std::vector<Ctx*>& chunks, const zb_pass_t* passes, int n, const int32_t* tokens,

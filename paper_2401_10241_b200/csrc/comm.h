@@ -65,6 +65,26 @@ struct Comm {
   cudaEvent_t event();
 };
 
+// Data parallelism: the D replicas of one stage share a
+// D-rank communicator; gradient all-reduces (f32 sum, in place) run on its own stream, each
+// ordered after the W unit that completes its gradient (plan.h dp_tail), so they overlap the
+// remaining W work; the compute stream joins them at the end of the iteration (before the
+// post-validation norm and the optimizer step).
+struct DpComm {
+  void* comm = nullptr;  // nullptr when world == 1
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> ev;
+  int ev_next = 0;
+  int64_t reduces = 0;  // all-reduce calls issued
+  ~DpComm();
+  cudaEvent_t event();
+};
+void attach_dp(Ctx& c, const void* id128, int dp_rank, int dp_world);
+void dp_all_reduce(Ctx& c, int unit);  // after everything enqueued so far on the compute stream
+void dp_join(Ctx& c);                  // the compute stream waits for every all-reduce issued
+int64_t dp_reduce_count(const Ctx& c);
+
 // ncclGetUniqueId through dlopen'ed libnccl (128 bytes).
 void nccl_unique_id(void* id128);
 // ids: 2*(world-1) unique ids, [k] for the activation comm of pair (k, k+1),

@@ -80,6 +80,38 @@ std::vector<Op> stage_plan(const zb_pass_t* passes, int n, int p, int m, int sta
   return ops;
 }
 
+std::vector<Op> dp_tail(const std::vector<Op>& ops, int n_units, bool reorder) {
+  if (n_units < 1) throw std::invalid_argument("dp_tail: no W units");
+  // the tail: W ops after the stage's last other compute / receive (1F1B's fused backward
+  // interleaves its gradient sends, each of which follows its microbatch's W)
+  size_t t = ops.size();
+  while (t > 0 && (ops[t - 1].type == OP_W || (ops[t - 1].type == OP_SEND_GRAD && t > 1 &&
+                                                ops[t - 2].type == OP_W && ops[t - 2].mb == ops[t - 1].mb)))
+    --t;
+  std::vector<Op> out(ops.begin(), ops.begin() + static_cast<long>(t));
+  std::vector<Op> tail, sends;
+  for (size_t i = t; i < ops.size(); ++i) (ops[i].type == OP_W ? tail : sends).push_back(ops[i]);
+  std::vector<std::pair<int, int>> order;  // (unit, tail index) in execution order
+  if (reorder)
+    for (int u = 0; u < n_units; ++u)
+      for (size_t i = 0; i < tail.size(); ++i) order.push_back({u, static_cast<int>(i)});
+  else
+    for (size_t i = 0; i < tail.size(); ++i)
+      for (int u = 0; u < n_units; ++u) order.push_back({u, static_cast<int>(i)});
+  std::vector<int> left_u(n_units, static_cast<int>(tail.size())), left_mb(tail.size(), n_units);
+  for (const auto& [u, i] : order) {
+    out.push_back({OP_WP, tail[i].mb, u, tail[i].slot});
+    if (--left_u[u] == 0) out.push_back({OP_ALLREDUCE, -1, u, -1});
+    if (--left_mb[i] == 0)
+      for (const Op& sg : sends)
+        if (sg.mb == tail[i].mb) out.push_back(sg);
+  }
+  if (tail.empty())  // no W after the last B (cannot happen for complete lists)
+    for (int u = 0; u < n_units; ++u) out.push_back({OP_ALLREDUCE, -1, u, -1});
+  out.push_back({OP_ALLREDUCE, -1, -1, -1});
+  return out;
+}
+
 std::vector<WOp> worker_plan(const zb_pass_t* passes, int n, int nv, int m, int worker, const int* worker_of,
                              bool fused) {
   std::vector<std::vector<std::vector<Op>>> groups(nv);  // per virtual stage of this worker: per pass

@@ -29,7 +29,9 @@ namespace plan {
 enum OpType : int32_t {
   OP_F = 0, OP_B = 1, OP_W = 2,
   OP_RECV_ACT = 3, OP_SEND_ACT = 4, OP_RECV_GRAD = 5, OP_SEND_GRAD = 6,
-  OP_VALIDATE = 7, OP_DISCARD_ACT = 8, OP_REPLAY_F = 9
+  OP_VALIDATE = 7, OP_DISCARD_ACT = 8, OP_REPLAY_F = 9,
+  OP_WP = 10,        // one W sub-computation: W unit `msg` of microbatch `mb` (data parallel tail)
+  OP_ALLREDUCE = 11  // data-parallel gradient all-reduce of W unit `msg` (-1: the vector region)
 };
 
 struct Op {
@@ -45,6 +47,20 @@ std::vector<int> speculative_counts(const zb_pass_t* passes, int n, int p);
 // backward (the gradient is sent after the W that follows its B).
 std::vector<Op> stage_plan(const zb_pass_t* passes, int n, int p, int m, int stage, bool pv_pending, bool amend,
                            bool fused);
+
+// ---- data parallelism (App. A) ---------------------------
+// D replicas of the pipeline; the stage's gradients are summed over its D replicas by an
+// all-reduce before the optimizer step.  A stage's W pass is n_units independent weight
+// gradient computations ("W units", Ctx::weight_unit order: the LM head on the last stage,
+// then per layer from the top fc2, fc1, proj, qkv, then the embedding on stage 0).  The W
+// passes at the TAIL of the stage's list (the maximal run of W ops ending the plan) become
+// OP_WP ops, one per (unit, microbatch), and each unit's OP_ALLREDUCE follows its last OP_WP:
+//   reorder = false  microbatch-major (the original W passes): the all-reduces can only
+//                    start inside the last tail W (App. A Fig. "poor overlapping")
+//   reorder = true   unit-major: all tail sub-computations of one parameter are clustered, so
+//                    its all-reduce overlaps the next parameter's sub-computations (App. A)
+// A final OP_ALLREDUCE(-1) sums the vector region (LayerNorm gammas / betas, biases).
+std::vector<Op> dp_tail(const std::vector<Op>& ops, int n_units, bool reorder);
 
 // ---- workers holding several model chunks (zb_schedule_chunked: ZB-V, 1F1B-I) ----------
 // Every chunk is a virtual stage v of an nv-stage chain (its own context and channels to

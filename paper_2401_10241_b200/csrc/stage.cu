@@ -302,7 +302,7 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
     void* dl = head_w_eager ? dlogits : sl.dlogits;
     lin_fwd(*this, sl.lnf, head_w, nullptr, logits, T, V, H, EPI_F32_STORE, nullptr);
     cross_entropy(dt, logits, sl.lab, dl, loss_rows, loss_acc, T, V,
-                  1.0f / (static_cast<float>(T) * static_cast<float>(cfg.m)), stream);
+                  1.0f / (static_cast<float>(T) * static_cast<float>(cfg.m) * static_cast<float>(dp_world)), stream);
     if (head_w_eager) lin_wgrad(*this, dl, sl.lnf, g_head_w, nullptr, V, H, T, beta);  // C8 eager option
     lin_dgrad(*this, dl, head_w, d_ln, T, H, V, EPI_F32_STORE, nullptr);
     ln_bwd(*this, d_ln, sl.xl, sl.muf, sl.rsf, lnf_g, nullptr, g32_dx, sl.dy, g_lnf_g, g_lnf_b, beta);
@@ -343,11 +343,24 @@ void Ctx::backward_weight(int mb, int slot_idx) { backward_weight_group(&mb, &sl
 // gradient read-modify-write is amortised over k microbatches.  k = 1 is the plain W.
 void Ctx::backward_weight_group(const int* mbs, const int* slot_idx, int k) {
   (void)mbs;
+  const int nu = n_w_units();
+  for (int u = 0; u < nu; ++u) weight_unit(u, slot_idx, k);
+  first_w_done = true;
+}
+
+// One W unit over k microbatches (the "computations calculating gradients for different
+// parameters" a W pass consists of, App. A).  beta = 0 on the unit's first contribution
+// of the iteration, so the units of the tail may run in any order (data-parallel reordering).
+void Ctx::weight_unit(int u, const int* slot_idx, int k) {
   if (k < 1 || k > kMaxSeg) throw std::invalid_argument("W group of 1..4 microbatches");
-  std::vector<Slot*> sl(k);
+  const int nu = n_w_units();
+  if (u < 0 || u >= nu) throw std::invalid_argument("W unit out of range");
+  if (static_cast<int>(unit_w_done.size()) != nu) unit_w_done.assign(nu, 0);
+  Slot* sl[kMaxSeg];
   for (int i = 0; i < k; ++i) sl[i] = &slots.at(slot_idx[i]);
   const int H = h;
-  const int beta = first_w_done ? 1 : 0;
+  const int beta = unit_w_done[u] ? 1 : 0;
+  unit_w_done[u] = 1;
   auto wgrad = [&](auto dy_of, auto x_of, float* dW, float* db, int M, int N) {
     GemmArgs g{};
     g.M = M; g.N = N; g.K = k * T;
@@ -365,29 +378,69 @@ void Ctx::backward_weight_group(const int* mbs, const int* slot_idx, int k) {
     }
     gemm(g, dt, stream);
   };
-  if (last && !head_w_eager)  // the LM head's W: dW_head += dlogits^T LN_f
+  const bool head = last && !head_w_eager;
+  if (head && u == 0) {  // the LM head's W: dW_head += dlogits^T LN_f
     wgrad([&](Slot& q) -> const void* { return q.dlogits; }, [&](Slot& q) -> const void* { return q.lnf; },
           g_head_w, nullptr, V, H);
-  for (int l = Ls - 1; l >= 0; --l) {
-    const LayerW& w = lw[l];
-    const bool top = l == Ls - 1;
-    wgrad([&](Slot& q) -> const void* { return top ? q.dy : q.L[l + 1].x; },
-          [&](Slot& q) -> const void* { return q.L[l].g; }, w.g_fc2_w, w.g_fc2_b, H, 4 * H);
-    wgrad([&](Slot& q) -> const void* { return q.L[l].u; }, [&](Slot& q) -> const void* { return q.L[l].ln2; },
-          w.g_fc1_w, w.g_fc1_b, 4 * H, H);
-    wgrad([&](Slot& q) -> const void* { return q.L[l].x1; }, [&](Slot& q) -> const void* { return q.L[l].o; },
-          w.g_proj_w, w.g_proj_b, H, H);
-    wgrad([&](Slot& q) -> const void* { return q.L[l].qkv; }, [&](Slot& q) -> const void* { return q.L[l].ln1; },
-          w.g_qkv_w, w.g_qkv_b, 3 * H, H);
+    return;
   }
-  if (first) {
-    if (!first_w_done) {
+  const int v = u - (head ? 1 : 0);
+  if (v == 4 * Ls) {  // stage 0: embedding scatter (wte, wpe)
+    if (!beta) {
       ZB_CUDA(cudaMemsetAsync(g_wte, 0, sizeof(float) * static_cast<size_t>(V) * H, stream));
       ZB_CUDA(cudaMemsetAsync(g_wpe, 0, sizeof(float) * static_cast<size_t>(s) * H, stream));
     }
     for (int i = 0; i < k; ++i) embed_bwd(dt, sl[i]->tok, sl[i]->L[0].x, g_wte, g_wpe, keys, T, s, H, stream);
+    return;
   }
-  first_w_done = true;
+  const int l = Ls - 1 - v / 4;
+  const LayerW& w = lw[l];
+  const bool top = l == Ls - 1;
+  switch (v % 4) {
+    case 0:
+      wgrad([&](Slot& q) -> const void* { return top ? q.dy : q.L[l + 1].x; },
+            [&](Slot& q) -> const void* { return q.L[l].g; }, w.g_fc2_w, w.g_fc2_b, H, 4 * H);
+      break;
+    case 1:
+      wgrad([&](Slot& q) -> const void* { return q.L[l].u; }, [&](Slot& q) -> const void* { return q.L[l].ln2; },
+            w.g_fc1_w, w.g_fc1_b, 4 * H, H);
+      break;
+    case 2:
+      wgrad([&](Slot& q) -> const void* { return q.L[l].x1; }, [&](Slot& q) -> const void* { return q.L[l].o; },
+            w.g_proj_w, w.g_proj_b, H, H);
+      break;
+    default:
+      wgrad([&](Slot& q) -> const void* { return q.L[l].qkv; }, [&](Slot& q) -> const void* { return q.L[l].ln1; },
+            w.g_qkv_w, w.g_qkv_b, 3 * H, H);
+  }
+}
+
+void Ctx::unit_grad_range(int u, int64_t* offset, int64_t* count) const {
+  if (u < 0) {  // LayerNorm gammas / betas and biases: [n_wd, n_total)
+    *offset = n_wd;
+    *count = n_total - n_wd;
+    return;
+  }
+  const bool head = last && !head_w_eager;
+  auto at = [&](const float* p, int64_t n) {
+    *offset = p - grad;
+    *count = n;
+  };
+  const int64_t H = h;
+  if (head && u == 0) return at(g_head_w, static_cast<int64_t>(V) * H);
+  const int v = u - (head ? 1 : 0);
+  if (v == 4 * Ls) {  // wte and wpe are adjacent in the flat layout
+    *offset = g_wte - grad;
+    *count = (g_wpe - g_wte) + static_cast<int64_t>(s) * H;
+    return;
+  }
+  const LayerW& w = lw[Ls - 1 - v / 4];
+  switch (v % 4) {
+    case 0: return at(w.g_fc2_w, 4 * H * H);
+    case 1: return at(w.g_fc1_w, 4 * H * H);
+    case 2: return at(w.g_proj_w, H * H);
+    default: return at(w.g_qkv_w, 3 * H * H);
+  }
 }
 
 void Ctx::timing_begin(int idx, int kind, int group) {

@@ -25,6 +25,7 @@
 namespace zb {
 
 struct Comm;  // NCCL transport (comm.cpp)
+struct DpComm;  // data-parallel all-reduce communicator (comm.cu)
 
 struct LayerW {
   float *ln1_g, *ln1_b, *qkv_b, *proj_b, *ln2_g, *ln2_b, *fc1_b, *fc2_b;  // f32 master
@@ -87,6 +88,11 @@ struct Ctx {
   PvState* pv = nullptr;
 
   bool first_b_done = false, first_w_done = false;
+  std::vector<uint8_t> unit_w_done;  // per W unit: its first contribution of the iteration landed (beta)
+
+  // data parallelism (zb_ctx_attach_dp): the stage's D replicas sum their gradients
+  std::unique_ptr<DpComm> dp;
+  int dp_world = 1;  // the cross-entropy mean runs over T m dp_world tokens
 
   // post-validation with NCCL: a validation of the last step is outstanding
   bool pv_pending = false;
@@ -110,6 +116,13 @@ struct Ctx {
   void backward_input(int mb, int slot, const void* dy, void* dx);
   void backward_weight(int mb, int slot);
   void backward_weight_group(const int* mbs, const int* slots, int k);  // W-grouping (k <= 4)
+  // W units (plan.h dp_tail): unit u of the W pass — the LM head (last stage, deferred), then per
+  // layer from the top fc2, fc1, proj, qkv (each with its bias), then the embedding (stage 0);
+  // backward_weight_group runs all units in this order
+  int n_w_units() const { return (last && !head_w_eager ? 1 : 0) + 4 * Ls + (first ? 1 : 0); }
+  void weight_unit(int u, const int* slots, int k);
+  // gradient range [offset, offset + count) of unit u in `grad` (the vector region: u = -1)
+  void unit_grad_range(int u, int64_t* offset, int64_t* count) const;
 
   void timing_begin(int idx, int kind, int group = 1);
   void timing_end(int idx);

@@ -3,7 +3,7 @@
 //
 // The round-end GPU boxes have one B200, and real NCCL refuses two ranks on the
 // same device, so libzb.so's NCCL transport (csrc/comm.cu: ncclGetUniqueId,
-// ncclCommInitRank, ncclSend, ncclRecv, ncclCommDestroy, ncclGetErrorString,
+// ncclCommInitRank, ncclSend, ncclRecv, ncclAllReduce, ncclCommDestroy, ncclGetErrorString,
 // dlopen'ed; ZB_NCCL_LIB selects this file instead) is exercised across real
 // processes through this shim: every 2-rank communicator owns, per receiving
 // rank, a device staging ring (NSLOT x CAP bytes) plus two 32-bit counters
@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -210,3 +211,63 @@ ncclResult_t ncclRecv(void* buf, size_t count, int dtype, int peer, void* comm, 
 }
 
 }  // extern "C"
+
+// ncclAllReduce (sum, 2 ranks): per chunk, my data goes to the peer's staging slot (as a send)
+// and the peer's chunk, once produced, is added into my buffer straight from my staging slot.
+// Rank 0 computes a + b, rank 1 b + a: IEEE addition is commutative, so both ranks hold the
+// same bits.  In place is allowed (the chunk is sent before it is overwritten, stream order).
+namespace {
+template <typename T>
+__global__ void k_add(T* out, const T* a, const T* b, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = a[i] + b[i];
+}
+}  // namespace
+
+extern "C" ncclResult_t ncclAllReduce(const void* sendbuf, void* recvbuf, size_t count, int dtype, int op, void* comm,
+                                      cudaStream_t st) {
+  auto* c = static_cast<Comm*>(comm);
+  if (!c || op != 0 || (dtype != 7 && dtype != 8)) return fail(kInvalid, "ncclAllReduce: only f32 / f64 sum");
+  const size_t es = dtype_size(dtype);
+  const size_t bytes = count * es;
+  uint32_t* out_ctr = c->ctr(c->out_base);
+  uint32_t* in_ctr = c->ctr(c->in_base);
+  for (size_t off = 0; off < bytes || (bytes == 0 && off == 0); off += c->cap) {
+    const size_t n = bytes - off < c->cap ? bytes - off : c->cap;
+    const uint32_t k = c->send_seq++;
+    if (k + 1 > static_cast<uint32_t>(NSLOT) &&
+        !cu_ok(cuStreamWaitValue32(st, reinterpret_cast<CUdeviceptr>(out_ctr + 1), k + 1 - NSLOT,
+                                   CU_STREAM_WAIT_VALUE_GEQ), "cuStreamWaitValue32"))
+      return kSystem;
+    if (n && cudaMemcpyAsync(c->out_base + (k % NSLOT) * c->cap, static_cast<const char*>(sendbuf) + off, n,
+                             cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return fail(kSystem, "ncclAllReduce: copy");
+    if (!cu_ok(cuStreamWriteValue32(st, reinterpret_cast<CUdeviceptr>(out_ctr + 0), k + 1,
+                                    CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32"))
+      return kSystem;
+    const uint32_t r = c->recv_seq++;
+    if (!cu_ok(cuStreamWaitValue32(st, reinterpret_cast<CUdeviceptr>(in_ctr + 0), r + 1, CU_STREAM_WAIT_VALUE_GEQ),
+               "cuStreamWaitValue32"))
+      return kSystem;
+    if (n) {
+      const size_t ne = n / es;
+      const int grid = static_cast<int>(std::min<size_t>((ne + 255) / 256, 1184));
+      const char* a = static_cast<const char*>(sendbuf) + off;
+      const char* b = c->in_base + (r % NSLOT) * c->cap;
+      char* o = static_cast<char*>(recvbuf) + off;
+      if (dtype == 7)
+        k_add<float><<<grid, 256, 0, st>>>(reinterpret_cast<float*>(o), reinterpret_cast<const float*>(a),
+                                           reinterpret_cast<const float*>(b), ne);
+      else
+        k_add<double><<<grid, 256, 0, st>>>(reinterpret_cast<double*>(o), reinterpret_cast<const double*>(a),
+                                            reinterpret_cast<const double*>(b), ne);
+      if (cudaGetLastError() != cudaSuccess) return fail(kSystem, "ncclAllReduce: add kernel");
+    }
+    if (!cu_ok(cuStreamWriteValue32(st, reinterpret_cast<CUdeviceptr>(in_ctr + 1), r + 1,
+                                    CU_STREAM_WRITE_VALUE_DEFAULT), "cuStreamWriteValue32"))
+      return kSystem;
+    if (bytes == 0) break;
+  }
+  return kOk;
+}

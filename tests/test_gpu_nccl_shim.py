@@ -1,7 +1,7 @@
 """The NCCL transport of libzb.so (comm.cu: zb_ctx_attach_nccl, zb_run_iteration over
 2-rank communicators on per-channel streams, the post-validation chains, the
 speculative warm-up F replay, zb_ctx_comm_probe) across REAL processes on one GPU:
-libnccl is replaced by the CUDA-IPC shim (tests/shim/nccl_ipc.cpp, ZB_NCCL_LIB) since
+libnccl is replaced by the CUDA-IPC shim (tests/shim/nccl_ipc.cu, ZB_NCCL_LIB) since
 NCCL refuses two ranks on one device.  Every rank is a separate process driven
 exactly as bench.py drives a GPU; the results must be BITWISE equal to the
 virtual-stage runner (zb_run_iteration_local + zb_post_validate_local), which the
