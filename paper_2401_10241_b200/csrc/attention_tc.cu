@@ -25,7 +25,7 @@ namespace attn_tc {
 // timeline of CTA (0, 0, 0) (the heaviest query-tile pair), globaltimer ns (measurement build only)
 __device__ unsigned long long g_trace_fwd[12][64];
 __device__ __forceinline__ void trf(int row, int n) {
-  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && n < 64) {
+  if (blockIdx.x == 0 && n < 64) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_trace_fwd[row][n] = t;
@@ -71,7 +71,8 @@ template <int D> struct FwdCfg {
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 
-// One CTA per (pair of 128-query tiles {2t, 2t+1}, head, sequence), heaviest pairs first.
+// One CTA per (pair of 128-query tiles {2t, 2t+1}, head, sequence), heaviest pairs first
+// (1-D grid in that order).
 // TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256, 256+D), O_1 [384, 384+D);
 // P_t (bf16 pairs) is written over the first 64 columns of S_t.
 // MMA issue order per key block j:  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) — the tensor core
@@ -101,8 +102,12 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / BQ;
   const int npair = (nqb + 1) / 2;
-  const int pr = npair - 1 - static_cast<int>(blockIdx.x);
-  const int hd = blockIdx.y, bb = blockIdx.z;
+  // 1-D grid in work order: every (head, sequence) of the heaviest pair first, so the
+  // hardware's in-order block dispatch is a longest-first list schedule (a 3-D grid
+  // dispatched x fastest interleaved heavy and light pairs and left heavy CTAs for the tail)
+  const int per = static_cast<int>(gridDim.x) / npair;  // a * b
+  const int pr = npair - 1 - static_cast<int>(blockIdx.x) / per;
+  const int hd = static_cast<int>(blockIdx.x) % per % a, bb = static_cast<int>(blockIdx.x) % per / a;
   const int h = a * D;
   const int q0 = 2 * pr;
   const bool two = q0 + 1 < nqb;
@@ -373,7 +378,7 @@ static void fwd_tc_launch(const AttnShape& sh, const void* qkv, void* o, float* 
   }
   const int h = sh.a * D;
   CUtensorMap tm = make_qkv_tmap(qkv, sh.b * sh.s, 3 * h);
-  dim3 grid((sh.s / attn_tc::BQ + 1) / 2, sh.a, sh.b);
+  const int grid = (sh.s / attn_tc::BQ + 1) / 2 * sh.a * sh.b;
   launch(PDL_ATTN, attn_tc::k_fwd_tc<D>, grid, 384, C::SMEM, st, tm, static_cast<bf16*>(o), lse, sh.s, sh.a,
                                                    attn_tc::LOG2E / sqrtf(static_cast<float>(D)));
   ZB_LAUNCH_CHECK();
