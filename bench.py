@@ -227,6 +227,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-validate", action="store_true", help="reference arm: skip the extrapolation check")
     ap.add_argument("--no-profile-p8", action="store_true")
+    ap.add_argument("--dp", type=int, default=1,
+                    help="data-parallel replicas (SURVEY §8(f)4): p = gpus / dp stages each, the global batch "
+                         "(m microbatches) split over the replicas, gradient all-reduces with App. A reordering")
     args = ap.parse_args()
     cfg = zb_synth.CONFIGS[args.config]
     if args.m:
@@ -242,6 +245,8 @@ def main():
     torch.cuda.set_device(0 if os.environ.get("ZB_SAME_DEVICE") == "1" else local)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dp > 1 and (world % args.dp or cfg.m % args.dp or args.family in ("zbv", "1f1bi")):
+        raise SystemExit("--dp must divide --gpus and m (and is not for the chunked families)")
     if world > 1:
         _start_watchdog(rank)
         if args.family in ("zbv", "1f1bi"):
@@ -353,7 +358,7 @@ def run_single(args, cfg, headline=True):
     lib.zb_dbg_launch_count(0, C.byref(nl))
     launches = int(nl.value)
     ms = ev0.elapsed_time(ev1) / args.steps
-    tokens_per_step = cfg.T * m
+    tokens_per_step = cfg.T * m * D          # all replicas
     value = tokens_per_step / (ms / 1000.0)
     loss = ctx.loss()
     # ---- the same workload again with CUDA events around every GEMM / attention / HBM-kernel
@@ -587,7 +592,13 @@ def run_pipeline(args, cfg, rank, world, local):
     import ctypes as C
 
     cdev = dist_setup(local)
-    p, m = world, cfg.m
+    D = args.dp                              # data-parallel replicas (1: pipeline only)
+    p, m = world // D, cfg.m // D            # stages per replica, microbatches per replica
+    rep, rank = divmod(rank, p)              # replica, stage (rank below = the stage)
+    grank = rep * p + rank
+    # every process creates every group in the same order
+    pgroups = [dist.new_group(list(range(r * p, r * p + p))) for r in range(D)] if D > 1 else [None]
+    pg = pgroups[rep]                        # this replica's pipeline
     mc = api.model_cfg(cfg, p, rank, m, 1, "bf16")
     sb = torch.tensor([api.slot_bytes(mc)], device=cdev, dtype=torch.int64)
     dist.all_reduce(sb, op=dist.ReduceOp.MAX)
@@ -599,16 +610,20 @@ def run_pipeline(args, cfg, rank, world, local):
     n_slots = max(1, sim.n_slots[rank], s1f.n_slots[rank])
     if args.family == "auto":
         n_slots = max(n_slots, lim // slot_b)
-    ids = [api.nccl_unique_ids(2 * (p - 1)) if rank == 0 else None]
+    ids = [([api.nccl_unique_ids(2 * (p - 1)) if p > 1 else b"" for _ in range(D)],
+            [api.nccl_unique_ids(1) for _ in range(p)] if D > 1 else None) if grank == 0 else None]
     dist.broadcast_object_list(ids, src=0)
     stream = torch.cuda.Stream()
     ctx = api.Context(cfg, p, rank, m, n_slots, dtype="bf16", stream=stream)
     params = zb_synth.make_stage_params(cfg, p, rank)
     ctx.set_params([params[n] for n, _, _ in zb_synth.param_specs(cfg, p, rank)])
     del params
-    ctx.attach_nccl(ids[0], rank, p)
+    if p > 1:
+        ctx.attach_nccl(ids[0][0][rep], rank, p)
+    if D > 1:   # the stage's replicas sum their gradients (App. A reordered tail)
+        ctx.attach_dp(ids[0][1][rank], rep, D)
     n_steps = args.warmup + args.steps
-    toks = [zb_synth.make_tokens(cfg, i) for i in range(n_steps)]
+    toks = [zb_synth.make_tokens(cfg, i)[rep * m:(rep + 1) * m] for i in range(n_steps)]
     tok_d = [torch.from_numpy(np.ascontiguousarray(t[..., :cfg.s])).cuda() for t in toks]
     lab_d = [torch.from_numpy(np.ascontiguousarray(t[..., 1:])).cuda() for t in toks]
     opt = api.optim_cfg(lr=1e-4, mode=args.opt, clip=1.0)
@@ -618,15 +633,19 @@ def run_pipeline(args, cfg, rank, world, local):
     lab_pin = [torch.from_numpy(np.ascontiguousarray(t[..., 1:])).pin_memory().numpy() for t in toks]
     fused_main = args.family == "1f1b"
 
+    dp_reorder = D > 1
+
     def run(family_passes, fused, steps, first, timing=False, host=False, o=None):
         o = o or opt
         for i in range(first, first + steps):
             if host:   # e2e: pinned host inputs copied inside the call, loss read back every step
                 ctx.run_iteration(family_passes, tok_pin[i % n_steps] if rank == 0 else None,
-                                  lab_pin[i % n_steps] if rank == p - 1 else None, host_inputs=True, fused=fused)
+                                  lab_pin[i % n_steps] if rank == p - 1 else None, host_inputs=True, fused=fused,
+                                  dp_reorder=dp_reorder)
             else:
                 ctx.run_iteration(family_passes, tok_d[i % n_steps] if rank == 0 else None,
-                                  lab_d[i % n_steps] if rank == p - 1 else None, timing=timing, fused=fused)
+                                  lab_d[i % n_steps] if rank == p - 1 else None, timing=timing, fused=fused,
+                                  dp_reorder=dp_reorder)
             ctx.post_validate_step(o)
             if host and rank == p - 1:
                 ctx.loss()
@@ -655,7 +674,7 @@ def run_pipeline(args, cfg, rank, world, local):
     t_ns, _ = ctx.profile()
     mine = torch.tensor(t_ns, device=cdev, dtype=torch.int64)
     allT = [torch.zeros_like(mine) for _ in range(p)]
-    dist.all_gather(allT, mine)
+    dist.all_gather(allT, mine, group=pg)
     TF, TB, TW = ([int(x[k]) for x in allT] for k in range(3))
     # T_comm: one f32 [T, h] boundary-gradient message, round trip / 2, max over pairs (zb_ctx_comm_probe)
     rt = torch.tensor([ctx.comm_probe(4 * cfg.T * cfg.h, 10)], device=cdev, dtype=torch.int64)
@@ -674,7 +693,7 @@ def run_pipeline(args, cfg, rank, world, local):
     lib.zb_dbg_launch_count(0, C.byref(nl))
     nlt = torch.tensor([nl.value], device=cdev, dtype=torch.int64)
     dist.all_reduce(nlt)                       # kernels launched by all ranks
-    tokens_per_step = cfg.T * m
+    tokens_per_step = cfg.T * m * D          # all replicas
     value = tokens_per_step / (ms / 1000.0)
     k_steps = min(args.steps, 5)
     # per-kernel-class timing over a second region (roofline)
@@ -695,7 +714,7 @@ def run_pipeline(args, cfg, rank, world, local):
     span = ends[-1] - starts[0] if starts else 0.0
     stat = torch.tensor([busy, span], device=cdev)
     gathered = [torch.zeros_like(stat) for _ in range(p)]
-    dist.all_gather(gathered, stat)
+    dist.all_gather(gathered, stat, group=pg)
     busys = [float(g[0]) for g in gathered]
     spans = [float(g[1]) for g in gathered]
     cost = max(spans)
@@ -714,7 +733,14 @@ def run_pipeline(args, cfg, rank, world, local):
     run(passes, fused_main, 1, 0, o=opt_other)
     ctx.post_validate_finish(opt_other)
     ms_other = timed(passes, fused_main, o=opt_other)
-    if rank == 0:
+    ms_noreorder = None
+    if D > 1:   # App. A ablation: the tail Ws in their W-major order (all-reduces start late)
+        dp_reorder = False
+        run(passes, fused_main, 1, 0)
+        ctx.post_validate_finish(opt)
+        ms_noreorder = timed(passes, fused_main)
+        dp_reorder = True
+    if grank == 0:
         peaks, src = read_peaks()
         flops_token = cfg.L * (72 * cfg.h ** 2 + 12 * cfg.s * cfg.h) + 6 * cfg.h * cfg.V
         g_tf = float(gt[1]) / (float(gt[0]) / 1e3) / 1e12 if float(gt[0]) else 0.0
@@ -728,7 +754,7 @@ def run_pipeline(args, cfg, rank, world, local):
                 "share_of_step": round(float(gt[0]) / p / k_steps / ms_ev, 4) if ms_ev else None}
         roof["traffic"], roof["traffic_source"] = gemm_traffic(cfg.name)
         e2e = {"value": tokens_per_step / (e2e_ms / 1000.0), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(2 * m * cfg.T * 4), "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(2 * m * D * cfg.T * 4), "d2h_bytes_per_step": 8 * D, "ms_per_step": e2e_ms,
                "steps": k_steps}
         pv_ms, sync_ms = (ms, ms_other) if args.opt == "pv" else (ms_other, ms)
         line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": p, "steps": args.steps,
@@ -744,7 +770,14 @@ def run_pipeline(args, cfg, rank, world, local):
                             "speedup": ms_1f1b / ms if ms_1f1b else None},
                 "pv_vs_sync": {"ms_per_step_pv": pv_ms, "ms_per_step_sync": sync_ms,
                                "speedup_pv": sync_ms / pv_ms if pv_ms else None},
-                "model_flops_utilization": round(value * flops_token / (p * peaks.get("bf16_tflops", 1680.3) * 1e12), 4)}
+                "model_flops_utilization": round(value * flops_token / (p * D * peaks.get("bf16_tflops", 1680.3) * 1e12), 4)}
+        if D > 1:
+            line["n_gpus"] = p * D
+            line["config"].update(parallelism=f"pp{p}dp{D}", replicas=D, microbatches_per_replica=m)
+            line["dp"] = {"replicas": D, "ms_per_step_app_a": ms, "ms_per_step_w_major_tail": ms_noreorder,
+                          "speedup_app_a": ms_noreorder / ms if ms_noreorder else None,
+                          "note": "gradient all-reduce per W unit on a side stream; App. A reorders the tail Ws "
+                                  "per parameter (P:452-454)"}
         print(json.dumps(line), flush=True)
     dist.barrier()
     ctx.close()

@@ -41,6 +41,12 @@ __device__ __forceinline__ void tr(int row, int n) {
   }
 }
 #define TR(row, n) tr(row, n)
+__device__ unsigned long long g_cta_bwd[16384][3];  // every CTA: {smid, start, end}
+__device__ __forceinline__ unsigned long long gtime_b() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #else
 #define TR(row, n)
 #endif
@@ -615,6 +621,14 @@ __global__ void __launch_bounds__(384, 1)
              const __grid_constant__ CUtensorMap do64, const __grid_constant__ CUtensorMap do128,
              const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a,
              int b, float scale, float scale_log2) {
+#ifdef ZB_ATTN_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 16384) {
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_cta_bwd[blockIdx.x][0] = sm;
+    g_cta_bwd[blockIdx.x][1] = gtime_b();
+  }
+#endif
   const int per = a * b;
   const int level = static_cast<int>(blockIdx.x) / (2 * per);
   int r = static_cast<int>(blockIdx.x) % (2 * per);
@@ -624,6 +638,9 @@ __global__ void __launch_bounds__(384, 1)
     r -= per;
     dq_body<D>(kv128, kv64, do128, lse, delta, dqkv, s, a, scale, scale_log2, level, r % a, r / a);
   }
+#ifdef ZB_ATTN_TRACE
+  if (threadIdx.x == 64 && blockIdx.x < 16384) g_cta_bwd[blockIdx.x][2] = gtime_b();
+#endif
 }
 
 }  // namespace attn_bwd_tc
@@ -665,6 +682,9 @@ bool attention_bwd_tc(const AttnShape& sh, const void* qkv, const void* dout, co
 }  // namespace zb
 
 #ifdef ZB_ATTN_TRACE
+extern "C" int zb_dbg_attn_bwd_cta_trace(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_bwd_tc::g_cta_bwd, sizeof(unsigned long long) * 16384 * 3));
+}
 extern "C" int zb_dbg_attn_trace(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_bwd_tc::g_trace, sizeof(unsigned long long) * 12 * 64));
 }

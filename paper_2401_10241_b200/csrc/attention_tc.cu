@@ -1,6 +1,7 @@
 // Causal flash-attention FORWARD on tcgen05 (bf16, s % 128 == 0).
 //
-// One CTA per (pair of 128-query tiles, head, sequence), heaviest pairs first.
+// Persistent CTAs (one per SM) over work items (pair of 128-query tiles, head, sequence),
+// heaviest pairs first.
 //   warp 0      TMA: Q_0, Q_1 once; K_j, V_j in 2-stage rings (boxes {64 cols, 128 rows} of the
 //               packed qkv [b*s, 3h], 128B swizzle), shared by both query tiles
 //   warp 1      MMA: S_t = Q_t K_j^T (SS) and O_t += P_t V_j (TS, P from TMEM), ping-ponging
@@ -32,6 +33,13 @@ __device__ __forceinline__ void trf(int row, int n) {
   }
 }
 #define TRF(row, n) trf(row, n)
+// every CTA: {smid, start, end} (globaltimer ns) — CTA durations and per-SM gaps
+__device__ unsigned long long g_cta_fwd[8192][3];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #else
 #define TRF(row, n)
 #endif
@@ -51,7 +59,6 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-constexpr bool kAlternate = false;
 // P of a key block is published to the MMA warp in PQ parts (2: halves of 64 keys, 4: quarters
 // of 32) so the PV products of the first parts overlap the exponentials of the later ones
 #ifndef ZB_ATTN_PQ
@@ -69,10 +76,18 @@ template <int D> struct FwdCfg {
   static constexpr int OFF_V = (2 + KST) * TILE;
   static constexpr int OFF_BAR = (2 + KST + VST) * TILE;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static_assert((18 + 2 * (PQ - 1) + 1) * 8 <= 256, "barrier area");
 };
 
-// One CTA per (pair of 128-query tiles {2t, 2t+1}, head, sequence), heaviest pairs first
-// (1-D grid in that order).
+// Persistent: one CTA per SM walks work items (pair of 128-query tiles {2t, 2t+1}, head,
+// sequence), numbered heaviest pair first; CTA c takes items r G + c (even rounds r) and
+// r G + G-1-c (odd rounds) of G = gridDim.x CTAs — a snake order that evens out the
+// triangular per-pair work.  Across items the TMEM allocation, barriers and K/V rings stay
+// live: the next item's Q is loaded as soon as the current item's last S product has read
+// Q (q_empty), its first S products run while the softmax warps still write the current
+// item's O (o_empty gates only the next item's first PV per tile), so the per-item
+// prologue / epilogue of the former one-CTA-per-item grid (~6.6 us per CTA at the 6.2B
+// shape, scripts/attn_cta_trace.py) overlaps compute.
 // TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256, 256+D), O_1 [384, 384+D);
 // P_t (bf16 pairs) is written over the first 64 columns of S_t.
 // MMA issue order per key block j:  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) — the tensor core
@@ -80,9 +95,12 @@ template <int D> struct FwdCfg {
 // P_t(j) that PV_t(j), issued just before it, reads: tcgen05.mma of one thread execute in issue
 // order.  The commit after S_t(j+1) also covers PV_t(j), so the softmax warps may rescale O_t
 // as soon as they see S_t(j+1).
+// Barrier parities come from running counters of the CTA (blocks per tile, items per tile,
+// K/V ring position), not from the block index of the current item.
 template <int D>
 __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o,
-                                                   float* __restrict__ lse, int s, int a, float scale_log2) {
+                                                   float* __restrict__ lse, int s, int a, int items,
+                                                   float scale_log2) {
   using C = FwdCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -96,26 +114,48 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   uint64_t* p_full = bar + 11;    // [2] per tile
   uint64_t* o_final = bar + 13;   // [2] per tile
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 15);
-  uint64_t* tok = bar + 16;       // [2] per tile: the other tile's exponential phase is done
+  uint64_t* o_empty = bar + 16;   // [2] per tile: the softmax warps have read O_t of their item
   uint64_t* p_part = bar + 18;    // [2][PQ - 1] per tile: P of keys [0, 32 (q + 1)) stored (PV may start)
+  uint64_t* q_empty = bar + 18 + 2 * (PQ - 1);  // the item's last S product has read Q
 
+#ifdef ZB_ATTN_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 8192) {
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_cta_fwd[blockIdx.x][0] = sm;
+    g_cta_fwd[blockIdx.x][1] = gtime();
+  }
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / BQ;
   const int npair = (nqb + 1) / 2;
-  // 1-D grid in work order: every (head, sequence) of the heaviest pair first, so the
-  // hardware's in-order block dispatch is a longest-first list schedule (a 3-D grid
-  // dispatched x fastest interleaved heavy and light pairs and left heavy CTAs for the tail)
-  const int per = static_cast<int>(gridDim.x) / npair;  // a * b
-  const int pr = npair - 1 - static_cast<int>(blockIdx.x) / per;
-  const int hd = static_cast<int>(blockIdx.x) % per % a, bb = static_cast<int>(blockIdx.x) % per / a;
+  const int per = items / npair;  // a * b
   const int h = a * D;
-  const int q0 = 2 * pr;
-  const bool two = q0 + 1 < nqb;
-  const int nkv0 = q0 + 1, nkv1 = two ? q0 + 2 : 0;
-  const int nkv = two ? nkv1 : nkv0;
+  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  // r-th item of this CTA (snake order), or -1
+  auto item_of = [&](int r) {
+    const int it = r * G + ((r & 1) ? G - 1 - c : c);
+    return it < items ? it : -1;
+  };
+  struct Item {
+    int q0, hd, bb, nkv0, nkv1;
+    bool two;
+  };
+  auto decode = [&](int it) {
+    Item w;
+    const int pr = npair - 1 - it / per;
+    w.hd = it % per % a;
+    w.bb = it % per / a;
+    w.q0 = 2 * pr;
+    w.two = w.q0 + 1 < nqb;
+    w.nkv0 = w.q0 + 1;
+    w.nkv1 = w.two ? w.q0 + 2 : 0;
+    return w;
+  };
 
   if (threadIdx.x == 0) {
     sm100::mbar_init(q_full, 1);
+    sm100::mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&k_full[i], 1);
       sm100::mbar_init(&k_empty[i], 1);
@@ -124,7 +164,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&p_full[i], 4);  // one arrival per softmax warp
       sm100::mbar_init(&o_final[i], 1);
-      sm100::mbar_init(&tok[i], 4);
+      sm100::mbar_init(&o_empty[i], 4);
       for (int q = 0; q < PQ - 1; ++q) sm100::mbar_init(&p_part[i * (PQ - 1) + q], 4);
     }
     sm100::fence_mbar_init();
@@ -137,35 +177,43 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
   pdl_wait();
   const uint32_t tbase = *tslot;
-  const int row0 = bb * s;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA
-      sm100::mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * C::TILE);
-      for (int t = 0; t < (two ? 2 : 1); ++t)
-        for (int at = 0; at < C::ATOMS; ++at)
-          sm100::tma_load_2d(smem + C::OFF_Q + t * C::TILE + at * 16384, &tm, q_full, hd * D + 64 * at,
-                             row0 + (q0 + t) * BQ);
-      auto load_k = [&](int j) {
-        const int st = j & 1;
-        sm100::mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
-        sm100::mbar_arrive_expect_tx(&k_full[st], C::TILE);
-        for (int at = 0; at < C::ATOMS; ++at)
-          sm100::tma_load_2d(smem + C::OFF_K + st * C::TILE + at * 16384, &tm, &k_full[st], h + hd * D + 64 * at,
-                             row0 + j * BKV);
-      };
-      auto load_v = [&](int j) {
-        const int st = j & 1;
-        sm100::mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
-        sm100::mbar_arrive_expect_tx(&v_full[st], C::TILE);
-        for (int at = 0; at < C::ATOMS; ++at)
-          sm100::tma_load_2d(smem + C::OFF_V + st * C::TILE + at * 16384, &tm, &v_full[st], 2 * h + hd * D + 64 * at,
-                             row0 + j * BKV);
-      };
-      load_k(0);
-      for (int j = 0; j < nkv; ++j) {  // K runs one block ahead of V
-        if (j + 1 < nkv) load_k(j + 1);
-        load_v(j);
+      int kn = 0, vn = 0;  // K / V ring positions (continuous over items)
+      for (int r = 0, it; (it = item_of(r)) >= 0; ++r) {
+        const Item w = decode(it);
+        const int row0 = w.bb * s;
+        const int nkv = w.two ? w.nkv1 : w.nkv0;
+        sm100::mbar_wait(q_empty, (r & 1) ^ 1);  // the previous item's S products are done with Q
+        sm100::mbar_arrive_expect_tx(q_full, (w.two ? 2 : 1) * C::TILE);
+        for (int t = 0; t < (w.two ? 2 : 1); ++t)
+          for (int at = 0; at < C::ATOMS; ++at)
+            sm100::tma_load_2d(smem + C::OFF_Q + t * C::TILE + at * 16384, &tm, q_full, w.hd * D + 64 * at,
+                               row0 + (w.q0 + t) * BQ);
+        auto load_k = [&](int j) {
+          const int st = kn & 1;
+          sm100::mbar_wait(&k_empty[st], ((kn >> 1) & 1) ^ 1);
+          sm100::mbar_arrive_expect_tx(&k_full[st], C::TILE);
+          for (int at = 0; at < C::ATOMS; ++at)
+            sm100::tma_load_2d(smem + C::OFF_K + st * C::TILE + at * 16384, &tm, &k_full[st],
+                               h + w.hd * D + 64 * at, row0 + j * BKV);
+          ++kn;
+        };
+        auto load_v = [&](int j) {
+          const int st = vn & 1;
+          sm100::mbar_wait(&v_empty[st], ((vn >> 1) & 1) ^ 1);
+          sm100::mbar_arrive_expect_tx(&v_full[st], C::TILE);
+          for (int at = 0; at < C::ATOMS; ++at)
+            sm100::tma_load_2d(smem + C::OFF_V + st * C::TILE + at * 16384, &tm, &v_full[st],
+                               2 * h + w.hd * D + 64 * at, row0 + j * BKV);
+          ++vn;
+        };
+        load_k(0);
+        for (int j = 0; j < nkv; ++j) {  // K runs one block ahead of V
+          if (j + 1 < nkv) load_k(j + 1);
+          load_v(j);
+        }
       }
     }
   } else if (warp == 1) {
@@ -173,192 +221,216 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = sm100::idesc_bf16(128, D, false, true);
       const uint32_t sq = sm100::smem_addr(smem + C::OFF_Q);
-      auto issue_s = [&](int t, int j) {  // S_t = Q_t K_j^T
-        const uint32_t sk = sm100::smem_addr(smem + C::OFF_K + (j & 1) * C::TILE);
-        const uint64_t qd = sm100::smem_desc(sq + t * C::TILE, 16, 1024, sm100::kSwizzle128B);
-        const uint64_t kd = sm100::smem_desc(sk, 16, 1024, sm100::kSwizzle128B);
+      int kn = 0, vn = 0;              // K / V ring positions
+      int pb[2] = {0, 0};              // PV blocks issued per tile (P barrier parity)
+      int ti[2] = {0, 0};              // items started per tile (o_empty parity)
+      for (int r = 0, it; (it = item_of(r)) >= 0; ++r) {
+        const Item w = decode(it);
+        const int nkv = w.two ? w.nkv1 : w.nkv0;
+        int s_left = w.nkv0 + w.nkv1;  // S products of the item still to issue (q_empty after the last)
+        auto issue_s = [&](int t, int stage) {  // S_t = Q_t K^T (K in ring stage `stage`)
+          const uint32_t sk = sm100::smem_addr(smem + C::OFF_K + stage * C::TILE);
+          const uint64_t qd = sm100::smem_desc(sq + t * C::TILE, 16, 1024, sm100::kSwizzle128B);
+          const uint64_t kd = sm100::smem_desc(sk, 16, 1024, sm100::kSwizzle128B);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          if (sm100::elect_one()) sm100::mma_bf16_ss(tbase + t * 128, sm100::desc_adv(qd, off), sm100::desc_adv(kd, off), idesc_s,
-                             kk != 0 ? 1u : 0u);
-        }
-        if (sm100::elect_one()) sm100::mma_commit(&s_full[t]);
-      };
-      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j, the first 64 keys as soon as their P is stored
-        const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + (j & 1) * C::TILE);
-        const uint64_t vd = sm100::smem_desc(sv, 16384, 1024, sm100::kSwizzle128B);
-#pragma unroll
-        for (int q = 0; q < PQ; ++q) {
-          constexpr int KQ = BKV / 16 / PQ;  // K-steps per published part of P
-          sm100::mbar_wait_warp(q + 1 < PQ ? &p_part[t * (PQ - 1) + q] : &p_full[t], j & 1);
-          if (q + 1 == PQ) TRF(t, j);
-          sm100::tc_fence_after();
-          if (sm100::elect_one()) {
-#pragma unroll
-            for (int kk = KQ * q; kk < KQ * q + KQ; ++kk)
-              sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, sm100::desc_adv(vd, kk * 2048),
-                                 idesc_o, (j | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            if (sm100::elect_one()) sm100::mma_bf16_ss(tbase + t * 128, sm100::desc_adv(qd, off), sm100::desc_adv(kd, off), idesc_s,
+                               kk != 0 ? 1u : 0u);
           }
-          __syncwarp();
-        }
-      };
-      sm100::mbar_wait_warp(q_full, 0);
-      sm100::mbar_wait_warp(&k_full[0], 0);
-      sm100::tc_fence_after();
-      issue_s(0, 0);
-      if (two) issue_s(1, 0);
-      if (sm100::elect_one()) sm100::mma_commit(&k_empty[0]);
-      for (int j = 0; j < nkv; ++j) {
-        const bool more = j + 1 < nkv;
-        sm100::mbar_wait_warp(&v_full[j & 1], (j >> 1) & 1);
-        if (more) sm100::mbar_wait_warp(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          if (sm100::elect_one()) sm100::mma_commit(&s_full[t]);
+          if (--s_left == 0) { if (sm100::elect_one()) sm100::mma_commit(q_empty); }
+        };
+        auto issue_pv = [&](int t, int j, int stage) {  // O_t += P_t V_j, the first keys as soon as their P is stored
+          const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + stage * C::TILE);
+          const uint64_t vd = sm100::smem_desc(sv, 16384, 1024, sm100::kSwizzle128B);
+          if (j == 0) {  // the softmax warps have read O_t of the tile's previous item
+            sm100::mbar_wait_warp(&o_empty[t], (ti[t] & 1) ^ 1);
+            ++ti[t];
+          }
+          const uint32_t par = pb[t] & 1;
+#pragma unroll
+          for (int q = 0; q < PQ; ++q) {
+            constexpr int KQ = BKV / 16 / PQ;  // K-steps per published part of P
+            sm100::mbar_wait_warp(q + 1 < PQ ? &p_part[t * (PQ - 1) + q] : &p_full[t], par);
+            if (q + 1 == PQ && r == 0) TRF(t, j);
+            sm100::tc_fence_after();
+            if (sm100::elect_one()) {
+#pragma unroll
+              for (int kk = KQ * q; kk < KQ * q + KQ; ++kk)
+                sm100::mma_bf16_ts(tbase + 256 + t * 128, tbase + t * 128 + kk * 8, sm100::desc_adv(vd, kk * 2048),
+                                   idesc_o, (j | kk) != 0 ? 1u : 0u);
+            }
+            __syncwarp();
+          }
+          ++pb[t];
+        };
+        sm100::mbar_wait_warp(q_full, r & 1);
+        sm100::mbar_wait_warp(&k_full[kn & 1], (kn >> 1) & 1);
         sm100::tc_fence_after();
-        if (j < nkv0) {
-          issue_pv(0, j);
-          if (j == nkv0 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[0]); }
+        issue_s(0, kn & 1);
+        if (w.two) issue_s(1, kn & 1);
+        if (sm100::elect_one()) sm100::mma_commit(&k_empty[kn & 1]);
+        ++kn;
+        for (int j = 0; j < nkv; ++j) {
+          const bool more = j + 1 < nkv;
+          const int vst = vn & 1;
+          sm100::mbar_wait_warp(&v_full[vst], (vn >> 1) & 1);
+          if (more) sm100::mbar_wait_warp(&k_full[kn & 1], (kn >> 1) & 1);
+          sm100::tc_fence_after();
+          if (j < w.nkv0) {
+            issue_pv(0, j, vst);
+            if (j == w.nkv0 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[0]); }
+          }
+          if (j + 1 < w.nkv0) issue_s(0, kn & 1);
+          if (j < w.nkv1) {
+            issue_pv(1, j, vst);
+            if (j == w.nkv1 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[1]); }
+          }
+          if (sm100::elect_one()) sm100::mma_commit(&v_empty[vst]);
+          ++vn;
+          if (j + 1 < w.nkv1) issue_s(1, kn & 1);
+          if (more) {
+            if (sm100::elect_one()) sm100::mma_commit(&k_empty[kn & 1]);
+            ++kn;
+          }
         }
-        if (j + 1 < nkv0) issue_s(0, j + 1);
-        if (j < nkv1) {
-          issue_pv(1, j);
-          if (j == nkv1 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[1]); }
-        }
-        if (sm100::elect_one()) sm100::mma_commit(&v_empty[j & 1]);
-        if (j + 1 < nkv1) issue_s(1, j + 1);
-        if (more) { if (sm100::elect_one()) sm100::mma_commit(&k_empty[(j + 1) & 1]); }
       }
     }
   } else if (warp >= 4) {  // ---------------- softmax: 4 warps per tile, one row per thread
     const int t = (warp - 4) >> 2;
-    const int nk = t == 0 ? nkv0 : nkv1;
-    const int r = (warp & 3) * 32 + lane;  // row within the tile = TMEM lane
+    const int r_ = (warp & 3) * 32 + lane;  // row within the tile = TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tbase + t * 128 + lane_off, t_o = tbase + 256 + t * 128 + lane_off;
-    const int qt = q0 + t;
-    float m = -INFINITY, l = 0.f;  // m: reference max (log2 units), l: running sum relative to m
-    for (int j = 0; j < nk; ++j) {
-      sm100::mbar_wait(&s_full[t], j & 1);
-      if ((warp & 3) == 0 && lane == 0) TRF(2 + 3 * t, j);
-      sm100::tc_fence_after();
-      float sv[128];
+    int sb = 0;  // S blocks consumed by this tile (s_full / p barrier parity)
+    int ni = 0;  // items finished by this tile (o_final parity)
+    for (int rr = 0, it; (it = item_of(rr)) >= 0; ++rr) {
+      const Item w = decode(it);
+      const int nk = t == 0 ? w.nkv0 : w.nkv1;
+      const int qt = w.q0 + t;
+      float m = -INFINITY, l = 0.f;  // m: reference max (log2 units), l: running sum relative to m
+      for (int j = 0; j < nk; ++j, ++sb) {
+        sm100::mbar_wait(&s_full[t], sb & 1);
+        if ((warp & 3) == 0 && lane == 0 && rr == 0) TRF(2 + 3 * t, j);
+        sm100::tc_fence_after();
+        float sv[128];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) sm100::tmem_ld32(t_s + c * 32, reinterpret_cast<uint32_t*>(sv + 32 * c));
-      sm100::tmem_ld_wait();
-      if ((warp & 3) == 0 && lane == 0) TRF(3 + 3 * t, j);
-      if (j == qt) {
-#pragma unroll
-        for (int k = 0; k < 128; ++k)
-          if (k > r) sv[k] = -INFINITY;
-      }
-      float mx;
-      {  // 8 independent chains, then a tree (a single 128-long chain is pure latency)
-        float m8[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) m8[i] = sv[i];
-#pragma unroll
-        for (int k = 8; k < 128; ++k) m8[k & 7] = fmaxf(m8[k & 7], sv[k]);
-        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-      }
-      mx *= scale_log2;
-      // lazy rescaling: keep the old reference max unless it grew by more than 8 (p <= 2^8).
-      // The decision is per row, but tcgen05.ld / st are warp-collective (.sync.aligned):
-      // the whole warp enters the rescale when any of its rows needs it (corr = 1 elsewhere).
-      const bool grow = mx > m + 8.f;
-      if (__any_sync(0xffffffffu, grow)) {
-        const float corr = grow ? sm100::ex2(m - mx) : 1.f;
-        if (grow) {
-          m = mx;
-          l *= corr;
-        }
-        if (j > 0) {  // O_t holds blocks < j (PV_t(j-1) completed before S_t(j) was committed)
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            sm100::tmem_ld32(t_o + c * 32, ov);
-            sm100::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-            sm100::tmem_st32(t_o + c * 32, ov);
-          }
-          sm100::tmem_st_wait();
-        }
-      }
-      // kAlternate: the two tiles' exponential phases strictly alternate (token passing), so
-      // each runs alone on the MUFU while the other tile's PV and next S use the tensor core.
-      // Measured: no faster than free-running (the per-tile chain exp -> PV, S -> exp, not
-      // the MUFU, sets the period: scripts/attn_fwd_trace.py), so it is off.
-      const bool alt = kAlternate && two && j < nkv0;
-      if (alt) sm100::mbar_wait(&tok[t], t == 0 ? ((j & 1) ^ 1) : (j & 1));
-      if ((warp & 3) == 0 && lane == 0) TRF(8 + t, j);
-      const float mneg = -m;
-      const bool poly = kPolyExp && j != qt;  // masked (-inf) scores only on the diagonal block: MUFU there
-      float sum4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int q = 0; q < PQ; ++q) {  // keys [KP q, KP q + KP) -> P columns [KP q / 2, KP (q + 1) / 2)
-        constexpr int KP = BKV / PQ;
-        uint32_t pk[KP / 2];
-#pragma unroll
-        for (int k = 0; k < KP; k += 2) {
-          const float x0 = fmaf(sv[KP * q + k], scale_log2, mneg), x1 = fmaf(sv[KP * q + k + 1], scale_log2, mneg);
-          float p0, p1;
-          if ((k & 6) == 6 && poly) {  // a quarter of the exponentials on the FMA pipe (MUFU is the bottleneck)
-            p0 = ex2_poly(x0);
-            p1 = ex2_poly(x1);
-          } else {
-            p0 = sm100::ex2(x0);
-            p1 = sm100::ex2(x1);
-          }
-          sum4[(k >> 1) & 3] += p0 + p1;
-          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
-          pk[k >> 1] = *reinterpret_cast<uint32_t*>(&v2);
-        }
-        if constexpr (KP == 64)
-          sm100::tmem_st32(t_s + KP / 2 * q, pk);
-        else
-          sm100::tmem_st16(t_s + KP / 2 * q, pk);
-        if (q + 1 < PQ) {  // publish this part of P: its PV products overlap the next part here
-          sm100::tmem_st_wait();
-          sm100::tc_fence_before();
-          sm100::mbar_arrive_warp(&p_part[t * (PQ - 1) + q]);
-        }
-      }
-      l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
-      if ((warp & 3) == 0 && lane == 0) TRF(10 + t, j);
-      if (alt) sm100::mbar_arrive_warp(&tok[t ^ 1]);
-      sm100::tmem_st_wait();
-      sm100::tc_fence_before();
-      if ((warp & 3) == 0 && lane == 0) TRF(4 + 3 * t, j);
-      sm100::mbar_arrive_warp(&p_full[t]);
-    }
-    if (nk > 0) {
-      sm100::mbar_wait(&o_final[t], 0);
-      sm100::tc_fence_after();
-      const int q = qt * BQ + r;
-      const float inv = 1.f / l;
-      bf16* orow = o + (static_cast<int64_t>(bb) * s + q) * h + hd * D;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        sm100::tmem_ld32(t_o + c * 32, ov);
+        for (int c4 = 0; c4 < 4; ++c4) sm100::tmem_ld32(t_s + c4 * 32, reinterpret_cast<uint32_t*>(sv + 32 * c4));
         sm100::tmem_ld_wait();
+        if ((warp & 3) == 0 && lane == 0 && rr == 0) TRF(3 + 3 * t, j);
+        if (j == qt) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint4 u;
-          __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * g + 2 * e]) * inv,
-                                          __uint_as_float(ov[8 * g + 2 * e + 1]) * inv);
-          *reinterpret_cast<uint4*>(orow + c * 32 + g * 8) = u;
+          for (int k = 0; k < 128; ++k)
+            if (k > r_) sv[k] = -INFINITY;
         }
+        float mx;
+        {  // 8 independent chains, then a tree (a single 128-long chain is pure latency)
+          float m8[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) m8[i] = sv[i];
+#pragma unroll
+          for (int k = 8; k < 128; ++k) m8[k & 7] = fmaxf(m8[k & 7], sv[k]);
+          mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        }
+        mx *= scale_log2;
+        // lazy rescaling: keep the old reference max unless it grew by more than 8 (p <= 2^8).
+        // The decision is per row, but tcgen05.ld / st are warp-collective (.sync.aligned):
+        // the whole warp enters the rescale when any of its rows needs it (corr = 1 elsewhere).
+        const bool grow = mx > m + 8.f;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float corr = grow ? sm100::ex2(m - mx) : 1.f;
+          if (grow) {
+            m = mx;
+            l *= corr;
+          }
+          if (j > 0) {  // O_t holds blocks < j (PV_t(j-1) completed before S_t(j) was committed)
+#pragma unroll 1
+            for (int c4 = 0; c4 < D / 32; ++c4) {
+              uint32_t ov[32];
+              sm100::tmem_ld32(t_o + c4 * 32, ov);
+              sm100::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
+              sm100::tmem_st32(t_o + c4 * 32, ov);
+            }
+            sm100::tmem_st_wait();
+          }
+        }
+        if ((warp & 3) == 0 && lane == 0 && rr == 0) TRF(8 + t, j);
+        const float mneg = -m;
+        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < PQ; ++q) {  // keys [KP q, KP q + KP) -> P columns [KP q / 2, KP (q + 1) / 2)
+          constexpr int KP = BKV / PQ;
+          uint32_t pk[KP / 2];
+#pragma unroll
+          for (int k = 0; k < KP; k += 2) {
+            const float x0 = fmaf(sv[KP * q + k], scale_log2, mneg), x1 = fmaf(sv[KP * q + k + 1], scale_log2, mneg);
+            float p0, p1;
+            if ((k & 6) == 6 && kPolyExp && j != qt) {  // a quarter on the FMA pipe (measured slower: off)
+              p0 = ex2_poly(x0);
+              p1 = ex2_poly(x1);
+            } else {
+              p0 = sm100::ex2(x0);
+              p1 = sm100::ex2(x1);
+            }
+            sum4[(k >> 1) & 3] += p0 + p1;
+            __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+            pk[k >> 1] = *reinterpret_cast<uint32_t*>(&v2);
+          }
+          if constexpr (KP == 64)
+            sm100::tmem_st32(t_s + KP / 2 * q, pk);
+          else
+            sm100::tmem_st16(t_s + KP / 2 * q, pk);
+          if (q + 1 < PQ) {  // publish this part of P: its PV products overlap the next part here
+            sm100::tmem_st_wait();
+            sm100::tc_fence_before();
+            sm100::mbar_arrive_warp(&p_part[t * (PQ - 1) + q]);
+          }
+        }
+        l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+        if ((warp & 3) == 0 && lane == 0 && rr == 0) TRF(10 + t, j);
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        if ((warp & 3) == 0 && lane == 0 && rr == 0) TRF(4 + 3 * t, j);
+        sm100::mbar_arrive_warp(&p_full[t]);
       }
-      lse[(static_cast<int64_t>(bb) * a + hd) * s + q] = (m + log2f(l)) * LN2;
+      if (nk > 0) {
+        sm100::mbar_wait(&o_final[t], ni & 1);
+        ++ni;
+        sm100::tc_fence_after();
+        const int q = qt * BQ + r_;
+        const float inv = 1.f / l;
+        bf16* orow = o + (static_cast<int64_t>(w.bb) * s + q) * h + w.hd * D;
+#pragma unroll 1
+        for (int c4 = 0; c4 < D / 32; ++c4) {
+          uint32_t ov[32];
+          sm100::tmem_ld32(t_o + c4 * 32, ov);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint4 u;
+            __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * g + 2 * e]) * inv,
+                                            __uint_as_float(ov[8 * g + 2 * e + 1]) * inv);
+            *reinterpret_cast<uint4*>(orow + c4 * 32 + g * 8) = u;
+          }
+        }
+        sm100::tc_fence_before();
+        sm100::mbar_arrive_warp(&o_empty[t]);  // O_t may be overwritten by the next item's PV
+        lse[(static_cast<int64_t>(w.bb) * a + w.hd) * s + q] = (m + log2f(l)) * LN2;
+      }
     }
   }
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   if (warp == 2) sm100::tmem_dealloc<512>(tbase);
+#ifdef ZB_ATTN_TRACE
+  if (threadIdx.x == 64 && blockIdx.x < 8192) g_cta_fwd[blockIdx.x][2] = gtime();
+#endif
 }
 
 }  // namespace attn_tc
@@ -378,9 +450,10 @@ static void fwd_tc_launch(const AttnShape& sh, const void* qkv, void* o, float* 
   }
   const int h = sh.a * D;
   CUtensorMap tm = make_qkv_tmap(qkv, sh.b * sh.s, 3 * h);
-  const int grid = (sh.s / attn_tc::BQ + 1) / 2 * sh.a * sh.b;
-  launch(PDL_ATTN, attn_tc::k_fwd_tc<D>, grid, 384, C::SMEM, st, tm, static_cast<bf16*>(o), lse, sh.s, sh.a,
-                                                   attn_tc::LOG2E / sqrtf(static_cast<float>(D)));
+  const int items = (sh.s / attn_tc::BQ + 1) / 2 * sh.a * sh.b;
+  const int grid = items < num_sms() ? items : num_sms();  // persistent: one CTA per SM
+  launch(PDL_ATTN, attn_tc::k_fwd_tc<D>, grid, 384, C::SMEM, st, tm, static_cast<bf16*>(o), lse, sh.s, sh.a, items,
+         attn_tc::LOG2E / sqrtf(static_cast<float>(D)));
   ZB_LAUNCH_CHECK();
 }
 
@@ -397,6 +470,9 @@ bool attention_fwd_tc(const AttnShape& sh, const void* qkv, void* o, float* lse,
 }  // namespace zb
 
 #ifdef ZB_ATTN_TRACE
+extern "C" int zb_dbg_attn_fwd_cta_trace(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_cta_fwd, sizeof(unsigned long long) * 8192 * 3));
+}
 extern "C" int zb_dbg_attn_fwd_trace(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_trace_fwd, sizeof(unsigned long long) * 12 * 64));
 }

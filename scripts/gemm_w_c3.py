@@ -38,9 +38,14 @@ for name, M, N in [("qkv", 3 * h, h), ("proj", h, h), ("fc1", 4 * h, h), ("fc2",
         "W_bf16": lambda: api.dbg_gemm(dY, X, C16, M=M, N=N, K=K, a_mn=True, b_mn=True, epi=0),
         "Kmaj_acc": lambda: api.dbg_gemm(dYt, Xt, C32, M=M, N=N, K=K, epi=4, beta=1),
         "Kmaj_bf16": lambda: api.dbg_gemm(dYt, Xt, C16, M=M, N=N, K=K, epi=0),
+        "W_acc_beta0": lambda: api.dbg_gemm(dY, X, C32, M=M, N=N, K=K, a_mn=True, b_mn=True, epi=4, beta=0),
         "cublas": lambda: torch.matmul(dY.t(), X, out=C16),
     }
     r = {"shape": f"W {name}", "MNK": [M, N, K]}
     for k, fn in v.items():
         r[k] = round(fl / timed(fn) / 1e9, 1)
+    # the same reduce-add epilogue behind twice the mainloop per tile (K = 2T)
+    dY2, X2 = torch.cat([dY, dY]), torch.cat([X, X])
+    r["W_acc_K2T"] = round(2 * fl / timed(lambda: api.dbg_gemm(dY2, X2, C32, M=M, N=N, K=2 * K, a_mn=True, b_mn=True,
+                                                               epi=4, beta=1)) / 1e9, 1)
     print(json.dumps(r), flush=True)

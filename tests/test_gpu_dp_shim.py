@@ -105,3 +105,22 @@ def test_dp_grouped_tail_within_tolerance():
             if k.startswith("g"):
                 err = np.linalg.norm(ra[k] - rb[k]) / max(np.linalg.norm(rb[k]), 1e-30)
                 assert err <= 1e-3, (k, err)
+
+
+def test_bench_dp_code_path_under_the_shim():
+    """bench.py --gpus 2 --dp 2 (two replicas of a 1-stage pipeline, one process each, on
+    one GPU through the shim): the data-parallel bench path runs end to end and prints the
+    App. A ablation (numbers meaningless on one shared GPU)."""
+    import json
+    port = _port()
+    env = dict(os.environ, ZB_NCCL_LIB=SHIM, ZB_SAME_DEVICE="1", ZB_DIST_BACKEND="gloo", ZB_BENCH_WATCHDOG_S="500")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dp", "2",
+           "--steps", "2", "--warmup", "3", "--config", "tiny"]
+    q = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert q.returncode == 0, q.stdout[-3000:] + q.stderr[-3000:]
+    lines = [x for x in q.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, q.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "pp1dp2"
+    assert d["dp"]["speedup_app_a"] is not None
