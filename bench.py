@@ -358,7 +358,7 @@ def run_single(args, cfg, headline=True):
     lib.zb_dbg_launch_count(0, C.byref(nl))
     launches = int(nl.value)
     ms = ev0.elapsed_time(ev1) / args.steps
-    tokens_per_step = cfg.T * m * D          # all replicas
+    tokens_per_step = cfg.T * m
     value = tokens_per_step / (ms / 1000.0)
     loss = ctx.loss()
     # ---- the same workload again with CUDA events around every GEMM / attention / HBM-kernel

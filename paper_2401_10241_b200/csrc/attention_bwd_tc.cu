@@ -82,6 +82,13 @@ __device__ __forceinline__ void tile_row_to_tmem(const uint8_t* tile, int r, uin
   }
 }
 
+// item (level, head, sequence) of a level-major list (per = a b items per level)
+__device__ __forceinline__ void decode_item(int it, int a, int per, int& level, int& hd, int& bb) {
+  level = it / per;
+  hd = it % per % a;
+  bb = it % per / a;
+}
+
 // ================================================================== dK / dV
 template <int D> struct DkdvCfg {
   // TMEM: S^T / dP^T x 2 buffers (256 columns), dK, dV (D each), then the CTA-constant A
@@ -101,12 +108,18 @@ template <int D> struct DkdvCfg {
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 
-// (the tensor maps are references to the launching kernel's __grid_constant__ parameters)
-template <int D>
-__device__ __forceinline__ void dkdv_body(const CUtensorMap& tmKV, const CUtensorMap& tmQ, const CUtensorMap& tmDO,
-                                          const float* __restrict__ lse, const float* __restrict__ delta,
-                                          bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2,
-                                          int kb_, int hd_, int bb_) {
+// Persistent over this CTA's dK/dV items (key block kb = level, head, sequence): barriers,
+// TMEM and the Q_i / dO_i ring stay live across items, barrier parities come from running
+// counters (items `ri`, query steps `gn`).  Per item the next item's K / V load waits only
+// for the last S^T / dP^T products of the current item (kv_empty), and its first dV / dK
+// products only for the softmax warps having read the current dK / dV (o_empty), so one
+// item's epilogue overlaps the next item's first steps.  (The tensor maps are references to
+// the launching kernel's __grid_constant__ parameters.)
+template <int D, typename ItemOf>
+__device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensorMap& tmQ, const CUtensorMap& tmDO,
+                                         const float* __restrict__ lse, const float* __restrict__ delta,
+                                         bf16* __restrict__ dqkv, int s, int a, int per, float scale,
+                                         float scale_log2, uint32_t tbase, ItemOf item_of) {
   using C = DkdvCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -119,18 +132,15 @@ __device__ __forceinline__ void dkdv_body(const CUtensorMap& tmKV, const CUtenso
   uint64_t* ds_full = sp_empty + 2;            // [2]
   uint64_t* o_final = ds_full + 2;
   uint64_t* at_full = o_final + 1;  // K (V) resident in TMEM
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(at_full + 1);
   uint64_t* ds_part = bar + 16;  // [2]: the first 16 queries / keys of each half are in TMEM
-  static_assert((1 + 2 * C::ST + 8) * 8 + 4 <= 256, "barrier area");
+  uint64_t* kv_empty = bar + 18;  // the item's last S^T / dP^T products have read K / V
+  uint64_t* o_empty = bar + 19;   // the elementwise warps have read dK / dV of their item
+  constexpr int NBAR = 20;
+  static_assert((NBAR + 1) * 8 <= 256, "barrier area");
+  static_assert((1 + 2 * C::ST + 8) <= 16, "barrier layout");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kb = kb_, hd = hd_, bb = bb_;
   const int h = a * D;
-  const int i0 = 2 * kb, nq = s / 64 - i0;
-  const int row0 = bb * s;
-  const int64_t stat0 = (static_cast<int64_t>(bb) * a + hd) * s;
-
-  if (threadIdx.x == 0) TR(6, 0);
   if (threadIdx.x == 0) {
     sm100::mbar_init(kv_full, 1);
     for (int i = 0; i < C::ST; ++i) {
@@ -145,45 +155,44 @@ __device__ __forceinline__ void dkdv_body(const CUtensorMap& tmKV, const CUtenso
     }
     sm100::mbar_init(o_final, 1);
     sm100::mbar_init(at_full, 8);
+    sm100::mbar_init(kv_empty, 1);
+    sm100::mbar_init(o_empty, 8);
 #ifdef ZB_ATTN_TRACE
     sm100::mbar_init(bar + 20, 1);
 #endif
     sm100::fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) {
-    sm100::tma_prefetch(&tmKV);
-    sm100::tma_prefetch(&tmQ);
-    sm100::tma_prefetch(&tmDO);
-  }
-  if (warp == 2) sm100::tmem_alloc<512>(tslot);
-  sm100::tc_fence_before();
   __syncthreads();
-  sm100::tc_fence_after();
-  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
-  pdl_wait();
-  const uint32_t tbase = *tslot;
   const uint32_t t_dk = tbase + 256, t_dv = tbase + 256 + D;
   const uint32_t t_kt = tbase + 256 + 2 * D, t_vt = t_kt + D / 2;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA / bulk copies
-      sm100::mbar_arrive_expect_tx(kv_full, 2 * C::KV_TILE);
-      for (int at = 0; at < C::ATOMS; ++at) {
-        sm100::tma_load_2d(smem + C::OFF_K + at * 16384, &tmKV, kv_full, h + hd * D + 64 * at, row0 + kb * 128);
-        sm100::tma_load_2d(smem + C::OFF_V + at * 16384, &tmKV, kv_full, 2 * h + hd * D + 64 * at, row0 + kb * 128);
-      }
-      for (int n = 0; n < nq; ++n) {
-        const int i = i0 + n, st = n % C::ST;
-        sm100::mbar_wait(&st_empty[st], ((n / C::ST) & 1) ^ 1);
-        TR(0, n);
-        uint8_t* sg = smem + C::OFF_ST + st * C::STAGE;
-        sm100::mbar_arrive_expect_tx(&st_full[st], 2 * C::Q_TILE + 512);
+      int gn = 0;  // query steps issued (ring position)
+      for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
+        int kb, hd, bb;
+        decode_item(it, a, per, kb, hd, bb);
+        const int i0 = 2 * kb, nq = s / 64 - i0, row0 = bb * s;
+        const int64_t stat0 = (static_cast<int64_t>(bb) * a + hd) * s;
+        sm100::mbar_wait(kv_empty, (ri & 1) ^ 1);  // the previous item's S^T / dP^T are done with K / V
+        sm100::mbar_arrive_expect_tx(kv_full, 2 * C::KV_TILE);
         for (int at = 0; at < C::ATOMS; ++at) {
-          sm100::tma_load_2d(sg + at * 8192, &tmQ, &st_full[st], hd * D + 64 * at, row0 + i * 64);
-          sm100::tma_load_2d(sg + C::Q_TILE + at * 8192, &tmDO, &st_full[st], hd * D + 64 * at, row0 + i * 64);
+          sm100::tma_load_2d(smem + C::OFF_K + at * 16384, &tmKV, kv_full, h + hd * D + 64 * at, row0 + kb * 128);
+          sm100::tma_load_2d(smem + C::OFF_V + at * 16384, &tmKV, kv_full, 2 * h + hd * D + 64 * at, row0 + kb * 128);
         }
-        sm100::bulk_load(sg + 2 * C::Q_TILE, lse + stat0 + i * 64, 256, &st_full[st]);
-        sm100::bulk_load(sg + 2 * C::Q_TILE + 256, delta + stat0 + i * 64, 256, &st_full[st]);
+        for (int n = 0; n < nq; ++n, ++gn) {
+          const int i = i0 + n, st = gn % C::ST;
+          sm100::mbar_wait(&st_empty[st], ((gn / C::ST) & 1) ^ 1);
+          if (ri == 0) TR(0, n);
+          uint8_t* sg = smem + C::OFF_ST + st * C::STAGE;
+          sm100::mbar_arrive_expect_tx(&st_full[st], 2 * C::Q_TILE + 512);
+          for (int at = 0; at < C::ATOMS; ++at) {
+            sm100::tma_load_2d(sg + at * 8192, &tmQ, &st_full[st], hd * D + 64 * at, row0 + i * 64);
+            sm100::tma_load_2d(sg + C::Q_TILE + at * 8192, &tmDO, &st_full[st], hd * D + 64 * at, row0 + i * 64);
+          }
+          sm100::bulk_load(sg + 2 * C::Q_TILE, lse + stat0 + i * 64, 256, &st_full[st]);
+          sm100::bulk_load(sg + 2 * C::Q_TILE + 256, delta + stat0 + i * 64, 256, &st_full[st]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -191,200 +200,231 @@ __device__ __forceinline__ void dkdv_body(const CUtensorMap& tmKV, const CUtenso
       constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 64, false, false);
       constexpr uint32_t idesc_g = sm100::idesc_bf16(128, D, false, true);
       const uint32_t sk = sm100::smem_addr(smem + C::OFF_K), sv = sm100::smem_addr(smem + C::OFF_V);
-      auto issue_grad = [&](int n) {
-        const int b = n & 1, st = n % C::ST;
-        const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
-        const uint32_t sdo = sq + C::Q_TILE;
-        const uint32_t tp = tbase + b * 128;
-        const uint64_t dod = sm100::smem_desc(sdo, 8192, 1024, sm100::kSwizzle128B);
-        const uint64_t qd = sm100::smem_desc(sq, 8192, 1024, sm100::kSwizzle128B);
-        // K = 64 queries: halves live at columns [0,16) and [32,48); each half's first 16 queries
-        // (K-steps 0 and 2) are published before its last 16 (K-steps 1 and 3)
+      int gn = 0;  // query steps whose S^T / dP^T were issued
+      for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
+        int kb, hd, bb;
+        decode_item(it, a, per, kb, hd, bb);
+        const int nq = s / 64 - 2 * kb;
+        const int g0 = gn;  // first step of the item
+        auto issue_grad = [&](int g) {  // step g (global count) of this item
+          const int n = g - g0;
+          const int b = g & 1, st = g % C::ST;
+          const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+          const uint32_t sdo = sq + C::Q_TILE;
+          const uint32_t tp = tbase + b * 128;
+          const uint64_t dod = sm100::smem_desc(sdo, 8192, 1024, sm100::kSwizzle128B);
+          const uint64_t qd = sm100::smem_desc(sq, 8192, 1024, sm100::kSwizzle128B);
+          if (n == 0) sm100::mbar_wait_warp(o_empty, (ri & 1) ^ 1);  // dK / dV of the previous item read
+          // K = 64 queries: halves live at columns [0,16) and [32,48); each half's first 16 queries
+          // (K-steps 0 and 2) are published before its last 16 (K-steps 1 and 3)
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {
-          sm100::mbar_wait_warp(part == 0 ? &ds_part[b] : &ds_full[b], (n >> 1) & 1);
-          if (part == 1) TR(3, n);
+          for (int part = 0; part < 2; ++part) {
+            sm100::mbar_wait_warp(part == 0 ? &ds_part[b] : &ds_full[b], (g >> 1) & 1);
+            if (part == 1 && ri == 0) TR(3, n);
+            sm100::tc_fence_after();
+            if (sm100::elect_one()) {
+#pragma unroll
+              for (int kh = 0; kh < 2; ++kh) {
+                const int kk = 2 * kh + part;
+                const uint32_t acol = kh * 32 + part * 8;
+                sm100::mma_bf16_ts(t_dv, tp + acol, sm100::desc_adv(dod, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+                sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::desc_adv(qd, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+              }
+            }
+            __syncwarp();
+          }
+          if (ri == 0) TR(10, n);
+          if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
+          if (sm100::elect_one()) sm100::mma_commit(&st_empty[st]);
+#ifdef ZB_ATTN_TRACE
+          if (ri == 0) { if (sm100::elect_one()) sm100::mma_commit(bar + 20); }
+#endif
+          if (n == nq - 1) { if (sm100::elect_one()) sm100::mma_commit(o_final); }
+        };
+        sm100::mbar_wait_warp(kv_full, ri & 1);
+        if constexpr (C::KT) {
+          sm100::mbar_wait_warp(at_full, ri & 1);
           sm100::tc_fence_after();
-          if (sm100::elect_one()) {
+        }
+        for (int n = 0; n < nq; ++n, ++gn) {
+          const int b = gn & 1, st = gn % C::ST;
+          sm100::mbar_wait_warp(&st_full[st], (gn / C::ST) & 1);
+          if (ri == 0) TR(1, n);
+          sm100::mbar_wait_warp(&sp_empty[b], ((gn >> 1) & 1) ^ 1);
+          if (ri == 0) TR(2, n);
+          sm100::tc_fence_after();
+          const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+          const uint32_t sdo = sq + C::Q_TILE;
+          const uint32_t tp = tbase + b * 128;
+          const uint64_t kd = sm100::smem_desc(sk, 16, 1024, sm100::kSwizzle128B);
+          const uint64_t vd = sm100::smem_desc(sv, 16, 1024, sm100::kSwizzle128B);
+          const uint64_t qd = sm100::smem_desc(sq, 16, 1024, sm100::kSwizzle128B);
+          const uint64_t dod = sm100::smem_desc(sdo, 16, 1024, sm100::kSwizzle128B);
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {
-              const int kk = 2 * kh + part;
-              const uint32_t acol = kh * 32 + part * 8;
-              sm100::mma_bf16_ts(t_dv, tp + acol, sm100::desc_adv(dod, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
-              sm100::mma_bf16_ts(t_dk, tp + 64 + acol, sm100::desc_adv(qd, kk * 2048), idesc_g, (n | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+            if (sm100::elect_one()) {
+              if constexpr (C::KT)
+                sm100::mma_bf16_ts(tp, t_kt + kk * 8, sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
+              else
+                sm100::mma_bf16_ss(tp, sm100::desc_adv(kd, oa), sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
+              if constexpr (C::VT)
+                sm100::mma_bf16_ts(tp + 64, t_vt + kk * 8, sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
+              else
+                sm100::mma_bf16_ss(tp + 64, sm100::desc_adv(vd, oa), sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
             }
           }
-          __syncwarp();
+          if (ri == 0) TR(11, n);
+          if (sm100::elect_one()) sm100::mma_commit(&sp_full[b]);
+          if (n == nq - 1) { if (sm100::elect_one()) sm100::mma_commit(kv_empty); }  // last reads of K / V
+          if (n > 0) issue_grad(gn - 1);
         }
-        TR(10, n);
-        if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
-        if (sm100::elect_one()) sm100::mma_commit(&st_empty[st]);
-#ifdef ZB_ATTN_TRACE
-        if (sm100::elect_one()) sm100::mma_commit(bar + 20);
-#endif
-        if (n == nq - 1) { if (sm100::elect_one()) sm100::mma_commit(o_final); }
-      };
-      sm100::mbar_wait_warp(kv_full, 0);
-      if constexpr (C::KT) {
-        sm100::mbar_wait_warp(at_full, 0);
-        sm100::tc_fence_after();
+        issue_grad(gn - 1);
       }
-      for (int n = 0; n < nq; ++n) {
-        const int b = n & 1, st = n % C::ST;
-        sm100::mbar_wait_warp(&st_full[st], (n / C::ST) & 1);
-        TR(1, n);
-        sm100::mbar_wait_warp(&sp_empty[b], ((n >> 1) & 1) ^ 1);
-        TR(2, n);
-        sm100::tc_fence_after();
-        const uint32_t sq = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
-        const uint32_t sdo = sq + C::Q_TILE;
-        const uint32_t tp = tbase + b * 128;
-        const uint64_t kd = sm100::smem_desc(sk, 16, 1024, sm100::kSwizzle128B);
-        const uint64_t vd = sm100::smem_desc(sv, 16, 1024, sm100::kSwizzle128B);
-        const uint64_t qd = sm100::smem_desc(sq, 16, 1024, sm100::kSwizzle128B);
-        const uint64_t dod = sm100::smem_desc(sdo, 16, 1024, sm100::kSwizzle128B);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * 16384 + (kk & 3) * 32, ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-          if (sm100::elect_one()) {
-            if constexpr (C::KT)
-              sm100::mma_bf16_ts(tp, t_kt + kk * 8, sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
-            else
-              sm100::mma_bf16_ss(tp, sm100::desc_adv(kd, oa), sm100::desc_adv(qd, ob), idesc_s, kk != 0 ? 1u : 0u);
-            if constexpr (C::VT)
-              sm100::mma_bf16_ts(tp + 64, t_vt + kk * 8, sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
-            else
-              sm100::mma_bf16_ss(tp + 64, sm100::desc_adv(vd, oa), sm100::desc_adv(dod, ob), idesc_s, kk != 0 ? 1u : 0u);
-          }
-        }
-        TR(11, n);
-        if (sm100::elect_one()) sm100::mma_commit(&sp_full[b]);
-        if (n > 0) issue_grad(n - 1);
-      }
-      issue_grad(nq - 1);
     }
 #ifdef ZB_ATTN_TRACE
-  } else if (warp == 3) {  // trace observer: completion of each step's dV / dK products
-    if (lane == 0)
-      for (int n = 0; n < nq; ++n) {
+  } else if (warp == 3) {  // trace observer (first item): completion of each step's dV / dK products
+    const int it0 = item_of(0);
+    if (lane == 0 && it0 >= 0) {
+      int kb, hd, bb;
+      decode_item(it0, a, per, kb, hd, bb);
+      for (int n = 0; n < s / 64 - 2 * kb; ++n) {
         sm100::mbar_wait(bar + 20, n & 1);
         TR(9, n);
       }
+    }
 #endif
   } else if (warp >= 4) {  // ---------------- elementwise: P^T, dS^T
     const int qw = warp & 3, hf = (warp - 4) >> 2;
     const int r = qw * 32 + lane;
-    const int key = kb * 128 + r;
     const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
-    if constexpr (C::KT) {
-      sm100::mbar_wait(kv_full, 0);
-      if (hf == 0) tile_row_to_tmem<D>(smem + C::OFF_K, r, t_kt + lane_off);
-      if (C::VT && hf == 1) tile_row_to_tmem<D>(smem + C::OFF_V, r, t_vt + lane_off);
-      sm100::tmem_st_wait();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive_warp(at_full);
-    }
-    for (int n = 0; n < nq; ++n) {
-      const int i = i0 + n, b = n & 1, st = n % C::ST;
-      sm100::mbar_wait(&sp_full[b], (n >> 1) & 1);
-      if (warp == 4 && lane == 0) TR(4, n);
-      sm100::tc_fence_after();
-      uint32_t sr[32], dr[32];
-      const uint32_t tp = tbase + b * 128 + lane_off;
-      sm100::tmem_ld32(tp + 32 * hf, sr);
-      sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
-      sm100::tmem_ld_wait();
-      // this half's 32 L_q and D_q (warp-uniform: broadcast loads), L in log2 units
-      float nl[32], dd[32];
-      {
-        const uint32_t sl = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE + 2 * C::Q_TILE) + 128 * hf;
-#pragma unroll
-        for (int c = 0; c < 32; c += 4) {
-          const float4 l4 = sm100::lds128(sl + 4 * c), d4 = sm100::lds128(sl + 256 + 4 * c);
-          nl[c] = -l4.x * LOG2E, nl[c + 1] = -l4.y * LOG2E, nl[c + 2] = -l4.z * LOG2E, nl[c + 3] = -l4.w * LOG2E;
-          dd[c] = d4.x, dd[c + 1] = d4.y, dd[c + 2] = d4.z, dd[c + 3] = d4.w;
-        }
+    int gn = 0;
+    for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
+      int kb, hd, bb;
+      decode_item(it, a, per, kb, hd, bb);
+      const int i0 = 2 * kb, nq = s / 64 - i0, row0 = bb * s;
+      const int key = kb * 128 + r;
+      if constexpr (C::KT) {
+        sm100::mbar_wait(kv_full, ri & 1);
+        sm100::mbar_wait(kv_empty, (ri & 1) ^ 1);  // the previous item's products are done with K / V in TMEM
+        if (hf == 0) tile_row_to_tmem<D>(smem + C::OFF_K, r, t_kt + lane_off);
+        if (C::VT && hf == 1) tile_row_to_tmem<D>(smem + C::OFF_V, r, t_vt + lane_off);
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive_warp(at_full);
       }
-      if (warp == 4 && lane == 0) TR(7, n);
-      // queries of this half: i*64 + 32 hf + c; the causal mask (q >= key) only bites on blocks
-      // that reach below the diagonal of this key block
-      const int qlo = i * 64 + 32 * hf;
-      const bool diag = qlo < kb * 128 + 128;
-      uint32_t pk[16], dk[16];
-      // the mask test only on the (warp-uniform) diagonal steps: off the diagonal the
-      // compare / select / index arithmetic was a third of the loop's instructions
-      auto elementwise = [&](auto masked, int c0) {
+      for (int n = 0; n < nq; ++n, ++gn) {
+        const int i = i0 + n, b = gn & 1, st = gn % C::ST;
+        sm100::mbar_wait(&sp_full[b], (gn >> 1) & 1);
+        if (warp == 4 && lane == 0 && ri == 0) TR(4, n);
+        sm100::tc_fence_after();
+        uint32_t sr[32], dr[32];
+        const uint32_t tp = tbase + b * 128 + lane_off;
+        sm100::tmem_ld32(tp + 32 * hf, sr);
+        sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
+        sm100::tmem_ld_wait();
+        // this half's 32 L_q and D_q (warp-uniform: broadcast loads), L in log2 units
+        float nl[32], dd[32];
+        {
+          const uint32_t sl = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE + 2 * C::Q_TILE) + 128 * hf;
 #pragma unroll
-        for (int c = c0; c < c0 + 16; c += 2) {
-          float pv[2], dv[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, nl[c + e]));
-            if constexpr (decltype(masked)::value)
-              if (qlo + c + e < key) p = 0.f;
-            pv[e] = p;
-            dv[e] = p * (__uint_as_float(dr[c + e]) - dd[c + e]);
+          for (int c = 0; c < 32; c += 4) {
+            const float4 l4 = sm100::lds128(sl + 4 * c), d4 = sm100::lds128(sl + 256 + 4 * c);
+            nl[c] = -l4.x * LOG2E, nl[c + 1] = -l4.y * LOG2E, nl[c + 2] = -l4.z * LOG2E, nl[c + 3] = -l4.w * LOG2E;
+            dd[c] = d4.x, dd[c + 1] = d4.y, dd[c + 2] = d4.z, dd[c + 3] = d4.w;
           }
-          pk[c >> 1] = pack_bf16(pv[0], pv[1]);
-          dk[c >> 1] = pack_bf16(dv[0], dv[1]);
         }
-      };
-      // two parts of 16 queries: the grad products of the first overlap the second's exponentials
+        if (warp == 4 && lane == 0 && ri == 0) TR(7, n);
+        // queries of this half: i*64 + 32 hf + c; the causal mask (q >= key) only bites on blocks
+        // that reach below the diagonal of this key block
+        const int qlo = i * 64 + 32 * hf;
+        const bool diag = qlo < kb * 128 + 128;
+        uint32_t pk[16], dk[16];
+        // the mask test only on the (warp-uniform) diagonal steps: off the diagonal the
+        // compare / select / index arithmetic was a third of the loop's instructions
+        auto elementwise = [&](auto masked, int c0) {
 #pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        if (diag)
-          elementwise(std::true_type{}, 16 * part);
-        else
-          elementwise(std::false_type{}, 16 * part);
-        sm100::tmem_st8(tp + 32 * hf + 8 * part, pk + 8 * part);       // P^T over this half's S^T columns
-        sm100::tmem_st8(tp + 64 + 32 * hf + 8 * part, dk + 8 * part);  // dS^T over this half's dP^T columns
-        if (part == 0) {
-          sm100::tmem_st_wait();
-          sm100::tc_fence_before();
-          sm100::mbar_arrive_warp(&ds_part[b]);
+          for (int c = c0; c < c0 + 16; c += 2) {
+            float pv[2], dv[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, nl[c + e]));
+              if constexpr (decltype(masked)::value)
+                if (qlo + c + e < key) p = 0.f;
+              pv[e] = p;
+              dv[e] = p * (__uint_as_float(dr[c + e]) - dd[c + e]);
+            }
+            pk[c >> 1] = pack_bf16(pv[0], pv[1]);
+            dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+          }
+        };
+        // two parts of 16 queries: the grad products of the first overlap the second's exponentials
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          if (diag)
+            elementwise(std::true_type{}, 16 * part);
+          else
+            elementwise(std::false_type{}, 16 * part);
+          sm100::tmem_st8(tp + 32 * hf + 8 * part, pk + 8 * part);       // P^T over this half's S^T columns
+          sm100::tmem_st8(tp + 64 + 32 * hf + 8 * part, dk + 8 * part);  // dS^T over this half's dP^T columns
+          if (part == 0) {
+            sm100::tmem_st_wait();
+            sm100::tc_fence_before();
+            sm100::mbar_arrive_warp(&ds_part[b]);
+          }
         }
+        if (warp == 4 && lane == 0 && ri == 0) TR(8, n);
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        if (warp == 4 && lane == 0 && ri == 0) TR(5, n);
+        sm100::mbar_arrive_warp(&ds_full[b]);
       }
-      if (warp == 4 && lane == 0) TR(8, n);
-      sm100::tmem_st_wait();
-      sm100::tc_fence_before();
-      if (warp == 4 && lane == 0) TR(5, n);
-      sm100::mbar_arrive_warp(&ds_full[b]);
-    }
-    sm100::mbar_wait(o_final, 0);
-    if (warp == 4 && lane == 0) TR(6, 1);
-    sm100::tc_fence_after();
-    bf16* row = dqkv + (static_cast<int64_t>(row0) + key) * (3 * h) + hd * D;
+      sm100::mbar_wait(o_final, ri & 1);
+      if (warp == 4 && lane == 0 && ri == 0) TR(6, 1);
+      sm100::tc_fence_after();
+      bf16* row = dqkv + (static_cast<int64_t>(row0) + key) * (3 * h) + hd * D;
 #pragma unroll 1
-    for (int c = hf; c < D / 32; c += 2) {
-      uint32_t v[32];
-      sm100::tmem_ld32(t_dk + lane_off + c * 32, v);
-      sm100::tmem_ld_wait();
+      for (int c = hf; c < D / 32; c += 2) {
+        uint32_t v[32];
+        sm100::tmem_ld32(t_dk + lane_off + c * 32, v);
+        sm100::tmem_ld_wait();
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        uint4 u;
-        u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
-        u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
-        u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
-        u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
-        *reinterpret_cast<uint4*>(row + h + c * 32 + g * 8) = u;
-      }
-      sm100::tmem_ld32(t_dv + lane_off + c * 32, v);
-      sm100::tmem_ld_wait();
+        for (int g = 0; g < 4; ++g) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
+          u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
+          u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
+          u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
+          *reinterpret_cast<uint4*>(row + h + c * 32 + g * 8) = u;
+        }
+        sm100::tmem_ld32(t_dv + lane_off + c * 32, v);
+        sm100::tmem_ld_wait();
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        uint4 u;
-        u.x = pack_bf16(__uint_as_float(v[8 * g]), __uint_as_float(v[8 * g + 1]));
-        u.y = pack_bf16(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
-        u.z = pack_bf16(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
-        u.w = pack_bf16(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
-        *reinterpret_cast<uint4*>(row + 2 * h + c * 32 + g * 8) = u;
+        for (int g = 0; g < 4; ++g) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(v[8 * g]), __uint_as_float(v[8 * g + 1]));
+          u.y = pack_bf16(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
+          u.z = pack_bf16(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
+          u.w = pack_bf16(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
+          *reinterpret_cast<uint4*>(row + 2 * h + c * 32 + g * 8) = u;
+        }
       }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive_warp(o_empty);  // dK / dV may be overwritten by the next item
     }
   }
+  // every role is done (all commits observed by their waiters): the barrier memory may be reused
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  if (warp == 2) sm100::tmem_dealloc<512>(tbase);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NBAR; ++i)
+      if (i != 15) sm100::mbar_inval(bar + i);  // 15: unused
+#ifdef ZB_ATTN_TRACE
+    sm100::mbar_inval(bar + 20);
+#endif
+  }
+  __syncthreads();
 }
 
 // ================================================================== dQ
@@ -399,11 +439,16 @@ template <int D> struct DqCfg {
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
 
-template <int D>
-__device__ __forceinline__ void dq_body(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const CUtensorMap& tmDO,
-                                        const float* __restrict__ lse, const float* __restrict__ delta,
-                                        bf16* __restrict__ dqkv, int s, int a, float scale, float scale_log2, int level,
-                                        int hd_, int bb_) {
+// Persistent over this CTA's dQ items (query block nqb-1-level, head, sequence); running
+// counters as in dkdv_run.  Q / dO of an item are only read by their copies into TMEM (the
+// products are TS), so the next item's Q / dO load waits for those copies (at_full), the next
+// copies for the current item's last S / dP products (qt_empty), and the next item's first dQ
+// product for the current dQ having been read (o_empty).
+template <int D, typename ItemOf>
+__device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const CUtensorMap& tmDO,
+                                       const float* __restrict__ lse, const float* __restrict__ delta,
+                                       bf16* __restrict__ dqkv, int s, int a, int per, float scale, float scale_log2,
+                                       uint32_t tbase, ItemOf item_of) {
   using C = DqCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -416,19 +461,16 @@ __device__ __forceinline__ void dq_body(const CUtensorMap& tmQ, const CUtensorMa
   uint64_t* ds_full = sp_empty + 2;            // [2]
   uint64_t* o_final = ds_full + 2;
   uint64_t* at_full = o_final + 1;  // Q, dO resident in TMEM
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(at_full + 1);
   uint64_t* ds_part = bar + 16;  // [2]: the first 16 queries / keys of each half are in TMEM
-  static_assert((1 + 2 * C::ST + 8) * 8 + 4 <= 256, "barrier area");
+  uint64_t* qt_empty = bar + 18;  // the item's last S / dP products have read Q / dO in TMEM
+  uint64_t* o_empty = bar + 19;   // the elementwise warps have read dQ of their item
+  constexpr int NBAR = 20;
+  static_assert((NBAR + 1) * 8 <= 256, "barrier area");
   static_assert(256 + 2 * D <= 512, "TMEM: S/dP x 2, dQ, Q and dO as packed bf16");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = s / 128;
-  const int qb = nqb - 1 - level;
-  const int hd = hd_, bb = bb_;
   const int h = a * D;
-  const int nkv = 2 * qb + 2;
-  const int row0 = bb * s;
-
   if (threadIdx.x == 0) {
     sm100::mbar_init(q_full, 1);
     for (int i = 0; i < C::ST; ++i) {
@@ -443,39 +485,37 @@ __device__ __forceinline__ void dq_body(const CUtensorMap& tmQ, const CUtensorMa
     }
     sm100::mbar_init(o_final, 1);
     sm100::mbar_init(at_full, 8);
+    sm100::mbar_init(qt_empty, 1);
+    sm100::mbar_init(o_empty, 8);
     sm100::fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) {
-    sm100::tma_prefetch(&tmQ);
-    sm100::tma_prefetch(&tmKV);
-    sm100::tma_prefetch(&tmDO);
-  }
-  if (warp == 2) sm100::tmem_alloc<512>(tslot);
-  sm100::tc_fence_before();
   __syncthreads();
-  sm100::tc_fence_after();
-  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
-  pdl_wait();
-  const uint32_t tbase = *tslot;
   const uint32_t t_dq = tbase + 256;
   const uint32_t t_qt = tbase + 256 + D, t_dot = t_qt + D / 2;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA
-      sm100::mbar_arrive_expect_tx(q_full, 2 * C::Q_TILE);
-      for (int at = 0; at < C::ATOMS; ++at) {
-        sm100::tma_load_2d(smem + C::OFF_Q + at * 16384, &tmQ, q_full, hd * D + 64 * at, row0 + qb * 128);
-        sm100::tma_load_2d(smem + C::OFF_DO + at * 16384, &tmDO, q_full, hd * D + 64 * at, row0 + qb * 128);
-      }
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j % C::ST;
-        sm100::mbar_wait(&st_empty[st], ((j / C::ST) & 1) ^ 1);
-        uint8_t* sg = smem + C::OFF_ST + st * C::STAGE;
-        sm100::mbar_arrive_expect_tx(&st_full[st], 2 * C::KV_TILE);
+      int gj = 0;  // key steps issued (ring position)
+      for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
+        int level, hd, bb;
+        decode_item(it, a, per, level, hd, bb);
+        const int qb = nqb - 1 - level, nkv = 2 * qb + 2, row0 = bb * s;
+        sm100::mbar_wait(at_full, (ri & 1) ^ 1);  // the previous item's Q / dO were copied into TMEM
+        sm100::mbar_arrive_expect_tx(q_full, 2 * C::Q_TILE);
         for (int at = 0; at < C::ATOMS; ++at) {
-          sm100::tma_load_2d(sg + at * 8192, &tmKV, &st_full[st], h + hd * D + 64 * at, row0 + j * 64);
-          sm100::tma_load_2d(sg + C::KV_TILE + at * 8192, &tmKV, &st_full[st], 2 * h + hd * D + 64 * at,
-                             row0 + j * 64);
+          sm100::tma_load_2d(smem + C::OFF_Q + at * 16384, &tmQ, q_full, hd * D + 64 * at, row0 + qb * 128);
+          sm100::tma_load_2d(smem + C::OFF_DO + at * 16384, &tmDO, q_full, hd * D + 64 * at, row0 + qb * 128);
+        }
+        for (int j = 0; j < nkv; ++j, ++gj) {
+          const int st = gj % C::ST;
+          sm100::mbar_wait(&st_empty[st], ((gj / C::ST) & 1) ^ 1);
+          uint8_t* sg = smem + C::OFF_ST + st * C::STAGE;
+          sm100::mbar_arrive_expect_tx(&st_full[st], 2 * C::KV_TILE);
+          for (int at = 0; at < C::ATOMS; ++at) {
+            sm100::tma_load_2d(sg + at * 8192, &tmKV, &st_full[st], h + hd * D + 64 * at, row0 + j * 64);
+            sm100::tma_load_2d(sg + C::KV_TILE + at * 8192, &tmKV, &st_full[st], 2 * h + hd * D + 64 * at,
+                               row0 + j * 64);
+          }
         }
       }
     }
@@ -483,138 +523,161 @@ __device__ __forceinline__ void dq_body(const CUtensorMap& tmQ, const CUtensorMa
     {  // ---------------- MMA
       constexpr uint32_t idesc_s = sm100::idesc_bf16(128, 64, false, false);
       constexpr uint32_t idesc_g = sm100::idesc_bf16(128, D, false, true);
-      auto issue_dq = [&](int j) {
-        const int b = j & 1, st = j % C::ST;
-        const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
-        const uint32_t tp = tbase + b * 128;
-        const uint64_t kjd = sm100::smem_desc(skj, 8192, 1024, sm100::kSwizzle128B);
+      int gj = 0;
+      for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
+        int level, hd, bb;
+        decode_item(it, a, per, level, hd, bb);
+        const int nkv = 2 * (nqb - 1 - level) + 2;
+        const int g0 = gj;
+        auto issue_dq = [&](int g) {
+          const int j = g - g0;
+          const int b = g & 1, st = g % C::ST;
+          const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+          const uint32_t tp = tbase + b * 128;
+          const uint64_t kjd = sm100::smem_desc(skj, 8192, 1024, sm100::kSwizzle128B);
+          if (j == 0) sm100::mbar_wait_warp(o_empty, (ri & 1) ^ 1);  // dQ of the previous item read
 #pragma unroll
-        for (int part = 0; part < 2; ++part) {  // see the dK / dV kernel
-          sm100::mbar_wait_warp(part == 0 ? &ds_part[b] : &ds_full[b], (j >> 1) & 1);
+          for (int part = 0; part < 2; ++part) {  // see dkdv_run
+            sm100::mbar_wait_warp(part == 0 ? &ds_part[b] : &ds_full[b], (g >> 1) & 1);
+            sm100::tc_fence_after();
+            if (sm100::elect_one()) {
+#pragma unroll
+              for (int kh = 0; kh < 2; ++kh) {
+                const int kk = 2 * kh + part;
+                sm100::mma_bf16_ts(t_dq, tp + kh * 32 + part * 8, sm100::desc_adv(kjd, kk * 2048), idesc_g,
+                                   (j | kk) != 0 ? 1u : 0u);
+              }
+            }
+            __syncwarp();
+          }
+          if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
+          if (sm100::elect_one()) sm100::mma_commit(&st_empty[st]);
+          if (j == nkv - 1) { if (sm100::elect_one()) sm100::mma_commit(o_final); }
+        };
+        sm100::mbar_wait_warp(at_full, ri & 1);
+        sm100::tc_fence_after();
+        for (int j = 0; j < nkv; ++j, ++gj) {
+          const int b = gj & 1, st = gj % C::ST;
+          sm100::mbar_wait_warp(&st_full[st], (gj / C::ST) & 1);
+          sm100::mbar_wait_warp(&sp_empty[b], ((gj >> 1) & 1) ^ 1);
           sm100::tc_fence_after();
-          if (sm100::elect_one()) {
+          const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
+          const uint32_t svj = skj + C::KV_TILE;
+          const uint32_t tp = tbase + b * 128;
+          const uint64_t kjd = sm100::smem_desc(skj, 16, 1024, sm100::kSwizzle128B);
+          const uint64_t vjd = sm100::smem_desc(svj, 16, 1024, sm100::kSwizzle128B);
 #pragma unroll
-            for (int kh = 0; kh < 2; ++kh) {
-              const int kk = 2 * kh + part;
-              sm100::mma_bf16_ts(t_dq, tp + kh * 32 + part * 8, sm100::desc_adv(kjd, kk * 2048), idesc_g,
-                                 (j | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
+            if (sm100::elect_one()) {
+              sm100::mma_bf16_ts(tp, t_qt + kk * 8, sm100::desc_adv(kjd, ob), idesc_s, kk != 0 ? 1u : 0u);
+              sm100::mma_bf16_ts(tp + 64, t_dot + kk * 8, sm100::desc_adv(vjd, ob), idesc_s, kk != 0 ? 1u : 0u);
             }
           }
-          __syncwarp();
+          if (sm100::elect_one()) sm100::mma_commit(&sp_full[b]);
+          if (j == nkv - 1) { if (sm100::elect_one()) sm100::mma_commit(qt_empty); }  // last reads of Q / dO
+          if (j > 0) issue_dq(gj - 1);
         }
-        if (sm100::elect_one()) sm100::mma_commit(&sp_empty[b]);
-        if (sm100::elect_one()) sm100::mma_commit(&st_empty[st]);
-        if (j == nkv - 1) { if (sm100::elect_one()) sm100::mma_commit(o_final); }
-      };
-      sm100::mbar_wait_warp(at_full, 0);
-      sm100::tc_fence_after();
-      for (int j = 0; j < nkv; ++j) {
-        const int b = j & 1, st = j % C::ST;
-        sm100::mbar_wait_warp(&st_full[st], (j / C::ST) & 1);
-        sm100::mbar_wait_warp(&sp_empty[b], ((j >> 1) & 1) ^ 1);
-        sm100::tc_fence_after();
-        const uint32_t skj = sm100::smem_addr(smem + C::OFF_ST + st * C::STAGE);
-        const uint32_t svj = skj + C::KV_TILE;
-        const uint32_t tp = tbase + b * 128;
-        const uint64_t kjd = sm100::smem_desc(skj, 16, 1024, sm100::kSwizzle128B);
-        const uint64_t vjd = sm100::smem_desc(svj, 16, 1024, sm100::kSwizzle128B);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t ob = (kk >> 2) * 8192 + (kk & 3) * 32;
-          if (sm100::elect_one()) {
-            sm100::mma_bf16_ts(tp, t_qt + kk * 8, sm100::desc_adv(kjd, ob), idesc_s, kk != 0 ? 1u : 0u);
-            sm100::mma_bf16_ts(tp + 64, t_dot + kk * 8, sm100::desc_adv(vjd, ob), idesc_s, kk != 0 ? 1u : 0u);
-          }
-        }
-        if (sm100::elect_one()) sm100::mma_commit(&sp_full[b]);
-        if (j > 0) issue_dq(j - 1);
+        issue_dq(gj - 1);
       }
-      issue_dq(nkv - 1);
     }
   } else if (warp >= 4) {  // ---------------- elementwise: dS
     const int qw = warp & 3, hf = (warp - 4) >> 2;
     const int r = qw * 32 + lane;
-    const int q = qb * 128 + r;
-    const int64_t si = (static_cast<int64_t>(bb) * a + hd) * s + q;
-    const float L2 = lse[si] * LOG2E, Dq = delta[si];
     const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
-    sm100::mbar_wait(q_full, 0);
-    tile_row_to_tmem<D>(smem + (hf == 0 ? C::OFF_Q : C::OFF_DO), r, (hf == 0 ? t_qt : t_dot) + lane_off);
-    sm100::tmem_st_wait();
-    sm100::tc_fence_before();
-    sm100::mbar_arrive_warp(at_full);
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1;
-      sm100::mbar_wait(&sp_full[b], (j >> 1) & 1);
-      sm100::tc_fence_after();
-      uint32_t sr[32], dr[32];
-      const uint32_t tp = tbase + b * 128 + lane_off;
-      sm100::tmem_ld32(tp + 32 * hf, sr);
-      sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
-      sm100::tmem_ld_wait();
-      uint32_t dk[16];
-      const int klo = j * 64 + 32 * hf;
-      auto elementwise = [&](auto masked, int c0) {
-#pragma unroll
-        for (int c = c0; c < c0 + 16; c += 2) {
-          float dv[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, -L2));
-            if constexpr (decltype(masked)::value)
-              if (klo + c + e > q) p = 0.f;
-            dv[e] = p * (__uint_as_float(dr[c + e]) - Dq);
-          }
-          dk[c >> 1] = pack_bf16(dv[0], dv[1]);
-        }
-      };
-      // keys of this half reach above the warp's first query only near the diagonal
-#pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        if (klo + 31 > qb * 128 + qw * 32)
-          elementwise(std::true_type{}, 16 * part);
-        else
-          elementwise(std::false_type{}, 16 * part);
-        sm100::tmem_st8(tp + 32 * hf + 8 * part, dk + 8 * part);  // dS over this half's S columns
-        if (part == 0) {
-          sm100::tmem_st_wait();
-          sm100::tc_fence_before();
-          sm100::mbar_arrive_warp(&ds_part[b]);
-        }
-      }
+    int gj = 0;
+    for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
+      int level, hd, bb;
+      decode_item(it, a, per, level, hd, bb);
+      const int qb = nqb - 1 - level, nkv = 2 * qb + 2;
+      const int q = qb * 128 + r;
+      const int64_t si = (static_cast<int64_t>(bb) * a + hd) * s + q;
+      const float L2 = lse[si] * LOG2E, Dq = delta[si];
+      sm100::mbar_wait(q_full, ri & 1);
+      sm100::mbar_wait(qt_empty, (ri & 1) ^ 1);  // the previous item's products are done with Q / dO in TMEM
+      tile_row_to_tmem<D>(smem + (hf == 0 ? C::OFF_Q : C::OFF_DO), r, (hf == 0 ? t_qt : t_dot) + lane_off);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
-      sm100::mbar_arrive_warp(&ds_full[b]);
-    }
-    sm100::mbar_wait(o_final, 0);
-    sm100::tc_fence_after();
-    bf16* row = dqkv + (static_cast<int64_t>(row0) + q) * (3 * h) + hd * D;
-#pragma unroll 1
-    for (int c = hf; c < D / 32; c += 2) {
-      uint32_t v[32];
-      sm100::tmem_ld32(t_dq + lane_off + c * 32, v);
-      sm100::tmem_ld_wait();
+      sm100::mbar_arrive_warp(at_full);
+      for (int j = 0; j < nkv; ++j, ++gj) {
+        const int b = gj & 1;
+        sm100::mbar_wait(&sp_full[b], (gj >> 1) & 1);
+        sm100::tc_fence_after();
+        uint32_t sr[32], dr[32];
+        const uint32_t tp = tbase + b * 128 + lane_off;
+        sm100::tmem_ld32(tp + 32 * hf, sr);
+        sm100::tmem_ld32(tp + 64 + 32 * hf, dr);
+        sm100::tmem_ld_wait();
+        uint32_t dk[16];
+        const int klo = j * 64 + 32 * hf;
+        auto elementwise = [&](auto masked, int c0) {
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        uint4 u;
-        u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
-        u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
-        u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
-        u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
-        *reinterpret_cast<uint4*>(row + c * 32 + g * 8) = u;
+          for (int c = c0; c < c0 + 16; c += 2) {
+            float dv[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              float p = sm100::ex2(fmaf(__uint_as_float(sr[c + e]), scale_log2, -L2));
+              if constexpr (decltype(masked)::value)
+                if (klo + c + e > q) p = 0.f;
+              dv[e] = p * (__uint_as_float(dr[c + e]) - Dq);
+            }
+            dk[c >> 1] = pack_bf16(dv[0], dv[1]);
+          }
+        };
+        // keys of this half reach above the warp's first query only near the diagonal
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          if (klo + 31 > qb * 128 + qw * 32)
+            elementwise(std::true_type{}, 16 * part);
+          else
+            elementwise(std::false_type{}, 16 * part);
+          sm100::tmem_st8(tp + 32 * hf + 8 * part, dk + 8 * part);  // dS over this half's S columns
+          if (part == 0) {
+            sm100::tmem_st_wait();
+            sm100::tc_fence_before();
+            sm100::mbar_arrive_warp(&ds_part[b]);
+          }
+        }
+        sm100::tmem_st_wait();
+        sm100::tc_fence_before();
+        sm100::mbar_arrive_warp(&ds_full[b]);
       }
+      sm100::mbar_wait(o_final, ri & 1);
+      sm100::tc_fence_after();
+      bf16* row = dqkv + (static_cast<int64_t>(bb) * s + q) * (3 * h) + hd * D;
+#pragma unroll 1
+      for (int c = hf; c < D / 32; c += 2) {
+        uint32_t v[32];
+        sm100::tmem_ld32(t_dq + lane_off + c * 32, v);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint4 u;
+          u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
+          u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
+          u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
+          u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
+          *reinterpret_cast<uint4*>(row + c * 32 + g * 8) = u;
+        }
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive_warp(o_empty);  // dQ may be overwritten by the next item
     }
   }
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
-  if (warp == 2) sm100::tmem_dealloc<512>(tbase);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NBAR; ++i)
+      if (i != 15) sm100::mbar_inval(bar + i);  // 15: unused
+  __syncthreads();
 }
 
-// One launch for both halves of the backward: CTA i takes work level i / (2 a b) (heaviest
-// first: dK/dV key block `level`, dQ query block nqb-1-level, both with the same step count
-// s/64 - 2 level ... 2 level + 2) and, within it, the dK/dV CTAs of every (head, sequence)
-// before the dQ ones.  The two kernels' partial last waves become one.
+// One persistent launch for both halves of the backward.  Items: the dK/dV items of every
+// level, heaviest (level 0) first, then the dQ items likewise; CTA c of G takes the items
+// r G + c (even rounds r) and r G + G-1-c (odd rounds) — its dK/dV items come first, then its
+// dQ items, so a CTA switches body (barrier layout) at most once.  TMEM (512 columns) is
+// allocated once for the CTA.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap kv128, const __grid_constant__ CUtensorMap kv64,
@@ -629,15 +692,40 @@ __global__ void __launch_bounds__(384, 1)
     g_cta_bwd[blockIdx.x][1] = gtime_b();
   }
 #endif
-  const int per = a * b;
-  const int level = static_cast<int>(blockIdx.x) / (2 * per);
-  int r = static_cast<int>(blockIdx.x) % (2 * per);
-  if (r < per)
-    dkdv_body<D>(kv128, kv64, do64, lse, delta, dqkv, s, a, scale, scale_log2, level, r % a, r / a);
-  else {
-    r -= per;
-    dq_body<D>(kv128, kv64, do128, lse, delta, dqkv, s, a, scale, scale_log2, level, r % a, r / a);
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0 && (threadIdx.x & 31) == 0) {
+    sm100::tma_prefetch(&kv128);
+    sm100::tma_prefetch(&kv64);
+    sm100::tma_prefetch(&do64);
+    sm100::tma_prefetch(&do128);
   }
+  if (warp == 2) sm100::tmem_alloc<512>(&tslot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  pdl_trigger();  // after the TMEM allocation (see launch() in common.cuh)
+  pdl_wait();
+  const uint32_t tbase = tslot;
+  const int per = a * b;
+  const int n_items = s / 128 * per;  // per half (dK/dV or dQ)
+  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  auto nth = [&](int r) {  // r-th item of this CTA in the combined list, or -1
+    const int it = r * G + ((r & 1) ? G - 1 - c : c);
+    return it < 2 * n_items ? it : -1;
+  };
+  int r_q = 0;  // first round whose item is a dQ item
+  while (nth(r_q) >= 0 && nth(r_q) < n_items) ++r_q;
+  dkdv_run<D>(kv128, kv64, do64, lse, delta, dqkv, s, a, per, scale, scale_log2, tbase,
+              [&](int r) { return r < r_q ? nth(r) : -1; });
+  dq_run<D>(kv128, kv64, do128, lse, delta, dqkv, s, a, per, scale, scale_log2, tbase, [&](int r) {
+    const int it = nth(r_q + r);
+    return it >= 0 ? it - n_items : -1;
+  });
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  if (warp == 2) sm100::tmem_dealloc<512>(tbase);
 #ifdef ZB_ATTN_TRACE
   if (threadIdx.x == 64 && blockIdx.x < 16384) g_cta_bwd[blockIdx.x][2] = gtime_b();
 #endif
@@ -662,7 +750,8 @@ static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout
   const CUtensorMap do64 = make_tmap(dout, h, rows, h, 64, 64);
   const CUtensorMap do128 = make_tmap(dout, h, rows, h, 64, 128);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
-  const int grid = 2 * (sh.s / 128) * sh.a * sh.b;
+  const int items = 2 * (sh.s / 128) * sh.a * sh.b;
+  const int grid = items < num_sms() ? items : num_sms();  // persistent: one CTA per SM
   launch(PDL_ATTN, attn_bwd_tc::k_bwd_tc<D>, grid, 384, SMEM, st, kv128, kv64, do64, do128, lse, delta,
          static_cast<bf16*>(dqkv), sh.s, sh.a, sh.b, scale, scale * attn_bwd_tc::LOG2E);
   ZB_LAUNCH_CHECK();

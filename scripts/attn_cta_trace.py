@@ -1,8 +1,9 @@
 """Per-CTA timeline of the attention kernels from the ZB_ATTN_TRACE build (libzb_trace.so):
 every CTA's SM, start and end (globaltimer).  Reports the kernel span, per-SM busy time
-(sum of its CTAs' durations) and gaps between consecutive CTAs on an SM, and a fit of CTA
-duration = c0 + c1 * work (work = 128x128 blocks for the forward, 64-row steps for the
-backward) — c0 is the fixed per-CTA cost (prologue, fill, drain, epilogue)."""
+(sum of its CTAs' durations) and gaps between consecutive CTAs on an SM, and (for grids of
+one CTA per work item, as in the first round-2 measurement) a fit of CTA duration =
+c0 + c1 * work — c0 the fixed per-CTA cost (prologue, fill, drain, epilogue).  Both kernels
+are persistent now (one CTA per SM): the busy / span figures are the meaningful ones."""
 import ctypes as C, json, os, sys
 os.environ["ZB_LIB"] = "libzb_trace.so"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -55,8 +56,7 @@ analyse("fwd (persistent)", buf, nf, np.ones(nf))
 for _ in range(3):
     api.dbg_attention_bwd(qkv, o, do, lse, dq, dl, b=b, s=s, a=a, d=d)
 torch.cuda.synchronize()
-nb = 2 * (s // 128) * a * b
+nb = min(2 * (s // 128) * a * b, torch.cuda.get_device_properties(0).multi_processor_count)  # persistent too
 buf = (C.c_ulonglong * (16384 * 3))()
 lib.zb_dbg_attn_bwd_cta_trace(buf)
-workb = np.array([s // 64 - 2 * (i // (2 * per)) for i in range(nb)], dtype=np.float64)  # 64-row steps
-analyse("bwd", buf, nb, workb)
+analyse("bwd (persistent)", buf, nb, np.ones(nb))
