@@ -396,7 +396,7 @@ template <int BN> struct Cfg2 {
   static constexpr int EPI_OFF = STAGES * STAGE;
   static constexpr int BAR_OFF = EPI_OFF + kEpiWarps * kStageBytes;
   static constexpr int CS_OFF = BAR_OFF + 512;  // column-sum combine buffer (16 x 8 floats)
-  static constexpr int SMEM = BAR_OFF + 1024 + 512 + 512;
+  static constexpr int SMEM = BAR_OFF + 1024 + 512 + 512 + 16;  // + the column sums' last-arrival flag
 };
 
 // Column sums of the A operand (W's bias gradient, A = dY MN-major) by warps 2-3 of each
@@ -408,8 +408,8 @@ template <int BN> struct Cfg2 {
 // (tile nt reads k-blocks kb = nt mod num_n), so every tile delays only ~1/num_n of its
 // stages: for those the leader's MMA commit lands on mdone, the warps read the stage and
 // release it to the producer (empty); the other stages go straight back.  Each tile writes
-// its partial sums (zeros if it read nothing); k_bias_finalize adds the (split, n-tile)
-// partials in a fixed order (deterministic).
+// its partial sums (zeros if it read nothing); the tile completing a 128-row block adds the
+// block's (split, n-tile) partials in a fixed order (deterministic, no second launch).
 __device__ __forceinline__ void colsum_stage(const uint8_t* sa, int t, float* acc) {
   const int c = t & 15, g = t >> 4;
   // shared-window address: a generic pointer after the alignment arithmetic would compile to LD.E
@@ -627,12 +627,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           acc[i] += o;
         }
         const int m = mt * BM2 + static_cast<int>(rank) * BM + (lane >> 3) * 64 + (lane & 7) * 8;
-        float* dst = ep.bias_part + static_cast<int64_t>(sp * num_n + nt) * M;  // summed by k_bias_finalize
+        float* dst = ep.bias_part + static_cast<int64_t>(sp * num_n + nt) * M;
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           if (m + i < M) dst[m + i] = acc[i];
+        __threadfence();  // the partial is visible before this tile's arrival is counted
       }
-      asm volatile("bar.sync 1, 64;" ::: "memory");  // xbuf is reused by the next tile
+      // the tile whose partial completes its 128-row block (all splits x n-tiles arrived) sums
+      // the block's partials in (split, n-tile) order — the order of the former separate
+      // finalize kernel, so the bias gradient is bitwise the same whichever CTA finishes last
+      uint32_t* last = reinterpret_cast<uint32_t*>(smem + C::CS_OFF + 512);
+      asm volatile("bar.sync 1, 64;" ::: "memory");  // xbuf is reused by the next tile; partial written
+      const int blk = mt * 2 + static_cast<int>(rank);
+      const int parts = splits * num_n;
+      if (t == 0) *last = atomicAdd(&ep.bias_tickets[blk], 1) == parts - 1 ? 1u : 0u;
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+      if (*last) {
+        __threadfence();
+        const int mb = mt * BM2 + static_cast<int>(rank) * BM;
+#pragma unroll
+        for (int hrow = 0; hrow < 2; ++hrow) {
+          const int m = mb + hrow * 64 + t;
+          if (m < M) {
+            float v = __ldcg(ep.bias_part + m);
+            for (int q = 1; q < parts; ++q) v += __ldcg(ep.bias_part + static_cast<int64_t>(q) * M + m);
+            ep.bias_out[m] = ep.beta ? ep.bias_out[m] + v : v;
+          }
+        }
+        if (t == 0) ep.bias_tickets[blk] = 0;  // ready for the next launch on this stream
+      }
     }
   } else if (warp >= 4) {  // ---------------- epilogue (both CTAs, own 128 rows)
     const int ew = (warp - 4) & 3, half = (warp - 4) >> 2;  // see the 1-CTA kernel
@@ -833,6 +856,8 @@ struct SplitFlags {
   int32_t base = 0;
   float* part = nullptr;  // bias partial sums [splits * n-tiles, M] (column-sum W GEMMs)
   size_t part_cap = 0;
+  int32_t* tick = nullptr;  // per-128-row-block arrival counters of the column sums
+  int tick_cap = 0;
 };
 static std::mutex g_split_mu;
 static std::map<cudaStream_t, SplitFlags> g_split_bufs;
@@ -881,9 +906,19 @@ static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs&
 
 // per-split bias partials of a column-sum W GEMM (stream-private, grown on demand; the
 // previous user on the same stream has finished before the next GEMM reads / writes it)
-static float* bias_partials(cudaStream_t st, size_t n) {
+static float* bias_partials(cudaStream_t st, size_t n, int32_t** tickets, int blocks) {
   std::lock_guard<std::mutex> lock(g_split_mu);
   SplitFlags& f = g_split_bufs[st];
+  if (f.tick_cap < blocks) {
+    if (f.tick) {
+      ZB_CUDA(cudaStreamSynchronize(st));
+      ZB_CUDA(cudaFree(f.tick));
+    }
+    ZB_CUDA(cudaMalloc(&f.tick, static_cast<size_t>(blocks) * sizeof(int32_t)));
+    ZB_CUDA(cudaMemsetAsync(f.tick, 0, static_cast<size_t>(blocks) * sizeof(int32_t), st));  // kernels reset them
+    f.tick_cap = blocks;
+  }
+  *tickets = f.tick;
   if (f.part_cap < n) {
     if (f.part) {
       ZB_CUDA(cudaStreamSynchronize(st));
@@ -893,16 +928,6 @@ static float* bias_partials(cudaStream_t st, size_t n) {
     f.part_cap = n;
   }
   return f.part;
-}
-
-// out[m] = (beta ? out[m] : 0) + sum_s part[s][m], the (split, n-tile) partials in order (deterministic)
-__global__ void k_bias_finalize(const float* __restrict__ part, int splits, int M, float* __restrict__ out, int beta) {
-  pdl_wait();
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
-  float v = part[m];
-  for (int s = 1; s < splits; ++s) v += part[static_cast<int64_t>(s) * M + m];
-  out[m] = beta ? out[m] + v : v;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI, bool CS = false>
@@ -937,17 +962,13 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   const int items = tiles * ep.splits;
   const int grid = 2 * (items < pairs ? items : pairs);
   const int num_n = static_cast<int>(ceil_div(g.N, BN));
-  if (CS) ep.bias_part = bias_partials(st, static_cast<size_t>(ep.splits) * num_n * g.M);
+  if (CS)
+    ep.bias_part = bias_partials(st, static_cast<size_t>(ep.splits) * num_n * g.M, &ep.bias_tickets,
+                                 static_cast<int>(ceil_div(g.M, tc::BM)));
   CUtensorMap tcm, txm;
   epi_tmaps<EPI>(g, tcm, txm);
   launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, ep, g.M, g.N, g.K, sg);
   ZB_LAUNCH_CHECK();
-  if (CS) {
-    launch(PDL_OPS, k_bias_finalize, static_cast<int>(ceil_div(g.M, 256)), 256, 0, st,
-           static_cast<const float*>(ep.bias_part), static_cast<int>(ep.splits * num_n), g.M, ep.bias_out,
-           static_cast<int>(ep.beta));
-    ZB_LAUNCH_CHECK();
-  }
 }
 
 // 2-CTA tiles when the problem fills at least one 256 x 256 pair tile; env ZB_GEMM_1CTA=1 forces 1-CTA.

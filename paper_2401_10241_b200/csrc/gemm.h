@@ -47,6 +47,9 @@ struct EpiArgs {
   // already streams (column-sum warps, gemm.cu); other paths fall back to ops.h bias_grad.
   float* bias_out = nullptr;
   float* bias_part = nullptr;  // set by gemm(): partial sums [splits * n-tiles, M]
+  // set by gemm(): one arrival counter per 128-row block of M (zero between launches): the
+  // column-sum warps that write the LAST partial of a block sum all of its partials in order
+  int32_t* bias_tickets = nullptr;
 };
 
 constexpr int kMaxSeg = 4;
