@@ -133,7 +133,7 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtensorMap* tmC, const CUtensorMap* tmX,
                                                 uint32_t taddr, uint8_t* buf, uint64_t* xbar, uint32_t& xph,
                                                 int row0, int col0, int ncols, int N, int lane, bool reduce,
-                                                bool pre = false) {
+                                                bool pre = false, bool stream_out = false) {
   using TO = OutT<EPI>;
   constexpr int CC = 128 / static_cast<int>(sizeof(TO));
   constexpr bool kAuxIn = EPI == EPI_RESID || EPI == EPI_GELU_BWD;
@@ -192,8 +192,12 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
     sm100::fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-      if (EPI == EPI_F32_ACC && reduce)
+      if (EPI == EPI_F32_ACC && reduce && stream_out)
+        sm100::tma_reduce_add_2d_hint(tmC, buf, col, row0, pol);
+      else if (EPI == EPI_F32_ACC && reduce)
         sm100::tma_reduce_add_2d(tmC, buf, col, row0);
+      else if (EPI == EPI_F32_ACC && stream_out)
+        sm100::tma_store_2d_hint(tmC, buf, col, row0, pol);
       else if (EPI == EPI_F32_ACC)
         sm100::tma_store_2d(tmC, buf, col, row0);
       else
@@ -502,6 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t ph = 0;
+      const uint64_t pol_ops = sm100::l2_evict_last();
       for (int t = cid; t < items; t += ncl) {
         int mt, nt;
         tile_coords(t % tiles, num_m, num_n, mt, nt);
@@ -525,17 +530,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mB = &sg.b[sgi];
             k0 = (kb - sgi * sg.kbseg) * BK;
           }
-          if (!A_MN) {
-            sm100::tma_load_2d_pair(sa, mA, fbar, k0, m0);
-          } else {
-            sm100::tma_load_2d_pair(sa, mA, fbar, m0, k0);
-            sm100::tma_load_2d_pair(sa + 8192, mA, fbar, m0 + 64, k0);
-          }
-          if (!B_MN) {
-            sm100::tma_load_2d_pair(sb, mB, fbar, k0, n0);
-          } else {
+          if (ep.cache_hints & 2) {  // operands re-read by other CTAs: keep them in L2
+            if (!A_MN) {
+              sm100::tma_load_2d_pair_hint(sa, mA, fbar, k0, m0, pol_ops);
+            } else {
+              sm100::tma_load_2d_pair_hint(sa, mA, fbar, m0, k0, pol_ops);
+              sm100::tma_load_2d_pair_hint(sa + 8192, mA, fbar, m0 + 64, k0, pol_ops);
+            }
+            if (!B_MN) {
+              sm100::tma_load_2d_pair_hint(sb, mB, fbar, k0, n0, pol_ops);
+            } else {
 #pragma unroll
-            for (int i = 0; i < BN / 128; ++i) sm100::tma_load_2d_pair(sb + i * 8192, mB, fbar, n0 + 64 * i, k0);
+              for (int i = 0; i < BN / 128; ++i)
+                sm100::tma_load_2d_pair_hint(sb + i * 8192, mB, fbar, n0 + 64 * i, k0, pol_ops);
+            }
+          } else {
+            if (!A_MN) {
+              sm100::tma_load_2d_pair(sa, mA, fbar, k0, m0);
+            } else {
+              sm100::tma_load_2d_pair(sa, mA, fbar, m0, k0);
+              sm100::tma_load_2d_pair(sa + 8192, mA, fbar, m0 + 64, k0);
+            }
+            if (!B_MN) {
+              sm100::tma_load_2d_pair(sb, mB, fbar, k0, n0);
+            } else {
+#pragma unroll
+              for (int i = 0; i < BN / 128; ++i) sm100::tma_load_2d_pair(sb + i * 8192, mB, fbar, n0 + 64 * i, k0);
+            }
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -687,7 +708,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       sm100::tc_fence_after();
       epilogue_chunks<EPI>(ep, &tmC, &tmX,
                            tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
-                           &xbar[warp - 4], xph, erow, ecol, BN / 2, N, lane, ep.beta != 0 || sp > 0, kAuxIn);
+                           &xbar[warp - 4], xph, erow, ecol, BN / 2, N, lane, ep.beta != 0 || sp > 0, kAuxIn,
+                           EPI == EPI_F32_ACC && splits == 1 && (ep.cache_hints & 1));
       if (sp + 1 < splits && lane == 0) {  // publish: this region's reduce-adds are complete
         sm100::bulk_wait<0>();
         fence_proxy_async_global();
@@ -959,6 +981,11 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   const int pairs = num_sms() / 2;
   EpiArgs ep = g.ep;
   if (EPI == EPI_F32_ACC) split_k_plan(tiles, static_cast<int>(ceil_div(g.K, tc::BK)), pairs, st, ep);
+  static const int chint = [] {  // ZB_GEMM_CHINT: L2 cache-hint bits (gemm.h EpiArgs::cache_hints)
+    const char* e = getenv("ZB_GEMM_CHINT");
+    return e ? atoi(e) : 0;
+  }();
+  ep.cache_hints = chint;
   const int items = tiles * ep.splits;
   const int grid = 2 * (items < pairs ? items : pairs);
   const int num_n = static_cast<int>(ceil_div(g.N, BN));

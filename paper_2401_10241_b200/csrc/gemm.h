@@ -50,6 +50,9 @@ struct EpiArgs {
   // set by gemm(): one arrival counter per 128-row block of M (zero between launches): the
   // column-sum warps that write the LAST partial of a block sum all of its partials in order
   int32_t* bias_tickets = nullptr;
+  // set by gemm(): L2 cache hints of the 2-CTA kernel (ZB_GEMM_CHINT bits, measurement):
+  // 1 = W's f32 output (unsplit) evict-first, 2 = operand tiles evict-last
+  int32_t cache_hints = 0;
 };
 
 constexpr int kMaxSeg = 4;

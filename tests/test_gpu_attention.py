@@ -10,7 +10,10 @@ from zbtest_util import assert_close, cuda_available
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA GPU")]
 
 CASES = [(1, 1024, 1, 64), (2, 256, 3, 64), (2, 192, 2, 96), (1, 256, 2, 128), (2, 200, 2, 96), (1, 130, 1, 128),
-         (2, 384, 2, 96), (1, 1024, 2, 128), (3, 128, 1, 96)]
+         (2, 384, 2, 96), (1, 1024, 2, 128), (3, 128, 1, 96),
+         # persistent kernels with several items per CTA (forward: 2 x 128 = 256 items, backward:
+         # 1024 items incl. the dK/dV -> dQ switch, on 148 CTAs) and an odd query-tile count
+         (8, 512, 16, 64), (6, 640, 16, 128), (6, 384, 8, 96)]
 
 
 
