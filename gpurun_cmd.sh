@@ -1,10 +1,5 @@
 mkdir -p gpurun_out
-export PATH=/usr/local/cuda/bin:$PATH
-for h in 0 1 2 3; do
-  echo "# ZB_GEMM_CHINT=$h" >> gpurun_out/r02_gemm_chint.jsonl
-  ZB_GEMM_CHINT=$h timeout 600 python scripts/gemm_sustained.py --model 6.2B --secs 1.0 >> gpurun_out/r02_gemm_chint.jsonl 2>&1
-done
-for h in 0 3; do
-  ZB_GEMM_CHINT=$h timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --profile-from-start off -k regex:k_gemm --csv --log-file gpurun_out/r02_gemm_dram_chint$h.csv python scripts/profile_step.py --config 6.2B --layers 2 --m 2 > /dev/null 2>&1
-done
-cat gpurun_out/r02_gemm_chint.jsonl
+timeout 600 python -m pytest tests/test_gpu_gemm.py -q -x -p no:cacheprovider -k "layernorm or bias" > gpurun_out/ln_fused_tests.log 2>&1; echo "rc $?" >> gpurun_out/ln_fused_tests.log
+ZB_PDL=3 timeout 2400 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider > gpurun_out/gputests_pdl3.log 2>&1; echo "tests rc $?" >> gpurun_out/gputests_pdl3.log
+ZB_PDL=3 timeout 1200 python bench.py --second-config none --no-cpu-baseline > gpurun_out/bench_lnfused_pdl3.log 2>&1
+tail -5 gpurun_out/ln_fused_tests.log; tail -3 gpurun_out/gputests_pdl3.log; head -c 300 gpurun_out/bench_lnfused_pdl3.log
