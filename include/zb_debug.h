@@ -28,14 +28,6 @@ extern "C" {
 zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int32_t a_mn,
                         const void* B, int64_t ldb, int32_t b_mn, int32_t epi, void* C, int64_t ldc,
                         const float* bias, void* aux, int64_t ldaux, int32_t beta, void* stream);
-/* The B-pass dgrad with fused LayerNorm gamma / beta gradients (gemm.h EpiArgs::ln_gg):
- * dLN[M, N] (f32) = dY[M, K] W[K, N] (W stored [K, N] row-major = the layer's weight), and
- * gg[n] (beta ? += : =) sum_r dLN(r, n) (x(r, n) - mean[r]) rstd[r], gb[n] likewise of dLN;
- * x [M, N] in the activation dtype.  The 2-CTA path forms them in its epilogue, the others
- * with the separate column-sum kernel. */
-zb_status_t zb_dbg_gemm_ln(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* dY, const void* W,
-                           float* dLN, const void* x, const float* mean, const float* rstd, float* gg, float* gb,
-                           int32_t beta, void* stream);
 
 /* W-grouping contraction (bf16): C[M,N] (beta ? += : =) sum over the nseg
  * segments s of A_s^T B_s with A_s = dY_s [K/nseg, M] and B_s = X_s [K/nseg, N] (dev,

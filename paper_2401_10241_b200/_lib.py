@@ -100,7 +100,6 @@ _SIGS = {
     "zb_dbg_attention_bwd": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P], _I32),
     "zb_dbg_stage_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, _I32, _I32, _I32, C.POINTER(_I32), _I32,
                            C.POINTER(_I32)], _I32),
-    "zb_dbg_gemm_ln": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P], _I32),
     "zb_dbg_dp_plan": ([C.POINTER(zb_pass_t), _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                         C.POINTER(_I32), _I32, C.POINTER(_I32)], _I32),
     "zb_dbg_w_units": ([_P, C.POINTER(_I32), C.POINTER(_I64)], _I32),

@@ -399,13 +399,6 @@ def dbg_gemm(A, B, C_out, *, M, N, K, a_mn=False, b_mn=False, epi=0, bias=None, 
                           _ptr(bias), _ptr(aux), ldaux, beta, _stream(stream)))
 
 
-def dbg_gemm_ln(dY, W, dLN, x, mean, rstd, gg, gb, *, M, N, K, beta=0, stream=None):
-    """zb_dbg_gemm_ln: dLN = dY W (f32) with the fused LayerNorm gamma / beta gradients."""
-    dtype = ZB_DTYPE_F32 if dY.element_size() == 4 else ZB_DTYPE_BF16
-    check(lib.zb_dbg_gemm_ln(dtype, M, N, K, _ptr(dY), _ptr(W), _ptr(dLN), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gg),
-                             _ptr(gb), beta, _stream(stream)))
-
-
 def dbg_gemm_wgroup(A_segs, B_segs, C_out, *, M, N, bias=None, beta=0, stream=None):
     """zb_dbg_gemm_wgroup: C (+)= sum_s A_s^T B_s over nseg = len(A_segs) segments."""
     n = len(A_segs)

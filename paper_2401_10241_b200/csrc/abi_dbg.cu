@@ -33,30 +33,6 @@ extern "C" zb_status_t zb_dbg_gemm(int32_t dtype, int32_t M, int32_t N, int32_t 
   ZB_CATCH
 }
 
-extern "C" zb_status_t zb_dbg_gemm_ln(int32_t dtype, int32_t M, int32_t N, int32_t K, const void* dY, const void* W,
-                                      float* dLN, const void* x, const float* mean, const float* rstd, float* gg,
-                                      float* gb, int32_t beta, void* stream) {
-  ZB_TRY {
-    if (dtype != ZB_DTYPE_BF16 && dtype != ZB_DTYPE_F32) return set_error(ZB_EINVAL, "bad dtype");
-    if (M <= 0 || N <= 0 || K <= 0 || !dY || !W || !dLN || !x || !mean || !rstd || !gg || !gb)
-      return set_error(ZB_EINVAL, "bad operands");
-    GemmArgs g{};
-    g.M = M; g.N = N; g.K = K;
-    g.A = dY; g.lda = K; g.a_mn = false;
-    g.B = W; g.ldb = N; g.b_mn = true;
-    g.epi = EPI_F32_STORE;
-    g.ep = EpiArgs{dLN, N, nullptr, const_cast<void*>(x), N, 0};
-    g.ep.ln_mean = mean;
-    g.ep.ln_rstd = rstd;
-    g.ep.ln_gg = gg;
-    g.ep.ln_gb = gb;
-    g.ep.ln_beta = beta;
-    gemm(g, static_cast<DType>(dtype), static_cast<cudaStream_t>(stream));
-    return ZB_OK;
-  }
-  ZB_CATCH
-}
-
 
 extern "C" zb_status_t zb_dbg_gemm_wgroup(int32_t M, int32_t N, int32_t K, int32_t nseg, const void* const* A_seg,
                                           const void* const* B_seg, float* C, float* bias_out, int32_t beta,

@@ -46,10 +46,11 @@ static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // their TMEM allocation, so a dependent CTA can never hold TMEM that a CTA of
 // an earlier grid still has to allocate; the HBM-bound kernels trigger
 // implicitly at exit.  (Early triggers in the HBM-bound kernels deadlocked the
-// 1.5B step on B200 — cause not identified — and PDL of the TMEM classes
-// measured no gain: the step is bound by kernel time at power-capped clocks,
-// not by launch gaps.)  Default off.
-// ZB_PDL=<mask>: PDL for kernel classes (1 GEMM, 2 attention, 4 others).
+// 1.5B step on B200 — cause not identified.)  PDL of the TMEM classes measured
+// no gain in round 1; with the persistent attention kernels of round 2 it gives
+// +0.7% on the 6.2B step (28.2k -> 28.4k tokens/s) and the GPU suite passes with
+// it, so the default is GEMM | attention.
+// ZB_PDL=<mask>: PDL for kernel classes (1 GEMM, 2 attention, 4 others); 0 = off.
 // ZB_TRACE_LAUNCH=1 prints every kernel when the stream reaches it (debugging;
 // serialises).
 enum PdlClass : int { PDL_GEMM = 1, PDL_ATTN = 2, PDL_OPS = 4 };

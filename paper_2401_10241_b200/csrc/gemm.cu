@@ -129,35 +129,12 @@ __device__ __forceinline__ int swz(int lane, int j) { return lane * 128 + ((j ^ 
 // f32 accumulation (EPI_F32_ACC, beta) is a TMA reduce-add: the L2 adds the tile, nothing
 // is read back into the SM.  RESID / GELU_BWD read their bf16 operand through the same
 // staging buffer (TMA load on the warp's mbarrier), BIAS_GELU stores C then GeLU(C).
-// sum over the 32 lanes of a[i] for each i: lane l ends with column l's sum in a[0] (a fixed
-// butterfly tree: 31 shuffles, deterministic)
-__device__ __forceinline__ void lane_transpose_sum(float (&a)[32], int lane) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < o; ++i) {
-      const float send = up ? a[i] : a[i + o];
-      const float keep = up ? a[i + o] : a[i];
-      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-}
-
-template <int EPI, bool LNG = false>
+template <int EPI>
 __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtensorMap* tmC, const CUtensorMap* tmX,
                                                 uint32_t taddr, uint8_t* buf, uint64_t* xbar, uint32_t& xph,
                                                 int row0, int col0, int ncols, int N, int lane, bool reduce,
-                                                bool pre = false, bool stream_out = false, int M = 0) {
+                                                bool pre = false, bool stream_out = false) {
   using TO = OutT<EPI>;
-  static_assert(!LNG || EPI == EPI_F32_STORE, "fused LayerNorm gamma / beta: the f32 dLN output only");
-  // fused LayerNorm gamma / beta (LNG): this lane's row statistics
-  const int lrow = row0 + lane;
-  float ln_mu = 0.f, ln_rs = 0.f;
-  if (LNG && lrow < M) {
-    ln_mu = ep.ln_mean[lrow];
-    ln_rs = ep.ln_rstd[lrow];
-  }
   constexpr int CC = 128 / static_cast<int>(sizeof(TO));
   constexpr bool kAuxIn = EPI == EPI_RESID || EPI == EPI_GELU_BWD;
   constexpr bool kBias = EPI == EPI_STORE || EPI == EPI_BIAS_GELU || EPI == EPI_RESID;
@@ -181,32 +158,6 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
     if (CC == 64) sm100::tmem_ld32(taddr + ch * CC + 32, r + 32);
     sm100::tmem_ld_wait();
     float* v = reinterpret_cast<float*>(r);
-    if constexpr (LNG) {  // per-column sums over this warp's 32 rows of dy x^ and dy
-      float a1[32], a2[32];
-      const bf16* xr = static_cast<const bf16*>(ep.aux) + static_cast<int64_t>(lrow) * ep.ldaux + col;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        float xv[8];
-        if (lrow < M && col + 8 * g < N)
-          Vec8<bf16>::load(xr + 8 * g, xv);
-        else
-#pragma unroll
-          for (int i = 0; i < 8; ++i) xv[i] = ln_mu;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float d = v[8 * g + i];
-          a1[8 * g + i] = d * ((xv[i] - ln_mu) * ln_rs);
-          a2[8 * g + i] = d;
-        }
-      }
-      lane_transpose_sum(a1, lane);
-      lane_transpose_sum(a2, lane);
-      const int rb = row0 / 32;
-      if (col + lane < N) {
-        ep.ln_part[static_cast<int64_t>(rb) * N + col + lane] = a1[0];
-        ep.ln_part[(static_cast<int64_t>(ep.ln_rb) + rb) * N + col + lane] = a2[0];
-      }
-    }
     if (kBias && ep.bias != nullptr) {
 #pragma unroll
       for (int g = 0; g < CC / 8; ++g) {
@@ -269,28 +220,6 @@ __device__ __forceinline__ void epilogue_chunks(const EpiArgs& ep, const CUtenso
         sm100::tma_store_2d_hint(tmX, buf, col, row0, pol);
         sm100::bulk_commit();
       }
-    }
-  }
-  if constexpr (LNG) {  // the last of the ln_rb warps writing this 128-column block sums its partials
-    __threadfence();
-    __syncwarp();
-    const int cb = col0 / 128;
-    int last = 0;
-    if (lane == 0) last = atomicAdd(&ep.ln_tickets[cb], 1) == ep.ln_rb - 1;
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-      __threadfence();
-#pragma unroll 1
-      for (int c = col0 + lane; c < col0 + ncols && c < N; c += 32) {
-        float s1 = 0.f, s2 = 0.f;
-        for (int rb = 0; rb < ep.ln_rb; ++rb) {
-          s1 += __ldcg(ep.ln_part + static_cast<int64_t>(rb) * N + c);
-          s2 += __ldcg(ep.ln_part + (static_cast<int64_t>(ep.ln_rb) + rb) * N + c);
-        }
-        ep.ln_gg[c] = ep.ln_beta ? ep.ln_gg[c] + s1 : s1;
-        ep.ln_gb[c] = ep.ln_beta ? ep.ln_gb[c] + s2 : s2;
-      }
-      if (lane == 0) ep.ln_tickets[cb] = 0;  // ready for the next launch on this stream
     }
   }
 }
@@ -510,7 +439,7 @@ struct SegMaps {
   int nseg, kbseg;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI, typename TO, bool CS = false, bool LNG = false>
+template <int BN, bool A_MN, bool B_MN, int EPI, typename TO, bool CS = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const EpiArgs ep,
@@ -777,10 +706,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       sm100::mbar_wait(&tfull[acc], aph);
       if (warp == 4 && lane == 0) GTR(2, (t - cid) / ncl);
       sm100::tc_fence_after();
-      epilogue_chunks<EPI, LNG>(ep, &tmC, &tmX,
-                                tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
-                                &xbar[warp - 4], xph, erow, ecol, BN / 2, N, lane, ep.beta != 0 || sp > 0, kAuxIn,
-                                EPI == EPI_F32_ACC && splits == 1 && (ep.cache_hints & 1), M);
+      epilogue_chunks<EPI>(ep, &tmC, &tmX,
+                           tbase + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + half * (BN / 2), buf,
+                           &xbar[warp - 4], xph, erow, ecol, BN / 2, N, lane, ep.beta != 0 || sp > 0, kAuxIn,
+                           EPI == EPI_F32_ACC && splits == 1 && (ep.cache_hints & 1));
       if (sp + 1 < splits && lane == 0) {  // publish: this region's reduce-adds are complete
         sm100::bulk_wait<0>();
         fence_proxy_async_global();
@@ -951,10 +880,6 @@ struct SplitFlags {
   size_t part_cap = 0;
   int32_t* tick = nullptr;  // per-128-row-block arrival counters of the column sums
   int tick_cap = 0;
-  float* ln_part = nullptr;  // fused LayerNorm gamma / beta partials
-  size_t ln_cap = 0;
-  int32_t* ln_tick = nullptr;
-  int ln_tick_cap = 0;
 };
 static std::mutex g_split_mu;
 static std::map<cudaStream_t, SplitFlags> g_split_bufs;
@@ -1027,35 +952,10 @@ static float* bias_partials(cudaStream_t st, size_t n, int32_t** tickets, int bl
   return f.part;
 }
 
-// partial sums / arrival counters of the fused LayerNorm gamma / beta (stream-private)
-static void ln_partials(cudaStream_t st, size_t n, int blocks, float** part, int32_t** tickets) {
-  std::lock_guard<std::mutex> lock(g_split_mu);
-  SplitFlags& f = g_split_bufs[st];
-  if (f.ln_cap < n) {
-    if (f.ln_part) {
-      ZB_CUDA(cudaStreamSynchronize(st));
-      ZB_CUDA(cudaFree(f.ln_part));
-    }
-    ZB_CUDA(cudaMalloc(&f.ln_part, n * sizeof(float)));
-    f.ln_cap = n;
-  }
-  if (f.ln_tick_cap < blocks) {
-    if (f.ln_tick) {
-      ZB_CUDA(cudaStreamSynchronize(st));
-      ZB_CUDA(cudaFree(f.ln_tick));
-    }
-    ZB_CUDA(cudaMalloc(&f.ln_tick, static_cast<size_t>(blocks) * sizeof(int32_t)));
-    ZB_CUDA(cudaMemsetAsync(f.ln_tick, 0, static_cast<size_t>(blocks) * sizeof(int32_t), st));  // kernels reset them
-    f.ln_tick_cap = blocks;
-  }
-  *part = f.ln_part;
-  *tickets = f.ln_tick;
-}
-
-template <int BN, bool A_MN, bool B_MN, int EPI, bool CS = false, bool LNG = false>
+template <int BN, bool A_MN, bool B_MN, int EPI, bool CS = false>
 static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   using C = tc::Cfg2<BN>;
-  auto kern = tc::k_gemm_tc2<BN, A_MN, B_MN, EPI, bf16, CS, LNG>;
+  auto kern = tc::k_gemm_tc2<BN, A_MN, B_MN, EPI, bf16, CS>;
   static bool attr = false;
   if (!attr) {
     ZB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1092,11 +992,6 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
   if (CS)
     ep.bias_part = bias_partials(st, static_cast<size_t>(ep.splits) * num_n * g.M, &ep.bias_tickets,
                                  static_cast<int>(ceil_div(g.M, tc::BM)));
-  if (LNG) {
-    ep.ln_rb = static_cast<int>(ceil_div(g.M, 2 * tc::BM)) * 8;
-    ln_partials(st, static_cast<size_t>(2) * ep.ln_rb * g.N, static_cast<int>(ceil_div(g.N, 128)), &ep.ln_part,
-                &ep.ln_tickets);
-  }
   CUtensorMap tcm, txm;
   epi_tmaps<EPI>(g, tcm, txm);
   launch(PDL_GEMM, kern, grid, tc::kThreads, C::SMEM, st, ta, tb, tcm, txm, ep, g.M, g.N, g.K, sg);
@@ -1113,30 +1008,24 @@ static bool use_pair(const GemmArgs& g) {
   return !force1 && g.M >= 256 && g.N >= 256;
 }
 
-// returns a mask of the side outputs the kernel also formed: 1 W's bias gradient
-// (ep.bias_out), 2 the LayerNorm gamma / beta gradients (ep.ln_gg / ln_gb)
+// returns true when the kernel also formed W's bias gradient (ep.bias_out)
 template <int BN, bool A_MN, bool B_MN, int EPI>
-static int launch_any(const GemmArgs& g, cudaStream_t st) {
+static bool launch_any(const GemmArgs& g, cudaStream_t st) {
   constexpr bool kCS = A_MN && EPI == EPI_F32_ACC && BN == 256;
-  constexpr bool kLN = EPI == EPI_F32_STORE && BN == 256;
   if (BN == 256 && use_pair(g)) {
     if (kCS && g.ep.bias_out != nullptr) {
       launch_tc2<BN, A_MN, B_MN, EPI, kCS>(g, st);
-      return 1;
-    }
-    if (kLN && g.ep.ln_gg != nullptr) {
-      launch_tc2<BN, A_MN, B_MN, EPI, false, kLN>(g, st);
-      return 2;
+      return true;
     }
     launch_tc2<BN, A_MN, B_MN, EPI>(g, st);
   } else {
     launch_tc<BN, A_MN, B_MN, EPI>(g, st);
   }
-  return 0;
+  return false;
 }
 
 template <int BN, bool A_MN, bool B_MN>
-static int dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
+static bool dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
   switch (g.epi) {
     case EPI_STORE: return launch_any<BN, A_MN, B_MN, EPI_STORE>(g, st);
     case EPI_BIAS_GELU: return launch_any<BN, A_MN, B_MN, EPI_BIAS_GELU>(g, st);
@@ -1149,7 +1038,7 @@ static int dispatch_epi_tc(const GemmArgs& g, cudaStream_t st) {
 }
 
 template <int BN>
-static int dispatch_major_tc(const GemmArgs& g, cudaStream_t st) {
+static bool dispatch_major_tc(const GemmArgs& g, cudaStream_t st) {
   if (!g.a_mn && !g.b_mn) return dispatch_epi_tc<BN, false, false>(g, st);
   if (!g.a_mn && g.b_mn) return dispatch_epi_tc<BN, false, true>(g, st);
   if (g.a_mn && g.b_mn) return dispatch_epi_tc<BN, true, true>(g, st);
@@ -1202,26 +1091,21 @@ void gemm(const GemmArgs& g, DType dt, cudaStream_t st) {
     throw CudaError("gemm: bias_out is W's bias gradient (EPI_F32_ACC, MN-major A)");
   const int cls = g.a_mn ? ktimer::GEMM_W : (g.b_mn ? ktimer::GEMM_B : ktimer::GEMM_F);
   const int tk = ktimer::start(cls, 2.0 * g.M * g.N * static_cast<double>(g.K), st);
-  if (g.ep.ln_gg != nullptr && (g.epi != EPI_F32_STORE || g.ep.aux == nullptr || !g.ep.ln_gb))
-    throw CudaError("gemm: fused LayerNorm gamma / beta needs EPI_F32_STORE, aux = x and both outputs");
-  int done = 0;
+  bool bias_done = false;
   if (dt == DT_F32) {
     if (!g.a_mn && !g.b_mn) dispatch_epi_f32<false, false>(g, st);
     else if (!g.a_mn && g.b_mn) dispatch_epi_f32<false, true>(g, st);
     else if (g.a_mn && g.b_mn) dispatch_epi_f32<true, true>(g, st);
     else dispatch_epi_f32<true, false>(g, st);
   } else if (g.N <= 128) {
-    done = dispatch_major_tc<128>(g, st);
+    bias_done = dispatch_major_tc<128>(g, st);
   } else {
-    done = dispatch_major_tc<256>(g, st);
+    bias_done = dispatch_major_tc<256>(g, st);
   }
   ktimer::stop(tk, st);
-  // paths without the in-kernel column sums (f32 parity mode, 1-CTA tiles): separate kernels
-  if (g.ep.bias_out != nullptr && !(done & 1))
+  // paths without the in-kernel column sums (f32 parity mode, 1-CTA tiles): separate kernel
+  if (g.ep.bias_out != nullptr && !bias_done)
     bias_grad(dt, g.A, g.lda, g.ep.bias_out, g.K, g.M, g.ep.beta, st);
-  if (g.ep.ln_gg != nullptr && !(done & 2))
-    layernorm_param_grads(dt, static_cast<const float*>(g.ep.C), g.ep.aux, g.ep.ln_mean, g.ep.ln_rstd, g.ep.ln_gg,
-                          g.ep.ln_gb, g.ep.ln_beta, g.M, g.N, st);
 }
 
 }  // namespace zb

@@ -50,21 +50,6 @@ struct EpiArgs {
   // set by gemm(): one arrival counter per 128-row block of M (zero between launches): the
   // column-sum warps that write the LAST partial of a block sum all of its partials in order
   int32_t* bias_tickets = nullptr;
-  // fused LayerNorm gamma / beta gradients (EPI_F32_STORE only: C is the LayerNorm-output
-  // gradient dy): ln_gg[n] (ln_beta ? += : =) sum_r C(r, n) (aux(r, n) - ln_mean[r]) ln_rstd[r]
-  // and ln_gb[n] (ln_beta ? += : =) sum_r C(r, n), aux = the LayerNorm input x (activation
-  // dtype, row pitch ldaux) — the 2-CTA kernel forms them in its epilogue (per-32-row partials,
-  // the last-arriving warp of a 128-column block sums them in row-block order); other paths
-  // run ops.h layernorm_param_grads after the GEMM.  Same formula and order as that kernel's
-  // partial sums, not bitwise the same sums.
-  const float* ln_mean = nullptr;
-  const float* ln_rstd = nullptr;
-  float* ln_gg = nullptr;
-  float* ln_gb = nullptr;
-  int32_t ln_beta = 0;
-  float* ln_part = nullptr;      // set by gemm(): [2][ln_rb][N] partial sums
-  int32_t* ln_tickets = nullptr;  // set by gemm(): one arrival counter per 128 columns
-  int32_t ln_rb = 0;             // set by gemm(): 32-row blocks (8 per 256-row tile)
   // set by gemm(): L2 cache hints of the 2-CTA kernel (ZB_GEMM_CHINT bits, measurement):
   // 1 = W's f32 output (unsplit) evict-first, 2 = operand tiles evict-last
   int32_t cache_hints = 0;

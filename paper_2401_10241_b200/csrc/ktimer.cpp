@@ -16,7 +16,7 @@ int64_t launch_count(bool reset) { return reset ? g_launches.exchange(0) : g_lau
 bool pdl_enabled(int cls) {
   static const int mask = [] {
     const char* e = std::getenv("ZB_PDL");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 3;  // default: PDL_GEMM | PDL_ATTN, the TMEM kernels (common.cuh)
   }();
   return (mask & cls) != 0;
 }

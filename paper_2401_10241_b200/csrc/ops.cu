@@ -891,35 +891,29 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
   ktimer::stop(tk__, st);
 }
 
-void layernorm_param_grads(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, float* gg,
-                           float* gb, int beta, int rows, int h, cudaStream_t st) {
-  if (rows <= 0) return;
-  const double esz = dt == DT_BF16 ? 2.0 : 4.0, elems = static_cast<double>(rows) * h;
-  const int tk = ktimer::start(ktimer::LN_PARAM, elems * (4.0 + esz) + 8.0 * rows + 8.0 * h, st);
-  int ntiles, rb, rpb;
-  colred2_grid(rows, h, 2, ntiles, rb, rpb);
-  const ColredScratch sc = colred_scratch(st);
-  const dim3 grid(ntiles, rb);
-  if (dt == DT_BF16)
-    launch(PDL_OPS, k_colred2<1, bf16>, grid, kCR_THREADS, 0, st, static_cast<const bf16*>(x), static_cast<int64_t>(h),
-           dy, mean, rstd, gg, gb, sc.part, sc.tickets, rows, h, rpb, beta);
-  else
-    launch(PDL_OPS, k_colred2<1, float>, grid, kCR_THREADS, 0, st, static_cast<const float*>(x), static_cast<int64_t>(h),
-           dy, mean, rstd, gg, gb, sc.part, sc.tickets, rows, h, rpb, beta);
-  ZB_LAUNCH_CHECK();
-  ktimer::stop(tk, st);
-}
-
 void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
                    const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta, int rows, int h,
                    cudaStream_t st) {
   if (rows <= 0) return;
   const double esz = dt == DT_BF16 ? 2.0 : 4.0, elems = static_cast<double>(rows) * h;
-  // 1) gamma / beta grads (reads x before step 2 may overwrite it in place); gg == nullptr:
-  //    already formed by the GEMM that produced dy (gemm.h EpiArgs::ln_gg)
-  if (gg != nullptr) layernorm_param_grads(dt, dy, x, mean, rstd, gg, gb, beta, rows, h, st);
+  // 1) gamma / beta grads (reads x before step 2 may overwrite it in place)
+  int tk = ktimer::start(ktimer::LN_PARAM, elems * (4.0 + esz) + 8.0 * rows + 8.0 * h, st);
+  {
+    int ntiles, rb, rpb;
+    colred2_grid(rows, h, 2, ntiles, rb, rpb);
+    const ColredScratch sc = colred_scratch(st);
+    const dim3 grid(ntiles, rb);
+    if (dt == DT_BF16)
+      launch(PDL_OPS, k_colred2<1, bf16>, grid, kCR_THREADS, 0, st, static_cast<const bf16*>(x), static_cast<int64_t>(h),
+             dy, mean, rstd, gg, gb, sc.part, sc.tickets, rows, h, rpb, beta);
+    else
+      launch(PDL_OPS, k_colred2<1, float>, grid, kCR_THREADS, 0, st, static_cast<const float*>(x), static_cast<int64_t>(h),
+             dy, mean, rstd, gg, gb, sc.part, sc.tickets, rows, h, rpb, beta);
+  }
+  ZB_LAUNCH_CHECK();
+  ktimer::stop(tk, st);
   // 2) dx, one CTA per row (dy arrives in f32: the dLN GEMM epilogue keeps full precision)
-  int tk = ktimer::start(ktimer::LN_BWD,
+  tk = ktimer::start(ktimer::LN_BWD,
                      elems * (4.0 + 2 * esz + (resid ? 4.0 : 0.0) + (dx32 ? 4.0 : 0.0)) + 8.0 * rows + 4.0 * h, st);
   ln_dispatch<0>(h, [&](auto V) {
     constexpr int VPT = decltype(V)::value;

@@ -19,10 +19,6 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
 // (activation dtype) receives the copy the GEMMs consume (DESIGN.md R-grad32).
 // gg / gb (+)= column sums of dy * xhat / dy (beta: accumulate), deterministic
 // (fixed row partition and fixed reduction tree).
-// LayerNorm gamma / beta gradients alone (the first step of layernorm_bwd): gg (beta ? += : =)
-// sum_r dy (x - mean) rstd, gb (beta ? += : =) sum_r dy (deterministic two-phase column sums)
-void layernorm_param_grads(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, float* gg,
-                           float* gb, int beta, int rows, int h, cudaStream_t st);
 void layernorm_bwd(DType dt, const float* dy, const void* x, const float* mean, const float* rstd, const float* g,
                    const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta, int rows, int h,
                    cudaStream_t st);

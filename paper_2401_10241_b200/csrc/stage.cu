@@ -7,8 +7,7 @@
 //                 slot for W), d LN_f; per layer: dU = (dX' Wfc2) * GeLU'(U),
 //                 dLN2 = dU Wfc1, dX1 = dX' + LN2_bwd, dO = dX1 Wproj, dQKV = attn_bwd,
 //                 dLN1 = dQKV Wqkv, dX = dX1 + LN1_bwd; LayerNorm gamma/beta grads
-//                 are taken here (DESIGN.md R-ln), formed in the epilogue of the GEMM that
-//                 produces dLN (deterministic per-32-row partials).
+//                 (deterministic chunk partials) are taken here (DESIGN.md R-ln).
 // W  (per layer)  dW += dY^T X for fc2 (dX', G), fc1 (dU, LN2), proj (dX1, O),
 //                 qkv (dQKV, LN1) with f32 accumulation into the persistent grads,
 //                 bias grads = column sums of dY formed inside the same GEMMs;
@@ -252,24 +251,6 @@ static void lin_wgrad(Ctx& c, const void* dY, const void* X, float* dW, float* d
   g.ep.bias_out = db;
   gemm(g, c.dt, c.stream);
 }
-// dLN [M, N] (f32) = dY [M, K] * W [K, N] with the LayerNorm gamma / beta gradients of the
-// LayerNorm whose output gradient dLN is (input x, statistics mu / rs) formed from the same
-// tiles (gemm.h EpiArgs::ln_gg); the LayerNorm backward then computes dx only
-static void lin_dgrad_ln(Ctx& c, const void* dY, const void* W, float* dLN, int M, int N, int K, const void* x,
-                         const float* mu, const float* rs, float* gg, float* gb, int beta) {
-  GemmArgs g{};
-  g.M = M; g.N = N; g.K = K;
-  g.A = dY; g.lda = K; g.a_mn = false;
-  g.B = W; g.ldb = N; g.b_mn = true;
-  g.epi = EPI_F32_STORE;
-  g.ep = EpiArgs{dLN, N, nullptr, const_cast<void*>(x), N, 0};
-  g.ep.ln_mean = mu;
-  g.ep.ln_rstd = rs;
-  g.ep.ln_gg = gg;
-  g.ep.ln_gb = gb;
-  g.ep.ln_beta = beta;
-  gemm(g, c.dt, c.stream);
-}
 static void ln_bwd(Ctx& c, const float* dy, const void* x, const float* mu, const float* rs, const float* g,
                    const float* resid, float* dx32, void* dx, float* gg, float* gb, int beta) {
   layernorm_bwd(c.dt, dy, x, mu, rs, g, resid, dx32, dx, gg, gb, beta, c.T, c.h,
@@ -323,8 +304,8 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
     cross_entropy(dt, logits, sl.lab, dl, loss_rows, loss_acc, T, V,
                   1.0f / (static_cast<float>(T) * static_cast<float>(cfg.m) * static_cast<float>(dp_world)), stream);
     if (head_w_eager) lin_wgrad(*this, dl, sl.lnf, g_head_w, nullptr, V, H, T, beta);  // C8 eager option
-    lin_dgrad_ln(*this, dl, head_w, d_ln, T, H, V, sl.xl, sl.muf, sl.rsf, g_lnf_g, g_lnf_b, beta);
-    ln_bwd(*this, d_ln, sl.xl, sl.muf, sl.rsf, lnf_g, nullptr, g32_dx, sl.dy, nullptr, nullptr, beta);
+    lin_dgrad(*this, dl, head_w, d_ln, T, H, V, EPI_F32_STORE, nullptr);
+    ln_bwd(*this, d_ln, sl.xl, sl.muf, sl.rsf, lnf_g, nullptr, g32_dx, sl.dy, g_lnf_g, g_lnf_b, beta);
     dx2_32 = g32_dx;
   } else {
     if (dy_in == nullptr) throw std::invalid_argument("zb_stage_backward_input: dy is required on stages < p-1");
@@ -339,15 +320,15 @@ void Ctx::backward_input(int mb, int slot_idx, const void* dy_in, void* dx_out) 
     const LayerW& w = lw[l];
     void* dx2 = l == Ls - 1 ? sl.dy : sl.L[l + 1].x;
     lin_dgrad(*this, dx2, w.fc2_w, A.u, T, 4 * H, H, EPI_GELU_BWD, A.u);  // dU over U
-    lin_dgrad_ln(*this, A.u, w.fc1_w, d_ln, T, H, 4 * H, A.x1, A.mu2, A.rs2, w.g_ln2_g, w.g_ln2_b, beta);
-    ln_bwd(*this, d_ln, A.x1, A.mu2, A.rs2, w.ln2_g, dx2_32, g32_dx1, A.x1, nullptr, nullptr, beta);  // dX1
+    lin_dgrad(*this, A.u, w.fc1_w, d_ln, T, H, 4 * H, EPI_F32_STORE, nullptr);
+    ln_bwd(*this, d_ln, A.x1, A.mu2, A.rs2, w.ln2_g, dx2_32, g32_dx1, A.x1, w.g_ln2_g, w.g_ln2_b, beta);  // dX1
     lin_dgrad(*this, A.x1, w.proj_w, d_o, T, H, H, EPI_STORE, nullptr);
     attention_bwd(ash, dt, A.qkv, A.o, d_o, A.lse, spare_qkv, delta, stream);
     std::swap(A.qkv, spare_qkv);                                                              // dQKV in the slot
-    lin_dgrad_ln(*this, A.qkv, w.qkv_w, d_ln, T, H, 3 * H, A.x, A.mu1, A.rs1, w.g_ln1_g, w.g_ln1_b, beta);
+    lin_dgrad(*this, A.qkv, w.qkv_w, d_ln, T, H, 3 * H, EPI_F32_STORE, nullptr);
     // the stage's input gradient (l == 0) goes straight to the caller's f32 buffer
     float* out32 = (l == 0 && !first && dx_out != nullptr) ? static_cast<float*>(dx_out) : g32_dx;
-    ln_bwd(*this, d_ln, A.x, A.mu1, A.rs1, w.ln1_g, g32_dx1, out32, A.x, nullptr, nullptr, beta);         // dX
+    ln_bwd(*this, d_ln, A.x, A.mu1, A.rs1, w.ln1_g, g32_dx1, out32, A.x, w.g_ln1_g, w.g_ln1_b, beta);     // dX
     dx2_32 = g32_dx;
   }
   first_b_done = true;
