@@ -37,3 +37,21 @@ def test_full_width_multi_microbatch_two_stages_vs_oracle(name):
     ref_loss, ref = oracle_grads(cfg, "bf16")
     loss, grads, _ = gpu_run(cfg, 2, "bf16")
     check_tolerance(loss, grads, ref_loss, ref, "bf16")
+
+
+@pytest.mark.parametrize("name", ["14.6B", "28.3B"])
+def test_c4_c5_widths_grouped_w_vs_oracle(name):
+    """BASELINE configs[3] / [4] widths (14.6B: h 5120, 40 heads; 28.3B: h 6144, 48 heads;
+    d = 128, b = 1 so T = 1024 — the W GEMM at the HBM ridge): one layer, two
+    microbatches whose Ws are deferred and run as ONE grouped contraction per linear
+    (W-grouping, K = 2T), against the fp64 oracle (normwise + elementwise)."""
+    import torch
+    from test_gpu_wgroup import _ctx1, _deferred_list, _grads
+    cfg = zb_synth.CONFIGS[name].with_(L=1, b=1, m=2)
+    ref_loss, ref = oracle_grads(cfg, "bf16")
+    tok = zb_synth.make_tokens(cfg, 0)
+    tin = torch.from_numpy(np.ascontiguousarray(tok[..., :cfg.s])).cuda()
+    lab = torch.from_numpy(np.ascontiguousarray(tok[..., 1:])).cuda()
+    c = _ctx1(cfg, cfg.m, "bf16")
+    c.run_iteration(_deferred_list(cfg.m), tin, lab, group_w=True)
+    check_tolerance(c.loss(), _grads(c, cfg), ref_loss, ref, "bf16")
