@@ -246,14 +246,25 @@ enum { ZB_RUN_HOST_INPUTS = 1, /* tokens / labels are host pointers: H2D inside 
                                /* the same adjacency, within tolerance otherwise.  Not for  */
                                /* zb_run_iteration_worker.  A timed group records one event */
                                /* pair; zb_ctx_profile counts it as k W passes of 1/k each. */
-       ZB_RUN_DP_REORDER = 16  /* data parallelism (zb_ctx_attach_dp), App. A       */
+       ZB_RUN_DP_REORDER = 16, /* data parallelism (zb_ctx_attach_dp), App. A       */
                                /* the W passes at the tail of the stage's list   */
                                /* are reordered to cluster the computations of each         */
                                /* parameter, whose gradient all-reduce then starts while    */
                                /* the next parameter's computations run.  Without it the    */
                                /* tail keeps its W-major order (all-reduces start only      */
                                /* inside the last W).  Sub-computations of the tail are not */
-                               /* timed (ZB_RUN_TIMING).                                    */ };
+                               /* timed (ZB_RUN_TIMING).                                    */
+       ZB_RUN_GRAPH = 32       /* zb_run_iteration, p = 1 without NCCL: the iteration's     */
+                               /* launches are captured once into a CUDA graph and the     */
+                               /* graph is replayed while the pass list, the flags and the */
+                               /* input pointers stay the same (the first call with a new  */
+                               /* key runs eagerly and sizes lazy buffers, the second one  */
+                               /* captures).  Device tokens / labels are copied into the   */
+                               /* context's staging buffers first, so per-step input       */
+                               /* buffers do not invalidate the graph.  Ignored (eager)    */
+                               /* with ZB_RUN_TIMING, kernel timing on, or a context on    */
+                               /* the default stream (not capturable).  Results are        */
+                               /* bitwise those of the eager run.                          */ };
 
 typedef struct {
   int32_t n_passes;

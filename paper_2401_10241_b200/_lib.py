@@ -20,7 +20,7 @@ FAMILY = {"1f1b": ZB_1F1B, "zbh1": ZB_H1, "zbh2": ZB_H2, "auto": ZB_AUTO}
 ZB_V, ZB_1F1B_I = 4, 5
 CHUNKED_FAMILY = {"zbv": ZB_V, "1f1bi": ZB_1F1B_I}
 ZB_DTYPE_BF16, ZB_DTYPE_F32 = 0, 1
-ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_RUN_FUSED_BW, ZB_RUN_GROUP_W, ZB_RUN_DP_REORDER = 1, 2, 4, 8, 16
+ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_RUN_FUSED_BW, ZB_RUN_GROUP_W, ZB_RUN_DP_REORDER, ZB_RUN_GRAPH = 1, 2, 4, 8, 16, 32
 ZB_OPT_SYNC, ZB_OPT_PV = 0, 1
 ZB_CFG_HEAD_W_EAGER = 1
 ZB_MAX_STAGES = 64

@@ -11,7 +11,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from ._lib import (CHUNKED_FAMILY, FAMILY, ZB_DTYPE_BF16, ZB_DTYPE_F32, ZB_OPT_PV, ZB_OPT_SYNC, ZB_RUN_FUSED_BW,
-                   ZB_RUN_DP_REORDER, ZB_RUN_GROUP_W, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_CFG_HEAD_W_EAGER,
+                   ZB_RUN_DP_REORDER, ZB_RUN_GRAPH, ZB_RUN_GROUP_W, ZB_RUN_HOST_INPUTS, ZB_RUN_TIMING, ZB_CFG_HEAD_W_EAGER,
                    ACTIONS, check, lib, zb_iter_stats_t, zb_model_cfg_t, zb_optim_cfg_t, zb_pass_t, zb_pv_report_t,
                    zb_sim_t)
 
@@ -256,10 +256,10 @@ class Context:
         self._group = group
 
     def run_iteration(self, passes, tokens=None, labels=None, host_inputs=False, timing=False, fused=False,
-                      group_w=False, dp_reorder=False):
+                      group_w=False, dp_reorder=False, graph=False):
         flags = (ZB_RUN_HOST_INPUTS if host_inputs else 0) | (ZB_RUN_TIMING if timing else 0) | \
             (ZB_RUN_FUSED_BW if fused else 0) | (ZB_RUN_GROUP_W if group_w else 0) | \
-            (ZB_RUN_DP_REORDER if dp_reorder else 0)
+            (ZB_RUN_DP_REORDER if dp_reorder else 0) | (ZB_RUN_GRAPH if graph else 0)
         tp = tokens.ctypes.data if host_inputs and tokens is not None else _ptr(tokens)
         lp = labels.ctypes.data if host_inputs and labels is not None else _ptr(labels)
         check(lib.zb_run_iteration(self.h, passes, len(passes), tp, lp, flags))

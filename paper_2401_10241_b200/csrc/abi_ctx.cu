@@ -6,6 +6,7 @@
 #include "abi_util.h"
 #include "comm.h"
 #include "gemm.h"
+#include "ktimer.h"
 #include "stage.h"
 
 using namespace zb;
@@ -297,6 +298,11 @@ static void stage_inputs(Ctx& c, const int32_t*& tokens, const int32_t*& labels,
   if (c.last && !labels) throw Error(ZB_EINVAL, "labels required on the last stage");
 }
 
+static void run_iteration_passes(Ctx* c, const zb_pass_t* passes, int32_t n, const int32_t* tokens,
+                                 const int32_t* labels, int32_t flags);
+static void run_iteration_graph(Ctx& c, const zb_pass_t* passes, int32_t n, const int32_t* tokens,
+                                const int32_t* labels, int32_t flags);
+
 extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, int32_t n, const int32_t* tokens,
                                         const int32_t* labels, int32_t flags) {
   ZB_TRY {
@@ -309,6 +315,22 @@ extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, 
     }
     if (c->cfg.p != 1) return set_error(ZB_EINVAL, "p > 1 needs zb_ctx_attach_nccl or zb_run_iteration_local");
     stage_inputs(*c, tokens, labels, flags);
+    // (the legacy default stream cannot be captured: contexts on it run eagerly)
+    if ((flags & ZB_RUN_GRAPH) && !(flags & ZB_RUN_TIMING) && !ktimer::enabled() && c->stream != nullptr &&
+        c->stream != cudaStreamLegacy && c->stream != cudaStreamPerThread) {
+      run_iteration_graph(*c, passes, n, tokens, labels, flags);
+      return ZB_OK;
+    }
+    run_iteration_passes(c, passes, n, tokens, labels, flags);
+    return ZB_OK;
+  }
+  ZB_CATCH
+}
+
+// The launches of one single-stage iteration (zb_run_iteration, p = 1, no NCCL).
+static void run_iteration_passes(Ctx* c, const zb_pass_t* passes, int32_t n, const int32_t* tokens,
+                                 const int32_t* labels, int32_t flags) {
+  {
     begin_iteration(*c);
     const int T = c->T;
     c->n_timed = 0;
@@ -339,9 +361,63 @@ extern "C" zb_status_t zb_run_iteration(zb_ctx_t* ctx, const zb_pass_t* passes, 
         c->backward_input(q.microbatch, q.slot, nullptr, nullptr);
       if (flags & ZB_RUN_TIMING) c->timing_end(c->n_timed++);
     }
-    return ZB_OK;
   }
-  ZB_CATCH
+}
+
+// ZB_RUN_GRAPH: replay the captured iteration while its key (pass list, flags, input pointers)
+// is unchanged.  A new key runs eagerly once (lazy per-stream buffers of the GEMM / column-sum
+// paths are sized outside any capture), the next call with the same key captures (relaxed
+// mode, the split-K counters restarted inside the graph) and launches the graph.
+static void run_iteration_graph(Ctx& c, const zb_pass_t* passes, int32_t n, const int32_t* tokens,
+                                const int32_t* labels, int32_t flags) {
+  const size_t nt = static_cast<size_t>(c.cfg.m) * c.T;
+  if (c.first && tokens != c.tok_stage) {  // per-step device inputs -> the fixed staging buffers
+    ZB_CUDA(cudaMemcpyAsync(c.tok_stage, tokens, nt * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+    tokens = c.tok_stage;
+  }
+  if (c.last && labels != c.lab_stage) {
+    ZB_CUDA(cudaMemcpyAsync(c.lab_stage, labels, nt * sizeof(int32_t), cudaMemcpyDeviceToDevice, c.stream));
+    labels = c.lab_stage;
+  }
+  Ctx::IterGraph& G = c.graph;
+  const int key_flags = flags & ~ZB_RUN_HOST_INPUTS;
+  const bool same = G.flags == key_flags && G.tok == tokens && G.lab == labels &&
+                    G.passes.size() == static_cast<size_t>(n) &&
+                    std::memcmp(G.passes.data(), passes, sizeof(zb_pass_t) * n) == 0;
+  if (!same) {
+    if (G.exec) ZB_CUDA(cudaGraphExecDestroy(G.exec));
+    G.exec = nullptr;
+    G.captured = false;
+    G.passes.assign(passes, passes + n);
+    G.flags = key_flags;
+    G.tok = tokens;
+    G.lab = labels;
+    run_iteration_passes(&c, passes, n, tokens, labels, flags);
+    return;
+  }
+  if (!G.captured) {
+    ZB_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+    const int64_t l0 = launch_count(false);
+    try {
+      gemm_graph_begin(c.stream);
+      run_iteration_passes(&c, passes, n, tokens, labels, flags);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(c.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g = nullptr;
+    ZB_CUDA(cudaStreamEndCapture(c.stream, &g));
+    G.launches = launch_count(false) - l0;
+    add_launches(-G.launches);  // captured, not executed: counted per replay below
+    const cudaError_t e = cudaGraphInstantiate(&G.exec, g, 0);
+    cudaGraphDestroy(g);
+    ZB_CUDA(e);
+    G.captured = true;
+  }
+  ZB_CUDA(cudaGraphLaunch(G.exec, c.stream));
+  add_launches(G.launches);
 }
 
 extern "C" zb_status_t zb_ctx_attach_nccl_chunks(zb_ctx_t* const* chunks, int32_t k, const void* ids, int32_t nv,

@@ -926,6 +926,17 @@ static void split_k_plan(int tiles, int nk, int pairs, cudaStream_t st, EpiArgs&
   f.base += best;
 }
 
+// start of a CUDA-graph capture on st (ZB_RUN_GRAPH): the ordered split-K counters restart
+// from 0 inside the graph (a memset node), so every replay sees the flag bases it was captured
+// with; eager launches after it continue above the captured bases
+void gemm_graph_begin(cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_split_mu);
+  SplitFlags& f = g_split_bufs[st];
+  if (!f.dev) return;  // no split-K launch has run on st yet: the capture never allocates (eager first)
+  ZB_CUDA(cudaMemsetAsync(f.dev, 0, sizeof(int32_t) * 16 * kMaxFlagTiles, st));
+  f.base = 0;
+}
+
 // per-split bias partials of a column-sum W GEMM (stream-private, grown on demand; the
 // previous user on the same stream has finished before the next GEMM reads / writes it)
 static float* bias_partials(cudaStream_t st, size_t n, int32_t** tickets, int blocks) {

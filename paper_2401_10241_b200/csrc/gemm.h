@@ -79,6 +79,10 @@ struct GemmArgs {
 // Throws zb::CudaError on launch failure / unsupported shapes.
 void gemm(const GemmArgs& g, DType dt, cudaStream_t stream);
 
+// a CUDA-graph capture of launches on stream starts (ZB_RUN_GRAPH): restart the ordered
+// split-K flag counters of that stream inside the graph
+void gemm_graph_begin(cudaStream_t stream);
+
 // number of SMs of the current device (cached)
 int num_sms();
 

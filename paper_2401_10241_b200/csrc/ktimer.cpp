@@ -12,6 +12,7 @@ namespace {
 std::atomic<int64_t> g_launches{0};
 }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int64_t launch_count(bool reset) { return reset ? g_launches.exchange(0) : g_launches.load(); }
 bool pdl_enabled(int cls) {
   static const int mask = [] {

@@ -11,6 +11,8 @@ namespace zb {
 
 // kernel launches of the library since the last reset (common.cuh launch())
 int64_t launch_count(bool reset);
+// kernel nodes of a replayed CUDA graph (counted like launches)
+void add_launches(int64_t n);
 
 namespace ktimer {
 

@@ -26,6 +26,7 @@
 namespace zb {
 
 Ctx::~Ctx() {
+  if (graph.exec) cudaGraphExecDestroy(graph.exec);
   for (auto e : ev_start) cudaEventDestroy(e);
   for (auto e : ev_end) cudaEventDestroy(e);
 }

@@ -109,6 +109,17 @@ struct Ctx {
 
   std::unique_ptr<Comm> comm;
 
+  // ZB_RUN_GRAPH: the captured iteration and its key (pass list, flags, staged inputs)
+  struct IterGraph {
+    std::vector<zb_pass_t> passes;
+    int flags = 0;
+    const int32_t *tok = nullptr, *lab = nullptr;
+    bool captured = false;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;  // kernel nodes of the graph (added to zb_dbg_launch_count per replay)
+  };
+  IterGraph graph;
+
   ~Ctx();
 
   // passes

@@ -14,7 +14,8 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="
 
 
 
-LN_SHAPES = [(6144, 2304), (3072, 4096), (1024, 6144), (37, 64), (2000, 264), (300, 2304)]
+LN_SHAPES = [(6144, 2304), (3072, 4096), (1024, 6144), (37, 64), (2000, 264), (300, 2304), (5, 4096), (149, 1024),
+             (3001, 3072)]
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])

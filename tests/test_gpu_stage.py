@@ -306,3 +306,53 @@ def test_head_weight_gradient_in_w_equals_eager(dtype):
         assert all(np.array_equal(x, y) for x, y in zip(a, b))
     esz = 2 if dtype == "bf16" else 4
     assert b0[0] == b1[0] and b0[-1] - b1[-1] >= cfg.T * cfg.V * esz
+
+
+# ------------------------------------------------------------------ CUDA-graph replay (ZB_RUN_GRAPH)
+
+def test_graph_replay_bitwise_equals_eager():
+    """zb_run_iteration with ZB_RUN_GRAPH: eager on a new key, captured on the second call,
+    replayed after that — loss, gradients and post-validated parameters bitwise equal to the
+    eager context's over several iterations with per-step device input buffers (staged into
+    the context), ordered split-K W GEMMs inside the graph (T = 2048: the W launches split K),
+    and a re-key when the pass list changes."""
+    import torch
+    from paper_2401_10241_b200 import api
+    from paper_2401_10241_b200._lib import lib
+    import ctypes as C
+    cfg = zb_synth.ModelConfig("graph", h=256, a=2, L=2, s=1024, b=2, V=512, p=1, m=3, family="zbh1")
+    opt = api.optim_cfg(lr=1e-3, mode="pv", clip=1.0)
+    runs = []
+    passes, sim = api.schedule("zbh1", 1, cfg.m, 10, 11, 6, 0, M_B=10, M_W=10)
+    passes_h2, sim2 = api.schedule("zbh2", 1, cfg.m, 10, 11, 6, 0, M_B=10, M_W=10)
+    for graph in (False, True):
+        stream = torch.cuda.Stream()  # a capturable stream (the legacy default stream is not)
+        c = api.Context(cfg, 1, 0, cfg.m, max(sim.n_slots[0], sim2.n_slots[0]), dtype="bf16", stream=stream)
+        params = zb_synth.make_stage_params(cfg, 1, 0)
+        c.set_params([params[n] for n, _, _ in zb_synth.param_specs(cfg, 1, 0)])
+        out = []
+        for it in range(5):
+            q = passes if it < 4 else passes_h2
+            tok, lab = inputs(cfg, it)
+            with torch.cuda.stream(stream):
+                tok_d = torch.from_numpy(tok).cuda()
+                lab_d = torch.from_numpy(lab).cuda()
+            n0 = C.c_int64()
+            lib.zb_dbg_launch_count(1, C.byref(n0))
+            c.run_iteration(q, tok_d, lab_d, graph=graph)
+            n1 = C.c_int64()
+            lib.zb_dbg_launch_count(0, C.byref(n1))
+            loss = c.loss()
+            grads = [g.copy() for g in c.get_grads()]
+            c.post_validate_step(opt)
+            c.post_validate_finish(opt)
+            out.append((loss, grads, [v.copy() for v in c.get_params()], int(n1.value)))
+        runs.append(out)
+        c.close()
+    for it, (e, g) in enumerate(zip(*runs)):
+        assert e[0] == g[0], (it, e[0], g[0])
+        for a, b in zip(e[1], g[1]):
+            assert np.array_equal(a, b), it
+        for a, b in zip(e[2], g[2]):
+            assert np.array_equal(a, b), it
+        assert e[3] == g[3] > 0, (it, e[3], g[3])  # a replay counts its kernel nodes
