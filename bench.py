@@ -411,6 +411,14 @@ def run_single(args, cfg, headline=True):
     ctx.close()
     del ctx
     torch.cuda.empty_cache()
+    # ---- size context for the HBM classes: a same-size copy's bandwidth per launch
+    for v in hbm["classes"].values():
+        if v.get("launches_per_step") and v.get("bytes_per_step"):
+            cg = same_size_copy_gbs(v["bytes_per_step"] / v["launches_per_step"])
+            v["bytes_per_launch"] = round(v["bytes_per_step"] / v["launches_per_step"])
+            v["same_size_copy_gbs"] = round(cg, 1)
+            v["frac_of_same_size_copy"] = round(v["gbs"] / cg, 4) if cg else None
+    torch.cuda.empty_cache()
     # ---- roofline of the dominant kernel (the GEMM family)
     peaks, src = read_peaks()
     g = kstats["gemm"]
@@ -555,6 +563,29 @@ def hbm_classes(lib, steps, ms_ev):
                                        "note": "post-validation launch, predicated off on clean steps (no bytes)"}
     return {"unit": "GB/s (algorithmic bytes / event time)", "peak": peak, "peak_source": f"{src} hbm_gbs",
             "classes": out}
+
+
+def same_size_copy_gbs(nbytes, iters=20):
+    """Bandwidth of a torch device copy moving the same bytes per launch as an HBM-class
+    kernel (half read, half written; rotating over buffers larger than L2): the achievable
+    rate for a transfer of that size, reported beside the fraction of the 2 GB-copy peak."""
+    import torch
+    half = max(1 << 20, min(int(nbytes // 2), 1 << 30))
+    nb = max(2, -(-(320 << 20) // half))
+    src = [torch.empty(half, dtype=torch.uint8, device="cuda") for _ in range(nb)]
+    dst = [torch.empty(half, dtype=torch.uint8, device="cuda") for _ in range(nb)]
+    for i in range(3):
+        dst[i % nb].copy_(src[i % nb])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for i in range(iters):
+        dst[i % nb].copy_(src[i % nb])
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    del src, dst
+    return 2 * half / (ms / 1e3) / 1e9
 
 
 def gemm_traffic(model):

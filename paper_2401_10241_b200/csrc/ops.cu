@@ -39,13 +39,13 @@ __device__ __forceinline__ void block_sum2(float& a, float& b, float* red) {
 }
 
 // ---------------------------------------------------------------- LayerNorm forward
-template <typename T, int VPT>
-__global__ void __launch_bounds__(LN_THREADS) k_ln_fwd(const T* __restrict__ x, const float* __restrict__ g,
+template <typename T, int VPT, int NT = LN_THREADS>
+__global__ void __launch_bounds__(NT) k_ln_fwd(const T* __restrict__ x, const float* __restrict__ g,
                                                       const float* __restrict__ b, T* __restrict__ y,
                                                       float* __restrict__ mean, float* __restrict__ rstd, int h,
                                                       float eps) {
   pdl_wait();
-  constexpr int NW = LN_THREADS / 32;
+  constexpr int NW = NT / 32;
   __shared__ float red[2 * NW];
   const int64_t row = blockIdx.x;
   const T* xr = x + row * h;
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_fwd(const T* __restrict__ x, 
   float s = 0.f, dummy = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int vi = threadIdx.x + k * LN_THREADS;
+    const int vi = threadIdx.x + k * NT;
     if (vi < nv) {
       Vec8<T>::load(xr + vi * 8, v[k]);
 #pragma unroll
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_fwd(const T* __restrict__ x, 
   dummy = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int vi = threadIdx.x + k * LN_THREADS;
+    const int vi = threadIdx.x + k * NT;
     if (vi < nv) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(LN_THREADS) k_ln_fwd(const T* __restrict__ x, 
   const float rs = rsqrtf(q / h + eps);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int vi = threadIdx.x + k * LN_THREADS;
+    const int vi = threadIdx.x + k * NT;
     if (vi < nv) {
       float gg[8], bb[8], o[8];
       Vec8<float>::load(g + vi * 8, gg);
@@ -877,6 +877,22 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
   } else if (vpl <= 12) {
     ln_fwd_warp<12>(dt, x, g, b, y, mean, rstd, rows, h, eps, st);
   } else {
+    static const int nt = [] {  // ZB_LN_FWD_NT=<128|256|512>: threads per row (measurement)
+      const char* e = getenv("ZB_LN_FWD_NT");
+      return e ? atoi(e) : 256;
+    }();
+    const int nv = h / 8;
+    if (dt == DT_BF16 && nt == 128 && nv <= 128 * 6) {
+      if (nv <= 128 * 4)
+        launch(PDL_OPS, k_ln_fwd<bf16, 4, 128>, rows, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
+      else
+        launch(PDL_OPS, k_ln_fwd<bf16, 6, 128>, rows, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
+    } else if (dt == DT_BF16 && nt == 512 && nv <= 512 * 2) {
+      if (nv <= 512)
+        launch(PDL_OPS, k_ln_fwd<bf16, 1, 512>, rows, 512, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
+      else
+        launch(PDL_OPS, k_ln_fwd<bf16, 2, 512>, rows, 512, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
+    } else
     ln_dispatch<0>(h, [&](auto V) {
       constexpr int VPT = decltype(V)::value;
       if (dt == DT_BF16)
