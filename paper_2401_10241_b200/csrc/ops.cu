@@ -877,21 +877,12 @@ void layernorm_fwd(DType dt, const void* x, const float* g, const float* b, void
   } else if (vpl <= 12) {
     ln_fwd_warp<12>(dt, x, g, b, y, mean, rstd, rows, h, eps, st);
   } else {
-    static const int nt = [] {  // ZB_LN_FWD_NT=<128|256|512>: threads per row (measurement)
-      const char* e = getenv("ZB_LN_FWD_NT");
-      return e ? atoi(e) : 256;
-    }();
-    const int nv = h / 8;
-    if (dt == DT_BF16 && nt == 128 && nv <= 128 * 6) {
-      if (nv <= 128 * 4)
-        launch(PDL_OPS, k_ln_fwd<bf16, 4, 128>, rows, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
-      else
-        launch(PDL_OPS, k_ln_fwd<bf16, 6, 128>, rows, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
-    } else if (dt == DT_BF16 && nt == 512 && nv <= 512 * 2) {
-      if (nv <= 512)
-        launch(PDL_OPS, k_ln_fwd<bf16, 1, 512>, rows, 512, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
-      else
-        launch(PDL_OPS, k_ln_fwd<bf16, 2, 512>, rows, 512, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y), mean, rstd, h, eps);
+    // h in (3072, 4096] (bf16): 128 threads of 4 vectors per row measured 15.8 vs 16.7 us
+    // for 256 x 2 at 3072 x 4096 (512 threads: 20.8); wider rows stay at 256 threads
+    // (h = 5120: 19.2 vs 20.7 us for 128 threads) — profiles/r02_ln_fwd_threads_per_row.jsonl
+    if (dt == DT_BF16 && h / 8 <= 128 * 4) {
+      launch(PDL_OPS, k_ln_fwd<bf16, 4, 128>, rows, 128, 0, st, static_cast<const bf16*>(x), g, b, static_cast<bf16*>(y),
+             mean, rstd, h, eps);
     } else
     ln_dispatch<0>(h, [&](auto V) {
       constexpr int VPT = decltype(V)::value;
