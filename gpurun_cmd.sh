@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/final_gpu_tests.log 2>&1; echo "rc $?" >> gpurun_out/final_gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final_smoke.log 2>&1; echo "rc $?" >> gpurun_out/final_smoke.log
-timeout 900 python bench.py > gpurun_out/final_bench.log 2>&1; echo "rc $?" >> gpurun_out/final_bench.log
-timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/final_ref.log 2>&1; echo "rc $?" >> gpurun_out/final_ref.log
-tail -3 gpurun_out/final_gpu_tests.log; tail -2 gpurun_out/final_smoke.log; tail -c 400 gpurun_out/final_bench.log; tail -c 400 gpurun_out/final_ref.log
+ZB_GEMM_CHINT=8 timeout 900 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_wgroup.py -q -x -p no:cacheprovider > gpurun_out/la_tests.log 2>&1; echo "rc $?" >> gpurun_out/la_tests.log
+for h in 0 8 0 8; do echo "# CHINT $h" >> gpurun_out/w_loadadd.jsonl; ZB_GEMM_CHINT=$h timeout 600 python scripts/gemm_w_c3.py --secs 1.0 >> gpurun_out/w_loadadd.jsonl 2>&1; done
+tail -3 gpurun_out/la_tests.log; cat gpurun_out/w_loadadd.jsonl
