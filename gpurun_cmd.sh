@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/delta_perf2.jsonl
-for v in new old new old; do echo "# delta $v" >> gpurun_out/delta_perf2.jsonl; if [ $v = old ]; then export ZB_DELTA_OLD=1; else unset ZB_DELTA_OLD; fi; timeout 300 python scripts/attn_perf.py >> gpurun_out/delta_perf2.jsonl 2>&1; done
-cat gpurun_out/delta_perf2.jsonl
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -x -p no:cacheprovider -k bench_config > gpurun_out/full6.log 2>&1; echo "rc $?" >> gpurun_out/full6.log
+timeout 300 python scripts/attn_fwd_item_trace.py > gpurun_out/fwd_items.txt 2>&1
+tail -3 gpurun_out/full6.log; cat gpurun_out/fwd_items.txt

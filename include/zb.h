@@ -192,7 +192,8 @@ zb_status_t zb_ctx_param_count(zb_ctx_t* ctx, int32_t* n);
 zb_status_t zb_ctx_param_numel(zb_ctx_t* ctx, int64_t* numel /* [n] */);
 /* Upload host f32 parameters (canonical order); resets AdamW state and t. */
 zb_status_t zb_ctx_set_params(zb_ctx_t* ctx, const float* const* host_params, int32_t n);
-/* Download f32 master parameters / accumulated f32 gradients / AdamW moments (syncs). */
+/* Download f32 master parameters / accumulated f32 gradients / AdamW moments (syncs).
+ * A NULL entry of host_out skips that tensor (sampled reads of large models). */
 zb_status_t zb_ctx_get_params(zb_ctx_t* ctx, float* const* host_out, int32_t n);
 zb_status_t zb_ctx_get_grads(zb_ctx_t* ctx, float* const* host_out, int32_t n);
 zb_status_t zb_ctx_get_moments(zb_ctx_t* ctx, float* const* host_m, float* const* host_v, int32_t n);

@@ -188,17 +188,19 @@ class Context:
         ptrs = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
         check(lib.zb_ctx_set_params(self.h, ptrs, len(arrs)))
 
-    def _get(self, fn) -> List[np.ndarray]:
-        outs = [np.empty(n, dtype=np.float32) for n in self.numel]
-        ptrs = (C.c_void_p * len(outs))(*[a.ctypes.data for a in outs])
+    def _get(self, fn, only=None) -> List[Optional[np.ndarray]]:
+        """All tensors, or (only = indices) just those; the others come back as None."""
+        outs = [np.empty(n, dtype=np.float32) if only is None or i in only else None
+                for i, n in enumerate(self.numel)]
+        ptrs = (C.c_void_p * len(outs))(*[a.ctypes.data if a is not None else None for a in outs])
         check(fn(self.h, ptrs, len(outs)))
         return outs
 
-    def get_params(self):
-        return self._get(lib.zb_ctx_get_params)
+    def get_params(self, only=None):
+        return self._get(lib.zb_ctx_get_params, only)
 
-    def get_grads(self):
-        return self._get(lib.zb_ctx_get_grads)
+    def get_grads(self, only=None):
+        return self._get(lib.zb_ctx_get_grads, only)
 
     def get_moments(self):
         ms = [np.empty(n, dtype=np.float32) for n in self.numel]

@@ -195,8 +195,9 @@ static zb_status_t get_flat(zb_ctx_t* ctx, const float* src_base_sel, float* con
   if (n != static_cast<int32_t>(c->params.size())) return set_error(ZB_EINVAL, "wrong parameter count");
   ZB_CUDA(cudaStreamSynchronize(c->stream));
   for (int i = 0; i < n; ++i)
-    ZB_CUDA(cudaMemcpy(host[i], src_base_sel + c->params[i].off, sizeof(float) * c->params[i].numel,
-                       cudaMemcpyDeviceToHost));
+    if (host[i])  // a NULL entry skips that tensor
+      ZB_CUDA(cudaMemcpy(host[i], src_base_sel + c->params[i].off, sizeof(float) * c->params[i].numel,
+                         cudaMemcpyDeviceToHost));
   return ZB_OK;
 }
 

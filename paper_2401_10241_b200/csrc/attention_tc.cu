@@ -33,6 +33,18 @@ __device__ __forceinline__ void trf(int row, int n) {
   }
 }
 #define TRF(row, n) trf(row, n)
+// per-item events of CTA 0 (persistent walk): row e, column = item index r of the CTA
+//  0 MMA: first S issued   1 MMA: last PV issued   2/3 tile 0/1 softmax: S(0) ready
+//  4/5 tile 0/1: last P stored   6/7 tile 0/1: O final seen   8/9 tile 0/1: O stored
+__device__ unsigned long long g_item_fwd[10][16];
+__device__ __forceinline__ void tri(int e, int r) {
+  if (blockIdx.x == 0 && r < 16) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_item_fwd[e][r] = t;
+  }
+}
+#define TRI(e, r) tri(e, r)
 // every CTA: {smid, start, end} (globaltimer ns) — CTA durations and per-SM gaps
 __device__ unsigned long long g_cta_fwd[8192][3];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -42,6 +54,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #else
 #define TRF(row, n)
+#define TRI(e, r)
 #endif
 
 constexpr int BQ = 128, BKV = 128;
@@ -268,6 +281,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         sm100::mbar_wait_warp(q_full, r & 1);
         sm100::mbar_wait_warp(&k_full[kn & 1], (kn >> 1) & 1);
         sm100::tc_fence_after();
+        if (lane == 0) TRI(0, r);
         issue_s(0, kn & 1);
         if (w.two) issue_s(1, kn & 1);
         if (sm100::elect_one()) sm100::mma_commit(&k_empty[kn & 1]);
@@ -283,6 +297,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
             if (j == w.nkv0 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[0]); }
           }
           if (j + 1 < w.nkv0) issue_s(0, kn & 1);
+          if (j + 1 == nkv && lane == 0) TRI(1, r);
           if (j < w.nkv1) {
             issue_pv(1, j, vst);
             if (j == w.nkv1 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[1]); }
@@ -311,6 +326,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       float m = -INFINITY, l = 0.f;  // m: reference max (log2 units), l: running sum relative to m
       for (int j = 0; j < nk; ++j, ++sb) {
         sm100::mbar_wait(&s_full[t], sb & 1);
+        if ((warp & 3) == 0 && lane == 0 && j == 0) TRI(2 + t, rr);
         if ((warp & 3) == 0 && lane == 0 && rr == 0) TRF(2 + 3 * t, j);
         sm100::tc_fence_after();
         float sv[128];
@@ -394,9 +410,11 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         sm100::tc_fence_before();
         if ((warp & 3) == 0 && lane == 0 && rr == 0) TRF(4 + 3 * t, j);
         sm100::mbar_arrive_warp(&p_full[t]);
+        if ((warp & 3) == 0 && lane == 0 && j + 1 == nk) TRI(4 + t, rr);
       }
       if (nk > 0) {
         sm100::mbar_wait(&o_final[t], ni & 1);
+        if ((warp & 3) == 0 && lane == 0) TRI(6 + t, rr);
         ++ni;
         sm100::tc_fence_after();
         const int q = qt * BQ + r_;
@@ -420,6 +438,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         }
         sm100::tc_fence_before();
         sm100::mbar_arrive_warp(&o_empty[t]);  // O_t may be overwritten by the next item's PV
+        if ((warp & 3) == 0 && lane == 0) TRI(8 + t, rr);
         lse[(static_cast<int64_t>(w.bb) * a + w.hd) * s + q] = (m + log2f(l)) * LN2;
       }
     }
@@ -472,6 +491,9 @@ bool attention_fwd_tc(const AttnShape& sh, const void* qkv, void* o, float* lse,
 #ifdef ZB_ATTN_TRACE
 extern "C" int zb_dbg_attn_fwd_cta_trace(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_cta_fwd, sizeof(unsigned long long) * 8192 * 3));
+}
+extern "C" int zb_dbg_attn_fwd_item_trace(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_item_fwd, sizeof(unsigned long long) * 10 * 16));
 }
 extern "C" int zb_dbg_attn_fwd_trace(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_tc::g_trace_fwd, sizeof(unsigned long long) * 12 * 64));
