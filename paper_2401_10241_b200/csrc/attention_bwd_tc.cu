@@ -56,6 +56,33 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// One 32-column chunk of the calling warp's 32 rows (v: this thread's row, f32, times mul) to
+// global memory through the warp's 2 KB staging buffer stg (64 B per row, 16-B piece k of row
+// i at piece k ^ ((i >> 1) & 3)): written one row per thread, stored 8 rows x 64 contiguous
+// bytes per instruction (a row-per-thread 16-B store touched 32 lines per instruction).
+// base: row 0 of the warp's rows, first column of the chunk; ld: row pitch in elements.
+__device__ __forceinline__ void store_chunk_staged(uint32_t stg, const uint32_t* v, float mul, bf16* base,
+                                                   int64_t ld, int lane) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const uint32_t x = pack_bf16(__uint_as_float(v[8 * g]) * mul, __uint_as_float(v[8 * g + 1]) * mul);
+    const uint32_t y = pack_bf16(__uint_as_float(v[8 * g + 2]) * mul, __uint_as_float(v[8 * g + 3]) * mul);
+    const uint32_t z = pack_bf16(__uint_as_float(v[8 * g + 4]) * mul, __uint_as_float(v[8 * g + 5]) * mul);
+    const uint32_t w = pack_bf16(__uint_as_float(v[8 * g + 6]) * mul, __uint_as_float(v[8 * g + 7]) * mul);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4)),
+                 "r"(x), "r"(y), "r"(z), "r"(w)
+                 : "memory");
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int idx = it * 32 + lane, i = idx >> 2, k = idx & 3;
+    const float4 f = sm100::lds128(stg + i * 64 + ((k ^ ((i >> 1) & 3)) << 4));
+    *reinterpret_cast<float4*>(base + static_cast<int64_t>(i) * ld + k * 8) = f;
+  }
+  __syncwarp();
+}
+
 // Row r (0..127) of a 128-row SWIZZLE_128B bf16 tile (D columns in 64-column atoms 16 KB apart,
 // 16-byte chunk c of row r stored at chunk c ^ (r & 7)) into TMEM lane r, columns
 // [taddr, taddr + D/2) as packed bf16 pairs (low half = even column): the A-operand layout of a
@@ -105,7 +132,8 @@ template <int D> struct DkdvCfg {
   static constexpr int STAGE = 2 * Q_TILE + 1024;  // Q_i, dO_i, L_i[64], D_i[64] (1024-aligned)
   static constexpr int OFF_K = 0, OFF_V = KV_TILE, OFF_ST = 2 * KV_TILE;
   static constexpr int OFF_BAR = OFF_ST + ST * STAGE;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_OST = OFF_BAR + 1024;  // epilogue staging: 8 elementwise warps x 2 KB
+  static constexpr int SMEM = OFF_OST + 8 * 2048 + 1024;
 };
 
 // Persistent over this CTA's dK/dV items (key block kb = level, head, sequence): barriers,
@@ -382,32 +410,17 @@ __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensor
       sm100::mbar_wait(o_final, ri & 1);
       if (warp == 4 && lane == 0 && ri == 0) TR(6, 1);
       sm100::tc_fence_after();
-      bf16* row = dqkv + (static_cast<int64_t>(row0) + key) * (3 * h) + hd * D;
+      (void)key;
+      bf16* wrow = dqkv + (static_cast<int64_t>(row0) + kb * 128 + qw * 32) * (3 * h) + hd * D;  // warp's row 0
+      const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 2048;
 #pragma unroll 1
       for (int c = hf; c < D / 32; c += 2) {
-        uint32_t v[32];
+        uint32_t v[32], u[32];  // dK and dV chunk loads in flight together, one wait
         sm100::tmem_ld32(t_dk + lane_off + c * 32, v);
+        sm100::tmem_ld32(t_dv + lane_off + c * 32, u);
         sm100::tmem_ld_wait();
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint4 u;
-          u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
-          u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
-          u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
-          u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
-          *reinterpret_cast<uint4*>(row + h + c * 32 + g * 8) = u;
-        }
-        sm100::tmem_ld32(t_dv + lane_off + c * 32, v);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint4 u;
-          u.x = pack_bf16(__uint_as_float(v[8 * g]), __uint_as_float(v[8 * g + 1]));
-          u.y = pack_bf16(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
-          u.z = pack_bf16(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
-          u.w = pack_bf16(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
-          *reinterpret_cast<uint4*>(row + 2 * h + c * 32 + g * 8) = u;
-        }
+        store_chunk_staged(stg, v, scale, wrow + h + c * 32, 3 * h, lane);
+        store_chunk_staged(stg, u, 1.f, wrow + 2 * h + c * 32, 3 * h, lane);
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive_warp(o_empty);  // dK / dV may be overwritten by the next item
@@ -436,7 +449,8 @@ template <int D> struct DqCfg {
   static constexpr int STAGE = 2 * KV_TILE;      // K_j, V_j
   static constexpr int OFF_Q = 0, OFF_DO = Q_TILE, OFF_ST = 2 * Q_TILE;
   static constexpr int OFF_BAR = OFF_ST + ST * STAGE;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_OST = OFF_BAR + 1024;  // epilogue staging: 8 elementwise warps x 2 KB
+  static constexpr int SMEM = OFF_OST + 8 * 2048 + 1024;
 };
 
 // Persistent over this CTA's dQ items (query block nqb-1-level, head, sequence); running
@@ -644,21 +658,14 @@ __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap
       }
       sm100::mbar_wait(o_final, ri & 1);
       sm100::tc_fence_after();
-      bf16* row = dqkv + (static_cast<int64_t>(bb) * s + q) * (3 * h) + hd * D;
+      bf16* wrow = dqkv + (static_cast<int64_t>(bb) * s + qb * 128 + qw * 32) * (3 * h) + hd * D;  // warp's row 0
+      const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 2048;
 #pragma unroll 1
       for (int c = hf; c < D / 32; c += 2) {
         uint32_t v[32];
         sm100::tmem_ld32(t_dq + lane_off + c * 32, v);
         sm100::tmem_ld_wait();
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint4 u;
-          u.x = pack_bf16(__uint_as_float(v[8 * g]) * scale, __uint_as_float(v[8 * g + 1]) * scale);
-          u.y = pack_bf16(__uint_as_float(v[8 * g + 2]) * scale, __uint_as_float(v[8 * g + 3]) * scale);
-          u.z = pack_bf16(__uint_as_float(v[8 * g + 4]) * scale, __uint_as_float(v[8 * g + 5]) * scale);
-          u.w = pack_bf16(__uint_as_float(v[8 * g + 6]) * scale, __uint_as_float(v[8 * g + 7]) * scale);
-          *reinterpret_cast<uint4*>(row + c * 32 + g * 8) = u;
-        }
+        store_chunk_staged(stg, v, scale, wrow + c * 32, 3 * h, lane);
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive_warp(o_empty);  // dQ may be overwritten by the next item

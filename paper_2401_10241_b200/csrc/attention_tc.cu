@@ -88,8 +88,9 @@ template <int D> struct FwdCfg {
   static constexpr int OFF_K = 2 * TILE;
   static constexpr int OFF_V = (2 + KST) * TILE;
   static constexpr int OFF_BAR = (2 + KST + VST) * TILE;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static_assert((18 + 2 * (PQ - 1) + 1) * 8 <= 256, "barrier area");
+  static constexpr int OFF_OST = OFF_BAR + 1024;        // O epilogue staging: 8 softmax warps x 4 KB
+  static constexpr int SMEM = OFF_OST + 8 * 4096 + 1024;
+  static_assert((18 + 2 * (PQ - 1) + 3) * 8 <= 256, "barrier area");
 };
 
 // Persistent: one CTA per SM walks work items (pair of 128-query tiles {2t, 2t+1}, head,
@@ -129,7 +130,13 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 15);
   uint64_t* o_empty = bar + 16;   // [2] per tile: the softmax warps have read O_t of their item
   uint64_t* p_part = bar + 18;    // [2][PQ - 1] per tile: P of keys [0, 32 (q + 1)) stored (PV may start)
-  uint64_t* q_empty = bar + 18 + 2 * (PQ - 1);  // the item's last S product has read Q
+  // per tile t: q_full[t] Q_t landed; q_empty[t] the item's last S_t product has read Q_t (tile 0's
+  // buffer is refilled for the next item while tile 1 still runs its last block)
+  uint64_t* q_empty0 = bar + 18 + 2 * (PQ - 1);
+  uint64_t* q_full1 = q_empty0 + 1;
+  uint64_t* q_empty1 = q_empty0 + 2;
+  uint64_t* q_fulls[2] = {q_full, q_full1};
+  uint64_t* q_empties[2] = {q_empty0, q_empty1};
 
 #ifdef ZB_ATTN_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 8192) {
@@ -167,8 +174,10 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   };
 
   if (threadIdx.x == 0) {
-    sm100::mbar_init(q_full, 1);
-    sm100::mbar_init(q_empty, 1);
+    for (int t = 0; t < 2; ++t) {
+      sm100::mbar_init(q_fulls[t], 1);
+      sm100::mbar_init(q_empties[t], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&k_full[i], 1);
       sm100::mbar_init(&k_empty[i], 1);
@@ -194,16 +203,19 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA
       int kn = 0, vn = 0;  // K / V ring positions (continuous over items)
+      int qn[2] = {0, 0};  // Q_t loads issued
       for (int r = 0, it; (it = item_of(r)) >= 0; ++r) {
         const Item w = decode(it);
         const int row0 = w.bb * s;
         const int nkv = w.two ? w.nkv1 : w.nkv0;
-        sm100::mbar_wait(q_empty, (r & 1) ^ 1);  // the previous item's S products are done with Q
-        sm100::mbar_arrive_expect_tx(q_full, (w.two ? 2 : 1) * C::TILE);
-        for (int t = 0; t < (w.two ? 2 : 1); ++t)
+        auto load_q = [&](int t) {  // Q_t of this item once the previous item's last S_t has read it
+          sm100::mbar_wait(q_empties[t], (qn[t] & 1) ^ 1);
+          sm100::mbar_arrive_expect_tx(q_fulls[t], C::TILE);
           for (int at = 0; at < C::ATOMS; ++at)
-            sm100::tma_load_2d(smem + C::OFF_Q + t * C::TILE + at * 16384, &tm, q_full, w.hd * D + 64 * at,
+            sm100::tma_load_2d(smem + C::OFF_Q + t * C::TILE + at * 16384, &tm, q_fulls[t], w.hd * D + 64 * at,
                                row0 + (w.q0 + t) * BQ);
+          ++qn[t];
+        };
         auto load_k = [&](int j) {
           const int st = kn & 1;
           sm100::mbar_wait(&k_empty[st], ((kn >> 1) & 1) ^ 1);
@@ -222,7 +234,11 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
                                2 * h + w.hd * D + 64 * at, row0 + j * BKV);
           ++vn;
         };
+        // Q_0, K(0) first: the MMA warp issues this item's S_0(0) while the previous item's tile 1
+        // still finishes its last block; Q_1 waits for that block's S_1
+        load_q(0);
         load_k(0);
+        if (w.two) load_q(1);
         for (int j = 0; j < nkv; ++j) {  // K runs one block ahead of V
           if (j + 1 < nkv) load_k(j + 1);
           load_v(j);
@@ -237,11 +253,15 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
       int kn = 0, vn = 0;              // K / V ring positions
       int pb[2] = {0, 0};              // PV blocks issued per tile (P barrier parity)
       int ti[2] = {0, 0};              // items started per tile (o_empty parity)
+      int qm[2] = {0, 0};              // Q_t loads consumed (q_full parity)
+      bool pre = false;                // this item's S_0(0) was issued in the previous item's tail
+      int pre_left0 = 0;               // its remaining S_0 products after that
       for (int r = 0, it; (it = item_of(r)) >= 0; ++r) {
         const Item w = decode(it);
         const int nkv = w.two ? w.nkv1 : w.nkv0;
-        int s_left = w.nkv0 + w.nkv1;  // S products of the item still to issue (q_empty after the last)
-        auto issue_s = [&](int t, int stage) {  // S_t = Q_t K^T (K in ring stage `stage`)
+        // S_t products of the item still to issue; the last one commits q_empty[t]
+        int s_left[2] = {pre ? pre_left0 : w.nkv0, w.nkv1};
+        auto issue_s = [&](int t, int stage, int& left) {  // S_t = Q_t K^T (K in ring stage `stage`)
           const uint32_t sk = sm100::smem_addr(smem + C::OFF_K + stage * C::TILE);
           const uint64_t qd = sm100::smem_desc(sq + t * C::TILE, 16, 1024, sm100::kSwizzle128B);
           const uint64_t kd = sm100::smem_desc(sk, 16, 1024, sm100::kSwizzle128B);
@@ -252,7 +272,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
                                kk != 0 ? 1u : 0u);
           }
           if (sm100::elect_one()) sm100::mma_commit(&s_full[t]);
-          if (--s_left == 0) { if (sm100::elect_one()) sm100::mma_commit(q_empty); }
+          if (--left == 0) { if (sm100::elect_one()) sm100::mma_commit(q_empties[t]); }
         };
         auto issue_pv = [&](int t, int j, int stage) {  // O_t += P_t V_j, the first keys as soon as their P is stored
           const uint32_t sv = sm100::smem_addr(smem + C::OFF_V + stage * C::TILE);
@@ -278,13 +298,22 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
           }
           ++pb[t];
         };
-        sm100::mbar_wait_warp(q_full, r & 1);
-        sm100::mbar_wait_warp(&k_full[kn & 1], (kn >> 1) & 1);
-        sm100::tc_fence_after();
-        if (lane == 0) TRI(0, r);
-        issue_s(0, kn & 1);
-        if (w.two) issue_s(1, kn & 1);
-        if (sm100::elect_one()) sm100::mma_commit(&k_empty[kn & 1]);
+        if (!pre) {
+          sm100::mbar_wait_warp(q_fulls[0], qm[0] & 1);
+          ++qm[0];
+          sm100::mbar_wait_warp(&k_full[kn & 1], (kn >> 1) & 1);
+          sm100::tc_fence_after();
+          if (lane == 0) TRI(0, r);
+          issue_s(0, kn & 1, s_left[0]);
+        }
+        pre = false;
+        if (w.two) {
+          sm100::mbar_wait_warp(q_fulls[1], qm[1] & 1);
+          ++qm[1];
+          sm100::tc_fence_after();
+          issue_s(1, kn & 1, s_left[1]);
+        }
+        if (sm100::elect_one()) sm100::mma_commit(&k_empty[kn & 1]);  // after both S(0) products
         ++kn;
         for (int j = 0; j < nkv; ++j) {
           const bool more = j + 1 < nkv;
@@ -296,15 +325,32 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
             issue_pv(0, j, vst);
             if (j == w.nkv0 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[0]); }
           }
-          if (j + 1 < w.nkv0) issue_s(0, kn & 1);
+          if (j + 1 < w.nkv0) issue_s(0, kn & 1, s_left[0]);
           if (j + 1 == nkv && lane == 0) TRI(1, r);
+          if (j + 1 == nkv && w.two) {
+            // item tail: tile 0 is done (PV_0 of its last block issued, so S_0's TMEM is free in
+            // issue order) while tile 1's last softmax runs — issue the NEXT item's S_0(0) now, so
+            // its tile-0 softmax overlaps this block instead of following it
+            const int it2 = item_of(r + 1);
+            if (it2 >= 0) {
+              const Item w2 = decode(it2);
+              sm100::mbar_wait_warp(q_fulls[0], qm[0] & 1);
+              ++qm[0];
+              sm100::mbar_wait_warp(&k_full[kn & 1], (kn >> 1) & 1);
+              sm100::tc_fence_after();
+              if (lane == 0) TRI(0, r + 1);
+              pre_left0 = w2.nkv0;
+              issue_s(0, kn & 1, pre_left0);
+              pre = true;
+            }
+          }
           if (j < w.nkv1) {
             issue_pv(1, j, vst);
             if (j == w.nkv1 - 1) { if (sm100::elect_one()) sm100::mma_commit(&o_final[1]); }
           }
           if (sm100::elect_one()) sm100::mma_commit(&v_empty[vst]);
           ++vn;
-          if (j + 1 < w.nkv1) issue_s(1, kn & 1);
+          if (j + 1 < w.nkv1) issue_s(1, kn & 1, s_left[1]);
           if (more) {
             if (sm100::elect_one()) sm100::mma_commit(&k_empty[kn & 1]);
             ++kn;
@@ -419,22 +465,47 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         sm100::tc_fence_after();
         const int q = qt * BQ + r_;
         const float inv = 1.f / l;
-        bf16* orow = o + (static_cast<int64_t>(w.bb) * s + q) * h + w.hd * D;
+        // O rows leave through a warp-private staging buffer (this warp's 32 rows x 64 columns,
+        // 128 B per row, 16-B chunk k of row i at chunk k ^ (i & 7)): written one row per
+        // thread, read back row-contiguous, so every global store instruction covers whole
+        // 128-B lines (row-per-thread 16-B stores touched 32 lines each: ~2 us per tile,
+        // profiles/r02_attn_fwd_item_trace_before.txt)
+        const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;
+        bf16* obase = o + (static_cast<int64_t>(w.bb) * s + qt * BQ + (warp & 3) * 32) * h + w.hd * D;
 #pragma unroll 1
-        for (int c4 = 0; c4 < D / 32; ++c4) {
-          uint32_t ov[32];
-          sm100::tmem_ld32(t_o + c4 * 32, ov);
+        for (int h0 = 0; h0 < D; h0 += 64) {
+          const int nc = D - h0 < 64 ? D - h0 : 64;  // 64, or 32 for the last columns at d = 96
+          uint32_t ov[64];  // both 32-column loads in flight, one wait
+          sm100::tmem_ld32(t_o + h0, ov);
+          if (nc == 64) sm100::tmem_ld32(t_o + h0 + 32, ov + 32);
           sm100::tmem_ld_wait();
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            uint4 u;
-            __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
+          for (int c32 = 0; c32 < 64; c32 += 32) {
+            if (c32 < nc) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * g + 2 * e]) * inv,
-                                            __uint_as_float(ov[8 * g + 2 * e + 1]) * inv);
-            *reinterpret_cast<uint4*>(orow + c4 * 32 + g * 8) = u;
+              for (int g = 0; g < 4; ++g) {
+                uint4 u;
+                __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[c32 + 8 * g + 2 * e]) * inv,
+                                                __uint_as_float(ov[c32 + 8 * g + 2 * e + 1]) * inv);
+                const int k = c32 / 8 + g;
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((k ^ (lane & 7)) << 4)),
+                             "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+                             : "memory");
+              }
+            }
           }
+          __syncwarp();
+          const int cpr = nc / 8;  // 16-B chunks per row
+#pragma unroll 1
+          for (int it = 0; it < cpr; ++it) {
+            const int idx = it * 32 + lane, i = idx / cpr, k = idx % cpr;
+            const float4 f = sm100::lds128(stg + i * 128 + ((k ^ (i & 7)) << 4));
+            *reinterpret_cast<float4*>(obase + static_cast<int64_t>(i) * h + h0 + k * 8) = f;
+          }
+          __syncwarp();
         }
         sm100::tc_fence_before();
         sm100::mbar_arrive_warp(&o_empty[t]);  // O_t may be overwritten by the next item's PV
