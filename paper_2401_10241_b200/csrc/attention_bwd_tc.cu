@@ -415,12 +415,13 @@ __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensor
       const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 2048;
 #pragma unroll 1
       for (int c = hf; c < D / 32; c += 2) {
-        uint32_t v[32], u[32];  // dK and dV chunk loads in flight together, one wait
+        uint32_t v[32];
         sm100::tmem_ld32(t_dk + lane_off + c * 32, v);
-        sm100::tmem_ld32(t_dv + lane_off + c * 32, u);
         sm100::tmem_ld_wait();
         store_chunk_staged(stg, v, scale, wrow + h + c * 32, 3 * h, lane);
-        store_chunk_staged(stg, u, 1.f, wrow + 2 * h + c * 32, 3 * h, lane);
+        sm100::tmem_ld32(t_dv + lane_off + c * 32, v);
+        sm100::tmem_ld_wait();
+        store_chunk_staged(stg, v, 1.f, wrow + 2 * h + c * 32, 3 * h, lane);
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive_warp(o_empty);  // dK / dV may be overwritten by the next item

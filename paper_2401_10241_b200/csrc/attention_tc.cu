@@ -472,24 +472,23 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         // profiles/r02_attn_fwd_item_trace_before.txt)
         const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;
         bf16* obase = o + (static_cast<int64_t>(w.bb) * s + qt * BQ + (warp & 3) * 32) * h + w.hd * D;
-#pragma unroll 1
-        for (int h0 = 0; h0 < D; h0 += 64) {
+#pragma unroll
+        for (int h0 = 0; h0 < D; h0 += 64) {  // unrolled: nc is a compile-time 64 / 32 (no spills at d = 96)
           const int nc = D - h0 < 64 ? D - h0 : 64;  // 64, or 32 for the last columns at d = 96
-          uint32_t ov[64];  // both 32-column loads in flight, one wait
-          sm100::tmem_ld32(t_o + h0, ov);
-          if (nc == 64) sm100::tmem_ld32(t_o + h0 + 32, ov + 32);
-          sm100::tmem_ld_wait();
 #pragma unroll
           for (int c32 = 0; c32 < 64; c32 += 32) {
             if (c32 < nc) {
+              uint32_t ov[32];
+              sm100::tmem_ld32(t_o + h0 + c32, ov);
+              sm100::tmem_ld_wait();
 #pragma unroll
               for (int g = 0; g < 4; ++g) {
                 uint4 u;
                 __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                  hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[c32 + 8 * g + 2 * e]) * inv,
-                                                __uint_as_float(ov[c32 + 8 * g + 2 * e + 1]) * inv);
+                  hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * g + 2 * e]) * inv,
+                                                __uint_as_float(ov[8 * g + 2 * e + 1]) * inv);
                 const int k = c32 / 8 + g;
                 asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((k ^ (lane & 7)) << 4)),
                              "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
