@@ -42,6 +42,18 @@ __device__ __forceinline__ void tr(int row, int n) {
 }
 #define TR(row, n) tr(row, n)
 __device__ unsigned long long g_cta_bwd[16384][3];  // every CTA: {smid, start, end}
+// per-item events of CTA 0, warp 4 lane 0 (row = body * 5 + event, column = item of the body):
+// 0 item start (K / V or Q / dO resident), 1 first step's S ready, 2 last step published,
+// 3 final accumulator seen, 4 epilogue stored
+__device__ unsigned long long g_item_bwd[10][16];
+__device__ __forceinline__ void tri_b(int e, int r) {
+  if (blockIdx.x == 0 && r < 16) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_item_bwd[e][r] = t;
+  }
+}
+#define TRB(e, r) tri_b(e, r)
 __device__ __forceinline__ unsigned long long gtime_b() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -49,6 +61,7 @@ __device__ __forceinline__ unsigned long long gtime_b() {
 }
 #else
 #define TR(row, n)
+#define TRB(e, r)
 #endif
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -57,30 +70,36 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 // One 32-column chunk of the calling warp's 32 rows (v: this thread's row, f32, times mul) to
-// global memory through the warp's 2 KB staging buffer stg (64 B per row, 16-B piece k of row
-// i at piece k ^ ((i >> 1) & 3)): written one row per thread, stored 8 rows x 64 contiguous
-// bytes per instruction (a row-per-thread 16-B store touched 32 lines per instruction).
-// base: row 0 of the warp's rows, first column of the chunk; ld: row pitch in elements.
-__device__ __forceinline__ void store_chunk_staged(uint32_t stg, const uint32_t* v, float mul, bf16* base,
-                                                   int64_t ld, int lane) {
+// global memory by a TMA tensor store (box 32 rows x 64 B, SWIZZLE_64B: 16-B piece k of row i
+// at piece k ^ ((i >> 1) & 3)) from one of the warp's two 2 KB staging buffers (stg, stg +
+// 2048, alternating with nbuf).  The warp only writes shared memory and waits for the store
+// issued two chunks earlier to have READ its buffer; the global writes drain asynchronously
+// while the warp moves on to the next item.  (Row-per-thread 16-B global stores touched 32
+// lines per instruction; row-contiguous stores from the warp itself made the epilogue
+// write-bandwidth-bound when every CTA reached it at once: ~2 us per dK/dV item.)
+// Lane 0 issues and owns the bulk groups.
+__device__ __forceinline__ void store_chunk_tma(uint32_t stg, int& nbuf, const uint32_t* v, float mul,
+                                                const CUtensorMap* tm, int col, int row, int lane) {
+  const uint32_t buf = stg + (nbuf & 1) * 2048;
+  if (lane == 0) sm100::bulk_wait_read<1>();  // this buffer's previous store has read it
+  __syncwarp();
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     const uint32_t x = pack_bf16(__uint_as_float(v[8 * g]) * mul, __uint_as_float(v[8 * g + 1]) * mul);
     const uint32_t y = pack_bf16(__uint_as_float(v[8 * g + 2]) * mul, __uint_as_float(v[8 * g + 3]) * mul);
     const uint32_t z = pack_bf16(__uint_as_float(v[8 * g + 4]) * mul, __uint_as_float(v[8 * g + 5]) * mul);
     const uint32_t w = pack_bf16(__uint_as_float(v[8 * g + 6]) * mul, __uint_as_float(v[8 * g + 7]) * mul);
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4)),
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4)),
                  "r"(x), "r"(y), "r"(z), "r"(w)
                  : "memory");
   }
+  sm100::fence_proxy_async();  // generic-proxy shared writes -> visible to the TMA (async proxy)
   __syncwarp();
-#pragma unroll
-  for (int it = 0; it < 4; ++it) {
-    const int idx = it * 32 + lane, i = idx >> 2, k = idx & 3;
-    const float4 f = sm100::lds128(stg + i * 64 + ((k ^ ((i >> 1) & 3)) << 4));
-    *reinterpret_cast<float4*>(base + static_cast<int64_t>(i) * ld + k * 8) = f;
+  if (lane == 0) {
+    sm100::tma_store_2d_sa(tm, buf, col, row);
+    sm100::bulk_commit();
   }
-  __syncwarp();
+  ++nbuf;
 }
 
 // Row r (0..127) of a 128-row SWIZZLE_128B bf16 tile (D columns in 64-column atoms 16 KB apart,
@@ -132,8 +151,8 @@ template <int D> struct DkdvCfg {
   static constexpr int STAGE = 2 * Q_TILE + 1024;  // Q_i, dO_i, L_i[64], D_i[64] (1024-aligned)
   static constexpr int OFF_K = 0, OFF_V = KV_TILE, OFF_ST = 2 * KV_TILE;
   static constexpr int OFF_BAR = OFF_ST + ST * STAGE;
-  static constexpr int OFF_OST = OFF_BAR + 1024;  // epilogue staging: 8 elementwise warps x 2 KB
-  static constexpr int SMEM = OFF_OST + 8 * 2048 + 1024;
+  static constexpr int OFF_OST = OFF_BAR + 1024;  // epilogue staging: 8 elementwise warps x 2 x 2 KB
+  static constexpr int SMEM = OFF_OST + 8 * 4096 + 1024;
 };
 
 // Persistent over this CTA's dK/dV items (key block kb = level, head, sequence): barriers,
@@ -145,8 +164,9 @@ template <int D> struct DkdvCfg {
 // the launching kernel's __grid_constant__ parameters.)
 template <int D, typename ItemOf>
 __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensorMap& tmQ, const CUtensorMap& tmDO,
-                                         const float* __restrict__ lse, const float* __restrict__ delta,
-                                         bf16* __restrict__ dqkv, int s, int a, int per, float scale,
+                                         const CUtensorMap& tmOut, const float* __restrict__ lse,
+                                         const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a,
+                                         int per, float scale,
                                          float scale_log2, uint32_t tbase, ItemOf item_of) {
   using C = DkdvCfg<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -326,6 +346,8 @@ __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensor
     const int qw = warp & 3, hf = (warp - 4) >> 2;
     const int r = qw * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;  // epilogue staging (2 x 2 KB)
+    int nbuf = 0;
     int gn = 0;
     for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
       int kb, hd, bb;
@@ -341,9 +363,11 @@ __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensor
         sm100::tc_fence_before();
         sm100::mbar_arrive_warp(at_full);
       }
+      if (warp == 4 && lane == 0) TRB(0, ri);
       for (int n = 0; n < nq; ++n, ++gn) {
         const int i = i0 + n, b = gn & 1, st = gn % C::ST;
         sm100::mbar_wait(&sp_full[b], (gn >> 1) & 1);
+        if (warp == 4 && lane == 0 && n == 0) TRB(1, ri);
         if (warp == 4 && lane == 0 && ri == 0) TR(4, n);
         sm100::tc_fence_after();
         uint32_t sr[32], dr[32];
@@ -407,25 +431,28 @@ __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensor
         if (warp == 4 && lane == 0 && ri == 0) TR(5, n);
         sm100::mbar_arrive_warp(&ds_full[b]);
       }
+      if (warp == 4 && lane == 0) TRB(2, ri);
       sm100::mbar_wait(o_final, ri & 1);
+      if (warp == 4 && lane == 0) TRB(3, ri);
       if (warp == 4 && lane == 0 && ri == 0) TR(6, 1);
       sm100::tc_fence_after();
       (void)key;
-      bf16* wrow = dqkv + (static_cast<int64_t>(row0) + kb * 128 + qw * 32) * (3 * h) + hd * D;  // warp's row 0
-      const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 2048;
+      const int wr = row0 + kb * 128 + qw * 32;  // the warp's first row of dqkv
 #pragma unroll 1
       for (int c = hf; c < D / 32; c += 2) {
         uint32_t v[32];
         sm100::tmem_ld32(t_dk + lane_off + c * 32, v);
         sm100::tmem_ld_wait();
-        store_chunk_staged(stg, v, scale, wrow + h + c * 32, 3 * h, lane);
+        store_chunk_tma(stg, nbuf, v, scale, &tmOut, h + hd * D + c * 32, wr, lane);
         sm100::tmem_ld32(t_dv + lane_off + c * 32, v);
         sm100::tmem_ld_wait();
-        store_chunk_staged(stg, v, 1.f, wrow + 2 * h + c * 32, 3 * h, lane);
+        store_chunk_tma(stg, nbuf, v, 1.f, &tmOut, 2 * h + hd * D + c * 32, wr, lane);
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive_warp(o_empty);  // dK / dV may be overwritten by the next item
+      if (warp == 4 && lane == 0) TRB(4, ri);
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // epilogue stores complete (staging reused by the next body / exit)
   }
   // every role is done (all commits observed by their waiters): the barrier memory may be reused
   sm100::tc_fence_before();
@@ -450,8 +477,8 @@ template <int D> struct DqCfg {
   static constexpr int STAGE = 2 * KV_TILE;      // K_j, V_j
   static constexpr int OFF_Q = 0, OFF_DO = Q_TILE, OFF_ST = 2 * Q_TILE;
   static constexpr int OFF_BAR = OFF_ST + ST * STAGE;
-  static constexpr int OFF_OST = OFF_BAR + 1024;  // epilogue staging: 8 elementwise warps x 2 KB
-  static constexpr int SMEM = OFF_OST + 8 * 2048 + 1024;
+  static constexpr int OFF_OST = OFF_BAR + 1024;  // epilogue staging: 8 elementwise warps x 2 x 2 KB
+  static constexpr int SMEM = OFF_OST + 8 * 4096 + 1024;
 };
 
 // Persistent over this CTA's dQ items (query block nqb-1-level, head, sequence); running
@@ -461,7 +488,8 @@ template <int D> struct DqCfg {
 // product for the current dQ having been read (o_empty).
 template <int D, typename ItemOf>
 __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap& tmKV, const CUtensorMap& tmDO,
-                                       const float* __restrict__ lse, const float* __restrict__ delta,
+                                       const CUtensorMap& tmOut, const float* __restrict__ lse,
+                                       const float* __restrict__ delta,
                                        bf16* __restrict__ dqkv, int s, int a, int per, float scale, float scale_log2,
                                        uint32_t tbase, ItemOf item_of) {
   using C = DqCfg<D>;
@@ -600,6 +628,8 @@ __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap
     const int qw = warp & 3, hf = (warp - 4) >> 2;
     const int r = qw * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(qw * 32) << 16;
+    const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;  // epilogue staging (2 x 2 KB)
+    int nbuf = 0;
     int gj = 0;
     for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
       int level, hd, bb;
@@ -616,7 +646,9 @@ __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap
       sm100::mbar_arrive_warp(at_full);
       for (int j = 0; j < nkv; ++j, ++gj) {
         const int b = gj & 1;
+        if (warp == 4 && lane == 0 && j == 0) TRB(5, ri);
         sm100::mbar_wait(&sp_full[b], (gj >> 1) & 1);
+        if (warp == 4 && lane == 0 && j == 0) TRB(6, ri);
         sm100::tc_fence_after();
         uint32_t sr[32], dr[32];
         const uint32_t tp = tbase + b * 128 + lane_off;
@@ -657,20 +689,23 @@ __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap
         sm100::tc_fence_before();
         sm100::mbar_arrive_warp(&ds_full[b]);
       }
+      if (warp == 4 && lane == 0) TRB(7, ri);
       sm100::mbar_wait(o_final, ri & 1);
+      if (warp == 4 && lane == 0) TRB(8, ri);
       sm100::tc_fence_after();
-      bf16* wrow = dqkv + (static_cast<int64_t>(bb) * s + qb * 128 + qw * 32) * (3 * h) + hd * D;  // warp's row 0
-      const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 2048;
+      const int wr = bb * s + qb * 128 + qw * 32;  // the warp's first row of dqkv
 #pragma unroll 1
       for (int c = hf; c < D / 32; c += 2) {
         uint32_t v[32];
         sm100::tmem_ld32(t_dq + lane_off + c * 32, v);
         sm100::tmem_ld_wait();
-        store_chunk_staged(stg, v, scale, wrow + c * 32, 3 * h, lane);
+        store_chunk_tma(stg, nbuf, v, scale, &tmOut, hd * D + c * 32, wr, lane);
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive_warp(o_empty);  // dQ may be overwritten by the next item
+      if (warp == 4 && lane == 0) TRB(9, ri);
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // epilogue stores complete before the CTA exits
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -690,8 +725,9 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap kv128, const __grid_constant__ CUtensorMap kv64,
              const __grid_constant__ CUtensorMap do64, const __grid_constant__ CUtensorMap do128,
-             const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a,
-             int b, float scale, float scale_log2) {
+             const __grid_constant__ CUtensorMap tmOut, const float* __restrict__ lse,
+             const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a, int b, float scale,
+             float scale_log2) {
 #ifdef ZB_ATTN_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 16384) {
     unsigned int sm;
@@ -707,6 +743,7 @@ __global__ void __launch_bounds__(384, 1)
     sm100::tma_prefetch(&kv64);
     sm100::tma_prefetch(&do64);
     sm100::tma_prefetch(&do128);
+    sm100::tma_prefetch(&tmOut);
   }
   if (warp == 2) sm100::tmem_alloc<512>(&tslot);
   sm100::tc_fence_before();
@@ -724,9 +761,9 @@ __global__ void __launch_bounds__(384, 1)
   };
   int r_q = 0;  // first round whose item is a dQ item
   while (nth(r_q) >= 0 && nth(r_q) < n_items) ++r_q;
-  dkdv_run<D>(kv128, kv64, do64, lse, delta, dqkv, s, a, per, scale, scale_log2, tbase,
+  dkdv_run<D>(kv128, kv64, do64, tmOut, lse, delta, dqkv, s, a, per, scale, scale_log2, tbase,
               [&](int r) { return r < r_q ? nth(r) : -1; });
-  dq_run<D>(kv128, kv64, do128, lse, delta, dqkv, s, a, per, scale, scale_log2, tbase, [&](int r) {
+  dq_run<D>(kv128, kv64, do128, tmOut, lse, delta, dqkv, s, a, per, scale, scale_log2, tbase, [&](int r) {
     const int it = nth(r_q + r);
     return it >= 0 ? it - n_items : -1;
   });
@@ -760,7 +797,9 @@ static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const int items = 2 * (sh.s / 128) * sh.a * sh.b;
   const int grid = items < num_sms() ? items : num_sms();  // persistent: one CTA per SM
-  launch(PDL_ATTN, attn_bwd_tc::k_bwd_tc<D>, grid, 384, SMEM, st, kv128, kv64, do64, do128, lse, delta,
+  // dK / dV / dQ epilogue stores: box 32 rows x 32 columns (64 B), 64-byte swizzle
+  const CUtensorMap out32 = make_tmap(dqkv, 3 * h, rows, 3 * h, 32, 32, false, 64);
+  launch(PDL_ATTN, attn_bwd_tc::k_bwd_tc<D>, grid, 384, SMEM, st, kv128, kv64, do64, do128, out32, lse, delta,
          static_cast<bf16*>(dqkv), sh.s, sh.a, sh.b, scale, scale * attn_bwd_tc::LOG2E);
   ZB_LAUNCH_CHECK();
 }
@@ -779,6 +818,9 @@ bool attention_bwd_tc(const AttnShape& sh, const void* qkv, const void* dout, co
 }  // namespace zb
 
 #ifdef ZB_ATTN_TRACE
+extern "C" int zb_dbg_attn_bwd_item_trace(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_bwd_tc::g_item_bwd, sizeof(unsigned long long) * 10 * 16));
+}
 extern "C" int zb_dbg_attn_bwd_cta_trace(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, zb::attn_bwd_tc::g_cta_bwd, sizeof(unsigned long long) * 16384 * 3));
 }

@@ -111,8 +111,41 @@ template <int D> struct FwdCfg {
 // as soon as they see S_t(j+1).
 // Barrier parities come from running counters of the CTA (blocks per tile, items per tile,
 // K/V ring position), not from the block index of the current item.
+// One 32-column chunk of the calling warp's 32 O rows (v: this thread's row, f32, times inv) to
+// global memory by a TMA tensor store (box 32 rows x 64 B, SWIZZLE_64B: 16-B piece k of row i
+// at k ^ ((i >> 1) & 3)) from one of the warp's two 2 KB staging buffers (alternating with
+// nbuf); the warp waits only for the store issued two chunks earlier to have read its buffer,
+// the global writes drain while it moves on.  Lane 0 issues and owns the bulk groups.
+__device__ __forceinline__ void store_o_chunk(uint32_t stg, int& nbuf, const uint32_t* v, float inv,
+                                              const CUtensorMap* tm, int col, int row, int lane) {
+  const uint32_t buf = stg + (nbuf & 1) * 2048;
+  if (lane == 0) sm100::bulk_wait_read<1>();
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[8 * g + 2 * e]) * inv,
+                                                __uint_as_float(v[8 * g + 2 * e + 1]) * inv);
+      w[e] = *reinterpret_cast<uint32_t*>(&b2);
+    }
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 64 + ((g ^ ((lane >> 1) & 3)) << 4)),
+                 "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                 : "memory");
+  }
+  sm100::fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    sm100::tma_store_2d_sa(tm, buf, col, row);
+    sm100::bulk_commit();
+  }
+  ++nbuf;
+}
+
 template <int D>
-__global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ o,
+__global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUtensorMap tm,
+                                                   const __grid_constant__ CUtensorMap tmO, bf16* __restrict__ o,
                                                    float* __restrict__ lse, int s, int a, int items,
                                                    float scale_log2) {
   using C = FwdCfg<D>;
@@ -191,7 +224,10 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
     }
     sm100::fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) sm100::tma_prefetch(&tm);
+  if (warp == 0 && lane == 0) {
+    sm100::tma_prefetch(&tm);
+    sm100::tma_prefetch(&tmO);
+  }
   if (warp == 2) sm100::tmem_alloc<512>(tslot);
   sm100::tc_fence_before();
   __syncthreads();
@@ -363,6 +399,8 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
     const int r_ = (warp & 3) * 32 + lane;  // row within the tile = TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tbase + t * 128 + lane_off, t_o = tbase + 256 + t * 128 + lane_off;
+    const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;  // O staging (2 x 2 KB)
+    int nbuf = 0;
     int sb = 0;  // S blocks consumed by this tile (s_full / p barrier parity)
     int ni = 0;  // items finished by this tile (o_final parity)
     for (int rr = 0, it; (it = item_of(rr)) >= 0; ++rr) {
@@ -465,46 +503,17 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         sm100::tc_fence_after();
         const int q = qt * BQ + r_;
         const float inv = 1.f / l;
-        // O rows leave through a warp-private staging buffer (this warp's 32 rows x 64 columns,
-        // 128 B per row, 16-B chunk k of row i at chunk k ^ (i & 7)): written one row per
-        // thread, read back row-contiguous, so every global store instruction covers whole
-        // 128-B lines (row-per-thread 16-B stores touched 32 lines each: ~2 us per tile,
+        // O rows leave by TMA tensor stores from warp-private staging (store_o_chunk): the warp
+        // writes shared memory only, the global writes drain while it starts the next item
+        // (row-per-thread 16-B stores touched 32 lines per instruction: ~2 us per tile,
         // profiles/r02_attn_fwd_item_trace_before.txt)
-        const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;
-        bf16* obase = o + (static_cast<int64_t>(w.bb) * s + qt * BQ + (warp & 3) * 32) * h + w.hd * D;
-#pragma unroll
-        for (int h0 = 0; h0 < D; h0 += 64) {  // unrolled: nc is a compile-time 64 / 32 (no spills at d = 96)
-          const int nc = D - h0 < 64 ? D - h0 : 64;  // 64, or 32 for the last columns at d = 96
-#pragma unroll
-          for (int c32 = 0; c32 < 64; c32 += 32) {
-            if (c32 < nc) {
-              uint32_t ov[32];
-              sm100::tmem_ld32(t_o + h0 + c32, ov);
-              sm100::tmem_ld_wait();
-#pragma unroll
-              for (int g = 0; g < 4; ++g) {
-                uint4 u;
-                __nv_bfloat162* hv = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  hv[e] = __floats2bfloat162_rn(__uint_as_float(ov[8 * g + 2 * e]) * inv,
-                                                __uint_as_float(ov[8 * g + 2 * e + 1]) * inv);
-                const int k = c32 / 8 + g;
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + lane * 128 + ((k ^ (lane & 7)) << 4)),
-                             "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
-                             : "memory");
-              }
-            }
-          }
-          __syncwarp();
-          const int cpr = nc / 8;  // 16-B chunks per row
+        const int wr = w.bb * s + qt * BQ + (warp & 3) * 32;  // the warp's first O row
 #pragma unroll 1
-          for (int it = 0; it < cpr; ++it) {
-            const int idx = it * 32 + lane, i = idx / cpr, k = idx % cpr;
-            const float4 f = sm100::lds128(stg + i * 128 + ((k ^ (i & 7)) << 4));
-            *reinterpret_cast<float4*>(obase + static_cast<int64_t>(i) * h + h0 + k * 8) = f;
-          }
-          __syncwarp();
+        for (int c4 = 0; c4 < D / 32; ++c4) {
+          uint32_t ov[32];
+          sm100::tmem_ld32(t_o + c4 * 32, ov);
+          sm100::tmem_ld_wait();
+          store_o_chunk(stg, nbuf, ov, inv, &tmO, w.hd * D + c4 * 32, wr, lane);
         }
         sm100::tc_fence_before();
         sm100::mbar_arrive_warp(&o_empty[t]);  // O_t may be overwritten by the next item's PV
@@ -512,6 +521,7 @@ __global__ void __launch_bounds__(384, 1) k_fwd_tc(const __grid_constant__ CUten
         lse[(static_cast<int64_t>(w.bb) * a + w.hd) * s + q] = (m + log2f(l)) * LN2;
       }
     }
+    if (lane == 0) sm100::bulk_wait<0>();  // O stores complete before the CTA exits
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -541,7 +551,8 @@ static void fwd_tc_launch(const AttnShape& sh, const void* qkv, void* o, float* 
   CUtensorMap tm = make_qkv_tmap(qkv, sh.b * sh.s, 3 * h);
   const int items = (sh.s / attn_tc::BQ + 1) / 2 * sh.a * sh.b;
   const int grid = items < num_sms() ? items : num_sms();  // persistent: one CTA per SM
-  launch(PDL_ATTN, attn_tc::k_fwd_tc<D>, grid, 384, C::SMEM, st, tm, static_cast<bf16*>(o), lse, sh.s, sh.a, items,
+  const CUtensorMap tmO = make_tmap(o, h, sh.b * sh.s, h, 32, 32, false, 64);  // O stores: 32 x 32, 64-B swizzle
+  launch(PDL_ATTN, attn_tc::k_fwd_tc<D>, grid, 384, C::SMEM, st, tm, tmO, static_cast<bf16*>(o), lse, sh.s, sh.a, items,
          attn_tc::LOG2E / sqrtf(static_cast<float>(D)));
   ZB_LAUNCH_CHECK();
 }

@@ -818,7 +818,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D bf16 tensor map over a row-major [outer, inner] view with leading dim ld.
 CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-                      uint32_t box_outer, bool f32) {
+                      uint32_t box_outer, bool f32, int swizzle) {
   const uint64_t esz = f32 ? 4 : 2;
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || ((ld * esz) & 15))
     throw CudaError("gemm: operand must be 16-byte aligned with a 16-byte multiple row pitch");
@@ -828,7 +828,8 @@ CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t 
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&tm, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   return tm;

@@ -89,6 +89,7 @@ int num_sms();
 // 2-D bf16 (or f32) TMA descriptor (128B swizzle) over a row-major [outer, inner]
 // view with leading dimension ld elements and box {box_inner, box_outer}.
 CUtensorMap make_tmap(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-                      uint32_t box_outer, bool f32 = false);
+                      uint32_t box_outer, bool f32 = false,
+                      int swizzle = 128 /* 128 or 64 (bytes) */);
 
 }  // namespace zb
