@@ -349,20 +349,25 @@ __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensor
     const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;  // epilogue staging (2 x 2 KB)
     int nbuf = 0;
     int gn = 0;
-    for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
-      int kb, hd, bb;
-      decode_item(it, a, per, kb, hd, bb);
-      const int i0 = 2 * kb, nq = s / 64 - i0, row0 = bb * s;
-      const int key = kb * 128 + r;
+    // K (and V) of item ri into TMEM (TS A operands, d <= 96): waits for the tiles in shared
+    // memory and for the previous item's products to be done with the TMEM copies
+    auto copy_kv = [&](int ri_) {
       if constexpr (C::KT) {
-        sm100::mbar_wait(kv_full, ri & 1);
-        sm100::mbar_wait(kv_empty, (ri & 1) ^ 1);  // the previous item's products are done with K / V in TMEM
+        sm100::mbar_wait(kv_full, ri_ & 1);
+        sm100::mbar_wait(kv_empty, (ri_ & 1) ^ 1);
         if (hf == 0) tile_row_to_tmem<D>(smem + C::OFF_K, r, t_kt + lane_off);
         if (C::VT && hf == 1) tile_row_to_tmem<D>(smem + C::OFF_V, r, t_vt + lane_off);
         sm100::tmem_st_wait();
         sm100::tc_fence_before();
         sm100::mbar_arrive_warp(at_full);
       }
+    };
+    if (item_of(0) >= 0) copy_kv(0);
+    for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
+      int kb, hd, bb;
+      decode_item(it, a, per, kb, hd, bb);
+      const int i0 = 2 * kb, nq = s / 64 - i0, row0 = bb * s;
+      const int key = kb * 128 + r;
       if (warp == 4 && lane == 0) TRB(0, ri);
       for (int n = 0; n < nq; ++n, ++gn) {
         const int i = i0 + n, b = gn & 1, st = gn % C::ST;
@@ -432,6 +437,9 @@ __device__ __forceinline__ void dkdv_run(const CUtensorMap& tmKV, const CUtensor
         sm100::mbar_arrive_warp(&ds_full[b]);
       }
       if (warp == 4 && lane == 0) TRB(2, ri);
+      // the next item's K / V copies before this item's epilogue (its first S^T / dP^T products
+      // then run while the dK / dV stores are prepared)
+      if (item_of(ri + 1) >= 0) copy_kv(ri + 1);
       sm100::mbar_wait(o_final, ri & 1);
       if (warp == 4 && lane == 0) TRB(3, ri);
       if (warp == 4 && lane == 0 && ri == 0) TR(6, 1);
@@ -631,6 +639,17 @@ __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap
     const uint32_t stg = sm100::smem_addr(smem + C::OFF_OST) + (warp - 4) * 4096;  // epilogue staging (2 x 2 KB)
     int nbuf = 0;
     int gj = 0;
+    // Q / dO of item ri into TMEM (the TS A operands): waits for the tile in shared memory and
+    // for the previous item's last S / dP products to be done with the TMEM copies
+    auto copy_qdo = [&](int ri_) {
+      sm100::mbar_wait(q_full, ri_ & 1);
+      sm100::mbar_wait(qt_empty, (ri_ & 1) ^ 1);
+      tile_row_to_tmem<D>(smem + (hf == 0 ? C::OFF_Q : C::OFF_DO), r, (hf == 0 ? t_qt : t_dot) + lane_off);
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive_warp(at_full);
+    };
+    if (item_of(0) >= 0) copy_qdo(0);
     for (int ri = 0, it; (it = item_of(ri)) >= 0; ++ri) {
       int level, hd, bb;
       decode_item(it, a, per, level, hd, bb);
@@ -638,12 +657,6 @@ __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap
       const int q = qb * 128 + r;
       const int64_t si = (static_cast<int64_t>(bb) * a + hd) * s + q;
       const float L2 = lse[si] * LOG2E, Dq = delta[si];
-      sm100::mbar_wait(q_full, ri & 1);
-      sm100::mbar_wait(qt_empty, (ri & 1) ^ 1);  // the previous item's products are done with Q / dO in TMEM
-      tile_row_to_tmem<D>(smem + (hf == 0 ? C::OFF_Q : C::OFF_DO), r, (hf == 0 ? t_qt : t_dot) + lane_off);
-      sm100::tmem_st_wait();
-      sm100::tc_fence_before();
-      sm100::mbar_arrive_warp(at_full);
       for (int j = 0; j < nkv; ++j, ++gj) {
         const int b = gj & 1;
         if (warp == 4 && lane == 0 && j == 0) TRB(5, ri);
@@ -690,6 +703,9 @@ __device__ __forceinline__ void dq_run(const CUtensorMap& tmQ, const CUtensorMap
         sm100::mbar_arrive_warp(&ds_full[b]);
       }
       if (warp == 4 && lane == 0) TRB(7, ri);
+      // the next item's Q / dO copies before this item's epilogue: its first S / dP products then
+      // run while the dQ stores are prepared
+      if (item_of(ri + 1) >= 0) copy_qdo(ri + 1);
       sm100::mbar_wait(o_final, ri & 1);
       if (warp == 4 && lane == 0) TRB(8, ri);
       sm100::tc_fence_after();
