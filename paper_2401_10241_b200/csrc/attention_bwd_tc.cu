@@ -16,7 +16,13 @@
 // Q, dO, L, D of a query block arrive by TMA / bulk copy in a 3-stage ring.
 #include <math.h>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <tuple>
 #include <type_traits>
+#include <vector>
 
 #include "attention.h"
 #include "gemm.h"
@@ -741,9 +747,9 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     k_bwd_tc(const __grid_constant__ CUtensorMap kv128, const __grid_constant__ CUtensorMap kv64,
              const __grid_constant__ CUtensorMap do64, const __grid_constant__ CUtensorMap do128,
-             const __grid_constant__ CUtensorMap tmOut, const float* __restrict__ lse,
-             const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a, int b, float scale,
-             float scale_log2) {
+             const __grid_constant__ CUtensorMap tmOut, const int32_t* __restrict__ table,
+             const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int s, int a,
+             int b, float scale, float scale_log2) {
 #ifdef ZB_ATTN_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 16384) {
     unsigned int sm;
@@ -771,9 +777,12 @@ __global__ void __launch_bounds__(384, 1)
   const int per = a * b;
   const int n_items = s / 128 * per;  // per half (dK/dV or dQ)
   const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
-  auto nth = [&](int r) {  // r-th item of this CTA in the combined list, or -1
-    const int it = r * G + ((r & 1) ? G - 1 - c : c);
-    return it < 2 * n_items ? it : -1;
+  // this CTA's items from the host-built LPT table (bwd_item_table): table[c] .. table[c + 1]
+  // index ids in table[G + 1 ..]; an id < n_items is a dK/dV item, else a dQ item (id - n_items)
+  const int t_lo = __ldg(table + c), t_hi = __ldg(table + c + 1);
+  (void)G;
+  auto nth = [&](int r) {  // r-th item of this CTA (dK/dV items first), or -1
+    return t_lo + r < t_hi ? __ldg(table + G + 1 + t_lo + r) : -1;
   };
   int r_q = 0;  // first round whose item is a dQ item
   while (nth(r_q) >= 0 && nth(r_q) < n_items) ++r_q;
@@ -793,6 +802,59 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 }  // namespace attn_bwd_tc
+
+// Static LPT assignment of the backward's items to the G persistent CTAs (cached per shape):
+// cost of a dK/dV item of key block kb = its s/64 - 2 kb query steps + 1.5 (epilogue of two
+// tiles), of a dQ item of query block qb = its 2 qb + 2 key steps + 1 — the per-item trace of
+// the kernel (scripts/attn_bwd_item_trace.py) puts a step at ~1 us and the epilogues at
+// ~1.3 / 0.6 us.  Items go heaviest first to the least-loaded CTA (ties: lowest index); each
+// CTA then runs its dK/dV items before its dQ items, each group in id order.  The snake order
+// this replaces left the busiest CTA 9.5% above the mean (scripts/attn_cta_trace.py).  Which
+// CTA computes an item does not change its result (no cross-item accumulation).
+static const int32_t* bwd_item_table(int s, int a, int b, int G) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, int32_t*> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(s, a, b, G);
+  auto f = cache.find(key);
+  if (f != cache.end()) return f->second;
+  const int per = a * b, nqb = s / 128, n_items = nqb * per;
+  std::vector<std::pair<double, int>> items;  // (cost, combined id)
+  items.reserve(2 * n_items);
+  for (int id = 0; id < n_items; ++id) {
+    const int kb = id / per;                  // dK/dV: level = key block, heaviest first
+    items.push_back({(s / 64 - 2 * kb) + 1.5, id});
+  }
+  for (int id = 0; id < n_items; ++id) {
+    const int qb = nqb - 1 - id / per;        // dQ: level 0 = the last query block
+    items.push_back({(2 * qb + 2) + 1.0, n_items + id});
+  }
+  std::stable_sort(items.begin(), items.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  std::vector<double> load(G, 0.0);
+  std::vector<std::vector<int>> mine(G);
+  using E = std::pair<double, int>;
+  std::priority_queue<E, std::vector<E>, std::greater<E>> heap;  // (load, cta): least load, lowest index
+  for (int c = 0; c < G; ++c) heap.push({0.0, c});
+  for (const auto& it : items) {
+    E e = heap.top();
+    heap.pop();
+    mine[e.second].push_back(it.second);
+    heap.push({e.first + it.first, e.second});
+  }
+  std::vector<int32_t> host(G + 1 + 2 * n_items);
+  int pos = 0;
+  for (int c = 0; c < G; ++c) {
+    std::sort(mine[c].begin(), mine[c].end());  // dK/dV ids (< n_items) first, heaviest first
+    host[c] = pos;
+    for (int id : mine[c]) host[G + 1 + pos++] = id;
+  }
+  host[G] = pos;
+  int32_t* dev = nullptr;
+  ZB_CUDA(cudaMalloc(&dev, sizeof(int32_t) * host.size()));
+  ZB_CUDA(cudaMemcpy(dev, host.data(), sizeof(int32_t) * host.size(), cudaMemcpyHostToDevice));
+  cache[key] = dev;
+  return dev;
+}
 
 template <int D>
 static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout, const float* lse, void* dqkv,
@@ -815,7 +877,8 @@ static void bwd_tc_launch(const AttnShape& sh, const void* qkv, const void* dout
   const int grid = items < num_sms() ? items : num_sms();  // persistent: one CTA per SM
   // dK / dV / dQ epilogue stores: box 32 rows x 32 columns (64 B), 64-byte swizzle
   const CUtensorMap out32 = make_tmap(dqkv, 3 * h, rows, 3 * h, 32, 32, false, 64);
-  launch(PDL_ATTN, attn_bwd_tc::k_bwd_tc<D>, grid, 384, SMEM, st, kv128, kv64, do64, do128, out32, lse, delta,
+  const int32_t* table = bwd_item_table(sh.s, sh.a, sh.b, grid);
+  launch(PDL_ATTN, attn_bwd_tc::k_bwd_tc<D>, grid, 384, SMEM, st, kv128, kv64, do64, do128, out32, table, lse, delta,
          static_cast<bf16*>(dqkv), sh.s, sh.a, sh.b, scale, scale * attn_bwd_tc::LOG2E);
   ZB_LAUNCH_CHECK();
 }
