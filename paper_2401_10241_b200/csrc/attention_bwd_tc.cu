@@ -813,9 +813,11 @@ __global__ void __launch_bounds__(384, 1)
 // CTA computes an item does not change its result (no cross-item accumulation).
 static const int32_t* bwd_item_table(int s, int a, int b, int G) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int, int>, int32_t*> cache;
+  static std::map<std::tuple<int, int, int, int, int>, int32_t*> cache;
   std::lock_guard<std::mutex> lock(mu);
-  auto key = std::make_tuple(s, a, b, G);
+  int dev_id = 0;
+  ZB_CUDA(cudaGetDevice(&dev_id));
+  auto key = std::make_tuple(dev_id, s, a, b, G);  // per device: the table is device memory
   auto f = cache.find(key);
   if (f != cache.end()) return f->second;
   const int per = a * b, nqb = s / 128, n_items = nqb * per;
