@@ -1,10 +1,7 @@
 mkdir -p gpurun_out
-timeout 150 python -m pytest tests/test_gpu_attention.py -q -x -p no:cacheprovider > gpurun_out/c28_tests.log 2>&1; echo "rc $?" >> gpurun_out/c28_tests.log
-tail -3 gpurun_out/c28_tests.log
-if grep -q "rc 0" gpurun_out/c28_tests.log; then
-  timeout 300 python scripts/attn_perf.py > gpurun_out/c28_perf.jsonl 2>&1
-  timeout 300 python scripts/attn_perf.py >> gpurun_out/c28_perf.jsonl 2>&1
-  cat gpurun_out/c28_perf.jsonl
-  timeout 900 python -m pytest tests/test_gpu_stage.py tests/test_gpu_pipeline_loopback.py -q -x -p no:cacheprovider > gpurun_out/c28_tests2.log 2>&1; echo "rc $?" >> gpurun_out/c28_tests2.log
-  tail -3 gpurun_out/c28_tests2.log
-fi
+md5sum paper_2401_10241_b200/libzb.so > gpurun_out/final2_md5.txt
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/final2_gpu_tests.log 2>&1; echo "rc $?" >> gpurun_out/final2_gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final2_smoke.log 2>&1; echo "rc $?" >> gpurun_out/final2_smoke.log
+timeout 900 python bench.py > gpurun_out/final2_bench.log 2>&1; echo "rc $?" >> gpurun_out/final2_bench.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/final2_ref.log 2>&1; echo "rc $?" >> gpurun_out/final2_ref.log
+tail -3 gpurun_out/final2_gpu_tests.log; tail -2 gpurun_out/final2_smoke.log; tail -c 300 gpurun_out/final2_bench.log; tail -c 200 gpurun_out/final2_ref.log
