@@ -53,3 +53,22 @@ def test_arena_sizing_cpu_only():
     assert sb / 1e9 > 1.3     # SURVEY: c2 1.36 GB per slot per stage
     total = api.arena_bytes(mc)
     assert total > 8 * sb
+
+
+def test_python_constants_match_the_header_enums():
+    """Every ZB_* enum constant the binding re-declares (flags, kinds, families, status codes)
+    has the header's value: the binding must not drift from include/zb.h."""
+    from paper_2401_10241_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "zb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    header = {}
+    for body in re.findall(r"enum\s*\{([^}]*)\}", src):
+        for name, val in re.findall(r"\b(ZB_\w+)\s*=\s*(-?\d+)", body):
+            header[name] = int(val)
+    assert {"ZB_RUN_GRAPH", "ZB_RUN_GROUP_W", "ZB_EINVAL", "ZB_W"} <= set(header)
+    checked = 0
+    for name, val in header.items():
+        if hasattr(_lib, name):
+            assert getattr(_lib, name) == val, (name, getattr(_lib, name), val)
+            checked += 1
+    assert checked >= 8, checked
