@@ -1,7 +1,4 @@
 mkdir -p gpurun_out
-md5sum paper_2401_10241_b200/libzb.so > gpurun_out/final2_md5.txt
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/final2_gpu_tests.log 2>&1; echo "rc $?" >> gpurun_out/final2_gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final2_smoke.log 2>&1; echo "rc $?" >> gpurun_out/final2_smoke.log
-timeout 900 python bench.py > gpurun_out/final2_bench.log 2>&1; echo "rc $?" >> gpurun_out/final2_bench.log
-timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/final2_ref.log 2>&1; echo "rc $?" >> gpurun_out/final2_ref.log
-tail -3 gpurun_out/final2_gpu_tests.log; tail -2 gpurun_out/final2_smoke.log; tail -c 300 gpurun_out/final2_bench.log; tail -c 200 gpurun_out/final2_ref.log
+timeout 300 python scripts/attn_fwd_item_trace.py > gpurun_out/fwd_items_end.txt 2>&1
+timeout 300 python scripts/attn_fwd_trace.py > gpurun_out/fwd_blocks_end.txt 2>&1
+cat gpurun_out/fwd_items_end.txt gpurun_out/fwd_blocks_end.txt
