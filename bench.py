@@ -435,6 +435,13 @@ def run_single(args, cfg, headline=True):
     accounted = sum(v["ms_total"] for k, v in kstats.items() if k in ("gemm", "attn_fwd", "attn_bwd")) + \
         sum(v["ms_total"] for v in hbm["classes"].values())
     roof["unaccounted_ms_per_step"] = round(ms_ev - accounted, 3)
+    # the same against the value region's step (CUDA-graph replay, no per-launch events): the
+    # per-class times are measured with events around every launch (eager), which inflate each
+    # bracketed kernel, so a value near or below 0 means no time is left outside the kernels
+    roof["value_region_minus_kernels_ms_per_step"] = round(ms - accounted, 3)
+    roof["unaccounted_note"] = ("unaccounted_ms_per_step: eager timing region minus the event-timed classes "
+                                "(mostly the events' own cost); value_region_minus_kernels: the graph-replayed "
+                                "step minus the same class times")
     flops_token = cfg.L * (72 * cfg.h ** 2 + 12 * cfg.s * cfg.h) + 6 * cfg.h * cfg.V
     mfu = value * flops_token / (peaks.get("bf16_tflops", 1680.3) * 1e12)
     line = {"metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,

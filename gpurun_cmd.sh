@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python scripts/gemm_b_layout.py --secs 1.0 > gpurun_out/b_layout.jsonl 2>&1
-timeout 600 python scripts/gemm_b_layout.py --secs 1.0 >> gpurun_out/b_layout.jsonl 2>&1
-cat gpurun_out/b_layout.jsonl
+timeout 900 python bench.py --second-config none --no-profile-p8 --no-cpu-baseline > gpurun_out/c34_bench.log 2>&1; echo "rc $?" >> gpurun_out/c34_bench.log
+tail -c 400 gpurun_out/c34_bench.log
