@@ -633,11 +633,14 @@ void attention_bwd(const AttnShape& sh, DType dt, const void* qkv, const void* o
 void attention_bwd_impl(const AttnShape& sh, DType dt, const void* qkv, const void* o, const void* dout,
                         const float* lse, void* dqkv, float* delta, cudaStream_t st) {
   const int rows = sh.b * sh.s;
+  // 128 threads per CTA (more, smaller CTAs per SM): 28.3B backward 70.7-71.6 -> 68.6 us,
+  // 6.2B -0.5% against 256 (profiles/r02_attn_delta_block_size.jsonl)
+  constexpr int dnt = 128;
   const int blocks = static_cast<int>((static_cast<int64_t>(rows) * sh.a + 255) / 256);
   if (dt == DT_BF16) {
     auto kern = sh.d == 64 ? attn::k_delta<bf16, 64> : sh.d == 96 ? attn::k_delta<bf16, 96>
               : sh.d == 128 ? attn::k_delta<bf16, 128> : attn::k_delta<bf16, 0>;
-    launch(PDL_OPS, kern, blocks, 256, 0, st, static_cast<const bf16*>(o), static_cast<const bf16*>(dout), delta, sh.s,
+    launch(PDL_OPS, kern, static_cast<int>((static_cast<int64_t>(rows) * sh.a + dnt - 1) / dnt), dnt, 0, st, static_cast<const bf16*>(o), static_cast<const bf16*>(dout), delta, sh.s,
            sh.a, sh.d, rows);
   } else {
     launch(PDL_OPS, attn::k_delta<float, 0>, blocks, 256, 0, st, static_cast<const float*>(o),
