@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_attention.py tests/test_gpu_stage.py tests/test_gpu_fullsize.py -q -x -p no:cacheprovider -k "not c4_c5" > gpurun_out/c38_tests.log 2>&1; echo "rc $?" >> gpurun_out/c38_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/c38_smoke.log 2>&1; echo "rc $?" >> gpurun_out/c38_smoke.log
-timeout 300 python scripts/attn_perf.py > gpurun_out/c38_perf.jsonl 2>&1
-tail -2 gpurun_out/c38_tests.log; tail -2 gpurun_out/c38_smoke.log; cat gpurun_out/c38_perf.jsonl
+md5sum paper_2401_10241_b200/libzb.so > gpurun_out/final4_md5.txt
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/final4_gpu_tests.log 2>&1; echo "rc $?" >> gpurun_out/final4_gpu_tests.log
+timeout 900 python bench.py > gpurun_out/final4_bench.log 2>&1; echo "rc $?" >> gpurun_out/final4_bench.log
+tail -3 gpurun_out/final4_gpu_tests.log; tail -c 300 gpurun_out/final4_bench.log
